@@ -1,0 +1,608 @@
+/*
+ * csph_oracle.c -- TEST INFRASTRUCTURE ONLY (see csph_oracle.h).
+ *
+ * A plain, slow, single-threaded implementation of one CSPH-TVD step in the
+ * reading R of DESIGN.md section 3.  Every stage of R is its own loop nest
+ * over the grid with its intermediates materialised, in the paper's kernel
+ * order K1..K8.  No blocking, fusion or reordering.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC
+ * (IEEE binary64, round-to-nearest, no implicit FMA contraction).
+ */
+#include "csph_oracle.h"
+
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define G 3 /* ghost layers: the stencil radius of R */
+
+struct orc {
+  int nx, ny, pw, ph; /* interior size, padded width/height */
+  double h;           /* cell size ("h is cell size") */
+  orc_params p;
+  /* host-side constants of R */
+  double inv_h, inv_2h, cP, cgam, kappa;
+  int wall[4];
+  int have_state;
+  /* state U = (H, Hu, Hv, b) of Eq.6 and W = 1/(1-psi) of Eq.1 */
+  double *H, *Qx, *Qy, *b, *W;
+  /* intermediates (padded) */
+  double *eta, *r, *u, *v, *phix, *phiy, *gam, *Hh, *ut, *vt, *phix2, *phiy2;
+  double *QLx, *QLy, *J0x, *J0y, *J0a;
+  double *FH, *FQx, *FQy, *FJ, *GH, *GQx, *GQy, *GJ;
+  double *Hn, *Qxn, *Qyn, *bn;
+  unsigned char* w;
+  double M[3];
+  double t, last_dt;
+  long long steps;
+};
+
+#define IDX(o, i, j) ((size_t)((j) + G) * (size_t)(o)->pw + (size_t)((i) + G))
+
+/* ---- small pieces of R -------------------------------------------------- */
+
+/* explicit selects, never fmin/fmax */
+static double sel_min(double a, double b) { return (a < b) ? a : b; }
+static double sel_max(double a, double b) { return (a > b) ? a : b; }
+
+/* minmod TVD limiter ("TVD-limiters"; reading #12) */
+double orc_minmod(double a, double b) {
+  if (a > 0.0 && b > 0.0) return sel_min(a, b);
+  if (a < 0.0 && b < 0.0) return sel_max(a, b);
+  return 0.0;
+}
+
+/* pinned x^(-1/3) for x > 0 normal: integer seed from the
+ * exponent bits, then 5 Newton steps y <- y + y*((1 - x*y^3)*(1/3)). */
+double orc_icbrt(double x) {
+  uint64_t bits;
+  memcpy(&bits, &x, 8);
+  uint64_t yb = 0x553F751EB851EC00ull - bits / 3ull;
+  double y;
+  memcpy(&y, &yb, 8);
+  const double third = 1.0 / 3.0;
+  for (int k = 0; k < 5; ++k) {
+    double y3 = (y * y) * y;
+    double e = (1.0 - x * y3) * third;
+    y = y + y * e;
+  }
+  return y;
+}
+
+/* Grass formula Eq.3 with m = 2: J0 = A_J v |v|^2, |J0| = A_J |v|^3 */
+void orc_grass(double A_J, double vx, double vy, double* jx, double* jy, double* jabs) {
+  double s2 = vx * vx + vy * vy;
+  double a = A_J * s2;
+  *jx = a * vx;
+  *jy = a * vy;
+  *jabs = a * sqrt(s2);
+}
+
+/* Eq.2, vector reading #4: J_n = J0_n - C_J |J0| db/dn */
+double orc_slope_flux(double J0n, double J0abs, double C_J, double db_dn) {
+  return J0n - (C_J * J0abs) * db_dn;
+}
+
+/* Eq.5 Shamov gate, reading #6: |v| > v_k  <=>  s2^3 > kappa*H */
+int orc_shamov_gate(double kappa, double s2, double H, double C_Sh) {
+  if (C_Sh == 0.0) return 1;
+  return ((s2 * s2) * s2 > kappa * H) ? 1 : 0;
+}
+
+/* Manning friction coefficient (reading #19): gamma = g n^2 |v| / H^(4/3),
+ * written as (c_gam*s)*(r*H^(-1/3)) with r = 1/H. */
+double orc_gamma(const orc_params* p, double H, double u, double v) {
+  if (!(p->n_manning > 0.0)) return 0.0;
+  double cg = p->g * (p->n_manning * p->n_manning);
+  double s = sqrt(u * u + v * v);
+  double r = 1.0 / H;
+  return (cg * s) * (r * orc_icbrt(H));
+}
+
+/* Face pressure term of K2/K5 (Eq.6 row 2 with reading #1):
+ * P = (c_P * (0.5*(H_L+H_R))) * Delta*, Delta* from the wet/dry table. */
+static double face_force(double cP, double etaL, double HL, int wL,
+                         double etaR, double HR, int wR) {
+  double d = etaR - etaL;
+  double ds;
+  if (wL && wR) ds = d;
+  else if (wL && !wR) ds = sel_min(d, 0.0);
+  else if (!wL && wR) ds = sel_max(d, 0.0);
+  else ds = 0.0;
+  return (cP * (0.5 * (HL + HR))) * ds;
+}
+
+/* K7: hydrostatic step + HLL on F = (Hu, Hu^2, Huv) (Eq.6) */
+void orc_hll_face(double g, double eta_m, double H_m, double un_m, double ut_m,
+                  double eta_p, double H_p, double un_p, double ut_p,
+                  int wL, int wR, double out[3]) {
+  out[0] = 0.0; out[1] = 0.0; out[2] = 0.0;
+  if (!wL && !wR) return;
+  double b_m = eta_m - H_m, b_p = eta_p - H_p;
+  double bs = sel_max(b_m, b_p);
+  double Hs_m = sel_max(0.0, eta_m - bs);
+  double Hs_p = sel_max(0.0, eta_p - bs);
+  int dry_m = !(Hs_m > 0.0), dry_p = !(Hs_p > 0.0);
+  if (dry_m && dry_p) return;
+  double m_m = Hs_m * un_m, m_p = Hs_p * un_p;
+  double FL[3] = {m_m, m_m * un_m, m_m * ut_m};
+  double FR[3] = {m_p, m_p * un_p, m_p * ut_p};
+  double UL[3] = {Hs_m, m_m, Hs_m * ut_m};
+  double UR[3] = {Hs_p, m_p, Hs_p * ut_p};
+  double SL, SR;
+  if (!dry_m && !dry_p) {
+    double c_m = sqrt(g * Hs_m), c_p = sqrt(g * Hs_p);
+    SL = sel_min(un_m - c_m, un_p - c_p);
+    SR = sel_max(un_m + c_m, un_p + c_p);
+  } else if (dry_p) {
+    double c_m = sqrt(g * Hs_m);
+    SL = un_m - c_m;
+    SR = un_m + 2.0 * c_m;
+  } else {
+    double c_p = sqrt(g * Hs_p);
+    SL = un_p - 2.0 * c_p;
+    SR = un_p + c_p;
+  }
+  if (SL >= 0.0) {
+    for (int k = 0; k < 3; ++k) out[k] = FL[k];
+  } else if (SR <= 0.0) {
+    for (int k = 0; k < 3; ++k) out[k] = FR[k];
+  } else {
+    double inv = 1.0 / (SR - SL);
+    double SLSR = SL * SR;
+    for (int k = 0; k < 3; ++k)
+      out[k] = ((SR * FL[k] - SL * FR[k]) + SLSR * (UR[k] - UL[k])) * inv;
+  }
+}
+
+/* ---- lifecycle ------------------------------------------------------------ */
+
+static int valid_params(const orc_params* p) {
+  if (!(p->g > 0.0) || !isfinite(p->g)) return 0;
+  if (!(p->K > 0.0 && p->K < 1.0)) return 0;
+  if (!(p->eps_dry >= 0.0) || !isfinite(p->eps_dry)) return 0;
+  if (!(p->dt_max > 0.0)) return 0;
+  if (!(p->neg_tol >= 0.0)) return 0;
+  if (!(p->n_manning >= 0.0) || !isfinite(p->n_manning)) return 0;
+  if (!(p->A_J >= 0.0) || !isfinite(p->A_J)) return 0;
+  if (p->m_grass != 2) return 0;
+  if (!isfinite(p->C_J)) return 0;
+  if (!(p->C_Sh >= 0.0) || !isfinite(p->C_Sh)) return 0;
+  if (p->C_Sh > 0.0 && !(p->d50 > 0.0)) return 0;
+  if (!isfinite(p->q_plus) || !isfinite(p->q_minus)) return 0;
+  return 1;
+}
+
+orc_t* orc_create(int nx, int ny, double dx, const orc_params* p) {
+  if (nx < 3 || ny < 3 || !(dx > 0.0) || !isfinite(dx) || !p || !valid_params(p)) return NULL;
+  orc_t* o = (orc_t*)calloc(1, sizeof(orc_t));
+  if (!o) return NULL;
+  o->nx = nx; o->ny = ny; o->pw = nx + 2 * G; o->ph = ny + 2 * G;
+  o->h = dx; o->p = *p;
+  o->inv_h = 1.0 / dx;
+  o->inv_2h = 1.0 / (2.0 * dx);
+  o->cP = p->g / (2.0 * dx);
+  o->cgam = p->g * (p->n_manning * p->n_manning);
+  {
+    double c2 = p->C_Sh * p->C_Sh;
+    o->kappa = ((c2 * c2) * c2) * (p->d50 * p->d50);
+  }
+  for (int s = 0; s < 4; ++s) o->wall[s] = 1;
+  size_t n = (size_t)o->pw * (size_t)o->ph;
+  double** arrs[] = {&o->H, &o->Qx, &o->Qy, &o->b, &o->W, &o->eta, &o->r, &o->u, &o->v,
+                     &o->phix, &o->phiy, &o->gam, &o->Hh, &o->ut, &o->vt, &o->phix2,
+                     &o->phiy2, &o->QLx, &o->QLy, &o->J0x, &o->J0y, &o->J0a, &o->FH,
+                     &o->FQx, &o->FQy, &o->FJ, &o->GH, &o->GQx, &o->GQy, &o->GJ,
+                     &o->Hn, &o->Qxn, &o->Qyn, &o->bn};
+  for (size_t k = 0; k < sizeof(arrs) / sizeof(arrs[0]); ++k) {
+    *arrs[k] = (double*)calloc(n, sizeof(double));
+    if (!*arrs[k]) { orc_destroy(o); return NULL; }
+  }
+  o->w = (unsigned char*)calloc(n, 1);
+  if (!o->w) { orc_destroy(o); return NULL; }
+  return o;
+}
+
+void orc_destroy(orc_t* o) {
+  if (!o) return;
+  double* arrs[] = {o->H, o->Qx, o->Qy, o->b, o->W, o->eta, o->r, o->u, o->v, o->phix,
+                    o->phiy, o->gam, o->Hh, o->ut, o->vt, o->phix2, o->phiy2, o->QLx,
+                    o->QLy, o->J0x, o->J0y, o->J0a, o->FH, o->FQx, o->FQy, o->FJ,
+                    o->GH, o->GQx, o->GQy, o->GJ, o->Hn, o->Qxn, o->Qyn, o->bn};
+  for (size_t k = 0; k < sizeof(arrs) / sizeof(arrs[0]); ++k) free(arrs[k]);
+  free(o->w);
+  free(o);
+}
+
+int orc_set_walls(orc_t* o, int xlo, int xhi, int ylo, int yhi) {
+  if (!o) return ORC_EINVAL;
+  o->wall[0] = xlo != 0; o->wall[1] = xhi != 0; o->wall[2] = ylo != 0; o->wall[3] = yhi != 0;
+  return ORC_OK;
+}
+
+/* Solid walls (reading #14): 3-layer mirror ghosts.  H, b, W copied, the
+ * normal momentum negated, the tangential copied.  x-ghosts first on the
+ * interior rows, then y-ghosts over the full padded width (corners = double
+ * mirror). */
+static void mirror_fill(orc_t* o) {
+  int nx = o->nx, ny = o->ny;
+  for (int j = 0; j < ny; ++j) {
+    for (int k = 0; k < G; ++k) {
+      if (o->wall[0]) {
+        size_t d = IDX(o, -1 - k, j), s = IDX(o, k, j);
+        o->H[d] = o->H[s]; o->b[d] = o->b[s]; o->W[d] = o->W[s];
+        o->Qx[d] = -o->Qx[s]; o->Qy[d] = o->Qy[s];
+      }
+      if (o->wall[1]) {
+        size_t d = IDX(o, nx + k, j), s = IDX(o, nx - 1 - k, j);
+        o->H[d] = o->H[s]; o->b[d] = o->b[s]; o->W[d] = o->W[s];
+        o->Qx[d] = -o->Qx[s]; o->Qy[d] = o->Qy[s];
+      }
+    }
+  }
+  for (int i = -G; i < nx + G; ++i) {
+    for (int k = 0; k < G; ++k) {
+      if (o->wall[2]) {
+        size_t d = IDX(o, i, -1 - k), s = IDX(o, i, k);
+        o->H[d] = o->H[s]; o->b[d] = o->b[s]; o->W[d] = o->W[s];
+        o->Qx[d] = o->Qx[s]; o->Qy[d] = -o->Qy[s];
+      }
+      if (o->wall[3]) {
+        size_t d = IDX(o, i, ny + k), s = IDX(o, i, ny - 1 - k);
+        o->H[d] = o->H[s]; o->b[d] = o->b[s]; o->W[d] = o->W[s];
+        o->Qx[d] = o->Qx[s]; o->Qy[d] = -o->Qy[s];
+      }
+    }
+  }
+}
+
+/* Step 9: maxima over the owned wet cells of the state. */
+static void reduce_M(orc_t* o, const double* H, const double* Qx, const double* Qy,
+                     double M[3]) {
+  const orc_params* p = &o->p;
+  double M1 = 0.0, M2 = 0.0, M3 = 0.0;
+  for (int j = 0; j < o->ny; ++j) {
+    for (int i = 0; i < o->nx; ++i) {
+      size_t c = IDX(o, i, j);
+      double Hc = H[c];
+      if (!(Hc > p->eps_dry)) continue;
+      double r = 1.0 / Hc;
+      double u = Qx[c] * r, v = Qy[c] * r;
+      double s2 = u * u + v * v;
+      double a = sqrt(s2);
+      double t1 = s2;
+      double t2 = a + sqrt(p->g * Hc);
+      double t3 = 0.0;
+      if (orc_shamov_gate(o->kappa, s2, Hc, p->C_Sh)) t3 = ((p->A_J * s2) * a) * o->W[c];
+      /* max that lets NaN win */
+      if (!(t1 <= M1)) M1 = t1;
+      if (!(t2 <= M2)) M2 = t2;
+      if (!(t3 <= M3)) M3 = t3;
+    }
+  }
+  M[0] = M1; M[1] = M2; M[2] = M3;
+}
+
+static int finite_all(const double* a, size_t n) {
+  for (size_t k = 0; k < n; ++k)
+    if (!isfinite(a[k])) return 0;
+  return 1;
+}
+
+int orc_set_state(orc_t* o, const double* h, const double* hu, const double* hv,
+                  const double* b, const double* psi) {
+  if (!o || !h || !hu || !hv || !b) return ORC_EINVAL;
+  size_t n = (size_t)o->nx * o->ny;
+  if (!finite_all(h, n) || !finite_all(hu, n) || !finite_all(hv, n) || !finite_all(b, n))
+    return ORC_EINVAL;
+  for (size_t k = 0; k < n; ++k) {
+    if (h[k] < 0.0) return ORC_EINVAL;
+    if (psi && !(psi[k] >= 0.0 && psi[k] < 1.0)) return ORC_EINVAL;
+  }
+  for (int j = 0; j < o->ny; ++j)
+    for (int i = 0; i < o->nx; ++i) {
+      size_t s = (size_t)j * o->nx + i, d = IDX(o, i, j);
+      o->H[d] = h[s]; o->Qx[d] = hu[s]; o->Qy[d] = hv[s]; o->b[d] = b[s];
+      o->W[d] = 1.0 / (1.0 - (psi ? psi[s] : 0.0)); /* Eq.1: W = 1/(1-psi) */
+    }
+  mirror_fill(o);
+  reduce_M(o, o->H, o->Qx, o->Qy, o->M);
+  o->have_state = 1;
+  o->t = 0.0; o->steps = 0; o->last_dt = 0.0;
+  return ORC_OK;
+}
+
+int orc_set_state_padded(orc_t* o, const double* H, const double* Qx, const double* Qy,
+                         const double* b, const double* W) {
+  if (!o || !H || !Qx || !Qy || !b || !W) return ORC_EINVAL;
+  size_t n = (size_t)o->pw * o->ph;
+  memcpy(o->H, H, n * 8); memcpy(o->Qx, Qx, n * 8); memcpy(o->Qy, Qy, n * 8);
+  memcpy(o->b, b, n * 8); memcpy(o->W, W, n * 8);
+  mirror_fill(o);
+  reduce_M(o, o->H, o->Qx, o->Qy, o->M);
+  o->have_state = 1;
+  return ORC_OK;
+}
+
+int orc_get_state(orc_t* o, double* h, double* hu, double* hv, double* b) {
+  if (!o) return ORC_EINVAL;
+  if (!o->have_state) return ORC_ENOSTATE;
+  for (int j = 0; j < o->ny; ++j)
+    for (int i = 0; i < o->nx; ++i) {
+      size_t d = (size_t)j * o->nx + i, s = IDX(o, i, j);
+      if (h) h[d] = o->H[s];
+      if (hu) hu[d] = o->Qx[s];
+      if (hv) hv[d] = o->Qy[s];
+      if (b) b[d] = o->b[s];
+    }
+  return ORC_OK;
+}
+
+int orc_get_state_padded(orc_t* o, double* H, double* Qx, double* Qy, double* b) {
+  if (!o) return ORC_EINVAL;
+  if (!o->have_state) return ORC_ENOSTATE;
+  size_t n = (size_t)o->pw * o->ph;
+  if (H) memcpy(H, o->H, n * 8);
+  if (Qx) memcpy(Qx, o->Qx, n * 8);
+  if (Qy) memcpy(Qy, o->Qy, n * 8);
+  if (b) memcpy(b, o->b, n * 8);
+  return ORC_OK;
+}
+
+int orc_reduce_M(orc_t* o, double M[3]) {
+  if (!o) return ORC_EINVAL;
+  if (!o->have_state) return ORC_ENOSTATE;
+  reduce_M(o, o->H, o->Qx, o->Qy, M);
+  return ORC_OK;
+}
+
+/* Step 0 -- K3, Eq.7, reading #9 */
+int orc_tau_from_M(const orc_t* o, const double M[3], double* tau, int* lim) {
+  if (!isfinite(M[0]) || !isfinite(M[1]) || !isfinite(M[2])) return ORC_ENONFINITE;
+  double h = o->h;
+  double t1 = h / (2.0 * sqrt(M[0]));
+  double t2 = h / M[1];
+  double t3 = (h * h) / (2.0 * M[2]);
+  double m = t1;
+  int l = 0;
+  if (t2 < m) { m = t2; l = 1; }
+  if (t3 < m) { m = t3; l = 2; }
+  double T = o->p.K * m;
+  if (o->p.dt_max < T) { T = o->p.dt_max; l = 3; }
+  if (!isfinite(T)) return ORC_EDRY;
+  *tau = T;
+  if (lim) *lim = l;
+  return ORC_OK;
+}
+
+/* ---- one step of R with a given tau ---------------------------------------- */
+
+int orc_step_tau(orc_t* o, double tau) {
+  if (!o) return ORC_EINVAL;
+  if (!o->have_state) return ORC_ENOSTATE;
+  const orc_params* p = &o->p;
+  const int nx = o->nx, ny = o->ny;
+  const double eps = p->eps_dry;
+  const double theta = 0.5 * tau;
+  const double lam = tau / o->h;
+  const int fric = p->n_manning > 0.0;
+  double *H = o->H, *Qx = o->Qx, *Qy = o->Qy, *b = o->b, *W = o->W;
+  const size_t sx = 1, sy = (size_t)o->pw;
+
+  /* Step 1 -- K1: wet mask, eta, velocities on every cell */
+  for (int j = -G; j < ny + G; ++j)
+    for (int i = -G; i < nx + G; ++i) {
+      size_t c = IDX(o, i, j);
+      o->w[c] = H[c] > eps;
+      o->eta[c] = H[c] + b[c];
+      if (o->w[c]) {
+        o->r[c] = 1.0 / H[c];
+        o->u[c] = Qx[c] * o->r[c];
+        o->v[c] = Qy[c] * o->r[c];
+      } else {
+        o->r[c] = 0.0; o->u[c] = 0.0; o->v[c] = 0.0;
+      }
+    }
+
+  /* Step 2 -- K2: forces at t_n and friction gamma */
+  for (int j = -G + 1; j < ny + G - 1; ++j)
+    for (int i = -G + 1; i < nx + G - 1; ++i) {
+      size_t c = IDX(o, i, j);
+      if (!o->w[c]) { o->phix[c] = 0.0; o->phiy[c] = 0.0; o->gam[c] = 0.0; continue; }
+      size_t e = c + sx, wv = c - sx, nn = c + sy, s = c - sy;
+      double PE = face_force(o->cP, o->eta[c], H[c], o->w[c], o->eta[e], H[e], o->w[e]);
+      double PW = face_force(o->cP, o->eta[wv], H[wv], o->w[wv], o->eta[c], H[c], o->w[c]);
+      double PN = face_force(o->cP, o->eta[c], H[c], o->w[c], o->eta[nn], H[nn], o->w[nn]);
+      double PS = face_force(o->cP, o->eta[s], H[s], o->w[s], o->eta[c], H[c], o->w[c]);
+      o->phix[c] = -(PE + PW);
+      o->phiy[c] = -(PN + PS);
+      if (fric) {
+        double sp = sqrt(o->u[c] * o->u[c] + o->v[c] * o->v[c]);
+        o->gam[c] = (o->cgam * sp) * (o->r[c] * orc_icbrt(H[c]));
+      } else {
+        o->gam[c] = 0.0;
+      }
+    }
+
+  /* Step 3 -- K4: predictor to t_{n+1/2} */
+  for (int j = -G + 1; j < ny + G - 1; ++j)
+    for (int i = -G + 1; i < nx + G - 1; ++i) {
+      size_t c = IDX(o, i, j);
+      if (!o->w[c]) { o->Hh[c] = H[c]; o->ut[c] = 0.0; o->vt[c] = 0.0; continue; }
+      double div = ((o->u[c + sx] - o->u[c - sx]) + (o->v[c + sy] - o->v[c - sy])) * o->inv_2h;
+      o->Hh[c] = H[c] * (1.0 - theta * div);
+      double f = 1.0 / (1.0 + theta * o->gam[c]);
+      o->ut[c] = ((Qx[c] + theta * o->phix[c]) * f) * o->r[c];
+      o->vt[c] = ((Qy[c] + theta * o->phiy[c]) * f) * o->r[c];
+    }
+
+  /* Step 4 -- K5: forces at t_{n+1/2} from eta_half, step-n mask */
+  for (int j = -G + 2; j < ny + G - 2; ++j)
+    for (int i = -G + 2; i < nx + G - 2; ++i) {
+      size_t c = IDX(o, i, j);
+      if (!o->w[c]) { o->phix2[c] = 0.0; o->phiy2[c] = 0.0; continue; }
+      size_t e = c + sx, wv = c - sx, nn = c + sy, s = c - sy;
+      double ec = o->Hh[c] + b[c];
+      double PE = face_force(o->cP, ec, o->Hh[c], 1, o->Hh[e] + b[e], o->Hh[e], o->w[e]);
+      double PW = face_force(o->cP, o->Hh[wv] + b[wv], o->Hh[wv], o->w[wv], ec, o->Hh[c], 1);
+      double PN = face_force(o->cP, ec, o->Hh[c], 1, o->Hh[nn] + b[nn], o->Hh[nn], o->w[nn]);
+      double PS = face_force(o->cP, o->Hh[s] + b[s], o->Hh[s], o->w[s], ec, o->Hh[c], 1);
+      o->phix2[c] = -(PE + PW);
+      o->phiy2[c] = -(PN + PS);
+    }
+
+  /* Step 5 -- K6: corrector momenta Q^L */
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) {
+      size_t c = IDX(o, i, j);
+      if (!o->w[c]) { o->QLx[c] = 0.0; o->QLy[c] = 0.0; continue; }
+      double f = 1.0 / (1.0 + tau * o->gam[c]);
+      o->QLx[c] = (Qx[c] + tau * o->phix2[c]) * f;
+      o->QLy[c] = (Qy[c] + tau * o->phiy2[c]) * f;
+    }
+
+  /* Step 7a: per-cell Grass flux J0 (Eq.3) gated by Shamov (Eq.5) from
+   * (u~, v~, H) */
+  for (int j = -G + 1; j < ny + G - 1; ++j)
+    for (int i = -G + 1; i < nx + G - 1; ++i) {
+      size_t c = IDX(o, i, j);
+      double jx, jy, ja;
+      orc_grass(p->A_J, o->ut[c], o->vt[c], &jx, &jy, &ja);
+      double s2 = o->ut[c] * o->ut[c] + o->vt[c] * o->vt[c];
+      if (orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh)) {
+        o->J0x[c] = jx; o->J0y[c] = jy; o->J0a[c] = ja;
+      } else {
+        o->J0x[c] = 0.0; o->J0y[c] = 0.0; o->J0a[c] = 0.0;
+      }
+    }
+
+  /* Steps 6-7 -- K7: minmod reconstruction of
+   * (eta, H, u_n, u_t), hydrostatic step, HLL, sediment face flux.
+   * x-faces: FH[(j, i)] is the face between cells (i-1, j) and (i, j). */
+  for (int axis = 0; axis < 2; ++axis) {
+    const size_t st = axis == 0 ? sx : sy;
+    const double* un = axis == 0 ? o->ut : o->vt;
+    const double* utn = axis == 0 ? o->vt : o->ut;
+    const double* J0n = axis == 0 ? o->J0x : o->J0y;
+    double* FH = axis == 0 ? o->FH : o->GH;
+    double* FQn = axis == 0 ? o->FQx : o->GQy;
+    double* FQt = axis == 0 ? o->FQy : o->GQx;
+    double* FJ = axis == 0 ? o->FJ : o->GJ;
+    int i_end = axis == 0 ? nx + 1 : nx;
+    int j_end = axis == 0 ? ny : ny + 1;
+    for (int j = 0; j < j_end; ++j)
+      for (int i = 0; i < i_end; ++i) {
+        size_t R = IDX(o, i, j), L = R - st;
+        size_t LL = L - st, RR = R + st;
+        double sL[4], sR[4];
+        const double* q[4] = {o->eta, H, un, utn};
+        for (int k = 0; k < 4; ++k) {
+          sL[k] = orc_minmod(q[k][L] - q[k][LL], q[k][R] - q[k][L]);
+          sR[k] = orc_minmod(q[k][R] - q[k][L], q[k][RR] - q[k][R]);
+        }
+        double qm[4], qp[4];
+        for (int k = 0; k < 4; ++k) {
+          qm[k] = q[k][L] + 0.5 * sL[k];
+          qp[k] = q[k][R] - 0.5 * sR[k];
+        }
+        double F[3];
+        orc_hll_face(p->g, qm[0], qm[1], qm[2], qm[3], qp[0], qp[1], qp[2], qp[3],
+                     o->w[L], o->w[R], F);
+        FH[R] = F[0]; FQn[R] = F[1]; FQt[R] = F[2];
+        /* sediment face flux: donor by sign of u~_n,L + u~_n,R; tie averages */
+        double Jn, Ja;
+        if (!o->w[L] && !o->w[R]) {
+          FJ[R] = 0.0;
+          continue;
+        }
+        double us = un[L] + un[R];
+        if (us > 0.0) { Jn = J0n[L]; Ja = o->J0a[L]; }
+        else if (us < 0.0) { Jn = J0n[R]; Ja = o->J0a[R]; }
+        else { Jn = 0.5 * (J0n[L] + J0n[R]); Ja = 0.5 * (o->J0a[L] + o->J0a[R]); }
+        FJ[R] = orc_slope_flux(Jn, Ja, p->C_J, (b[R] - b[L]) * o->inv_h);
+      }
+  }
+
+  /* Step 8 -- K8 (Eq.1, Eq.6): conservative update */
+  int neg = 0;
+  const double src = p->q_plus - p->q_minus;
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) {
+      size_t c = IDX(o, i, j);
+      size_t e = c + sx, n = c + sy;
+      double dH = (o->FH[e] - o->FH[c]) + (o->GH[n] - o->GH[c]);
+      double dQx = (o->FQx[e] - o->FQx[c]) + (o->GQx[n] - o->GQx[c]);
+      double dQy = (o->FQy[e] - o->FQy[c]) + (o->GQy[n] - o->GQy[c]);
+      double dJ = (o->FJ[e] - o->FJ[c]) + (o->GJ[n] - o->GJ[c]);
+      double Hn = H[c] - lam * dH;
+      double Qxn = o->QLx[c] - lam * dQx;
+      double Qyn = o->QLy[c] - lam * dQy;
+      double bn = (b[c] - (lam * W[c]) * dJ) + (tau * W[c]) * src;
+      if (!(Hn > eps)) { Qxn = 0.0; Qyn = 0.0; }
+      if (Hn < -p->neg_tol) neg = 1;
+      o->Hn[c] = Hn; o->Qxn[c] = Qxn; o->Qyn[c] = Qyn; o->bn[c] = bn;
+    }
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) {
+      size_t c = IDX(o, i, j);
+      H[c] = o->Hn[c]; Qx[c] = o->Qxn[c]; Qy[c] = o->Qyn[c]; b[c] = o->bn[c];
+    }
+  mirror_fill(o);
+
+  /* Step 9: maxima for the next step's Eq.7 */
+  reduce_M(o, H, Qx, Qy, o->M);
+  o->t += tau;
+  o->last_dt = tau;
+  o->steps += 1;
+  return neg ? ORC_ENEGDEPTH : ORC_OK;
+}
+
+int orc_step(orc_t* o, int nsteps, double* dt_log, int* lim_log, int* n_done) {
+  if (!o || nsteps < 0) return ORC_EINVAL;
+  if (!o->have_state) return ORC_ENOSTATE;
+  int k = 0, st = ORC_OK;
+  for (; k < nsteps; ++k) {
+    double tau;
+    int lim;
+    st = orc_tau_from_M(o, o->M, &tau, &lim);
+    if (st != ORC_OK) break;
+    if (dt_log) dt_log[k] = tau;
+    if (lim_log) lim_log[k] = lim;
+    st = orc_step_tau(o, tau);
+    if (st != ORC_OK) { ++k; break; }
+  }
+  if (n_done) *n_done = k;
+  return st;
+}
+
+int orc_get_time(const orc_t* o, double* t, long long* steps, double* last_dt) {
+  if (!o) return ORC_EINVAL;
+  if (t) *t = o->t;
+  if (steps) *steps = o->steps;
+  if (last_dt) *last_dt = o->last_dt;
+  return ORC_OK;
+}
+
+int orc_get_debug(const orc_t* o, const char* name, double* out) {
+  if (!o || !name || !out) return ORC_EINVAL;
+  size_t n = (size_t)o->pw * o->ph;
+  if (strcmp(name, "w") == 0) {
+    for (size_t k = 0; k < n; ++k) out[k] = o->w[k];
+    return ORC_OK;
+  }
+  struct { const char* nm; const double* a; } tab[] = {
+      {"eta", o->eta}, {"u", o->u}, {"v", o->v}, {"phix", o->phix}, {"phiy", o->phiy},
+      {"gam", o->gam}, {"Hh", o->Hh}, {"ut", o->ut}, {"vt", o->vt}, {"phix2", o->phix2},
+      {"phiy2", o->phiy2}, {"QLx", o->QLx}, {"QLy", o->QLy}, {"J0x", o->J0x},
+      {"J0y", o->J0y}, {"J0a", o->J0a}, {"FH", o->FH}, {"FQx", o->FQx}, {"FQy", o->FQy},
+      {"FJ", o->FJ}, {"GH", o->GH}, {"GQx", o->GQx}, {"GQy", o->GQy}, {"GJ", o->GJ},
+      {"W", o->W}};
+  for (size_t k = 0; k < sizeof(tab) / sizeof(tab[0]); ++k)
+    if (strcmp(name, tab[k].nm) == 0) {
+      memcpy(out, tab[k].a, n * 8);
+      return ORC_OK;
+    }
+  return ORC_EINVAL;
+}
