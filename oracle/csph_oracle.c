@@ -101,17 +101,19 @@ double orc_gamma(const orc_params* p, double H, double u, double v) {
   return (cg * s) * (r * orc_icbrt(H));
 }
 
-/* Face pressure term of K2/K5 (Eq.6 row 2 with reading #1):
- * P = (c_P * (0.5*(H_L+H_R))) * Delta*, Delta* from the wet/dry table. */
+/* Face pressure term of K2/K5 (Eq.6 row 2, -gH grad(H+b), reading #1;
+ * DESIGN.md 3.3) in hydrostatic-reconstruction form:
+ *   b* = max(b_L, b_R), H*_s = max(0, eta_s - b*),
+ *   P  = (c_P * (0.5*(H*_L + H*_R))) * (H*_R - H*_L).
+ * The wet flags are not needed: a dry cell whose bed is above the water has
+ * H* = 0 on both sides of the face (a wall), a lower dry cell drives the flow. */
 static double face_force(double cP, double etaL, double HL, int wL,
                          double etaR, double HR, int wR) {
-  double d = etaR - etaL;
-  double ds;
-  if (wL && wR) ds = d;
-  else if (wL && !wR) ds = sel_min(d, 0.0);
-  else if (!wL && wR) ds = sel_max(d, 0.0);
-  else ds = 0.0;
-  return (cP * (0.5 * (HL + HR))) * ds;
+  (void)wL; (void)wR;
+  double bs = sel_max(etaL - HL, etaR - HR);
+  double HsL = sel_max(0.0, etaL - bs);
+  double HsR = sel_max(0.0, etaR - bs);
+  return (cP * (0.5 * (HsL + HsR))) * (HsR - HsL);
 }
 
 /* K7: hydrostatic step + HLL on F = (Hu, Hu^2, Huv) (Eq.6) */

@@ -101,7 +101,7 @@ def fbm(seed: int, P0: int, octaves: int, i: int, j: int) -> float:
 
 
 def random_state(nx: int, ny: int, seed: int, wet_frac: float = 0.7, rough: float = 0.3,
-                 vel: float = 0.8, psi_field: bool = True):
+                 vel: float = 0.8, psi_field: bool = True, film: float = 0.0):
     """Small random state with wet/dry islands (tests only): hash-based, so
     reproducible; values are kept away from branch thresholds only
     statistically."""
@@ -113,4 +113,11 @@ def random_state(nx: int, ny: int, seed: int, wet_frac: float = 0.7, rough: floa
     hu = np.where(h > 0, h * vel * rng.standard_normal((ny, nx)), 0.0)
     hv = np.where(h > 0, h * vel * rng.standard_normal((ny, nx)), 0.0)
     psi = 0.3 + 0.2 * rng.random((ny, nx)) if psi_field else np.full((ny, nx), 0.4)
+    if film > 0.0:
+        # thin films just above eps_dry = 1e-6 with random currents (wet/dry stress)
+        f = rng.random((ny, nx)) < film
+        hf = 1e-6 + 2e-6 * rng.random((ny, nx))
+        h = np.where(f, hf, h)
+        hu = np.where(f, hf * rng.standard_normal((ny, nx)), hu)
+        hv = np.where(f, hf * rng.standard_normal((ny, nx)), hv)
     return h, hu, hv, b, psi

@@ -569,7 +569,7 @@ def test_dry_cells_hold_no_momentum(orc):
     """Type invariant (reading #28): after every step, H <= eps implies
     hu = hv = +0 exactly, including cells that just dried."""
     nx, ny = 40, 32
-    h, hu, hv, b, psi = synth.random_state(nx, ny, seed=17, wet_frac=0.5, vel=2.0)
+    h, hu, hv, b, psi = synth.random_state(nx, ny, seed=17, wet_frac=0.5, vel=2.0, film=0.3)
     o = orc.Oracle(nx, ny, 1.0, orc.Params(n_manning=0.02))
     o.set_state(h, hu, hv, b, psi)
     dried = 0
@@ -583,3 +583,24 @@ def test_dry_cells_hold_no_momentum(orc):
         dried += int(np.sum(dry & (prev > 1e-6)))
         prev = H
     assert dried > 0  # the case really occurs
+
+
+def test_ledge_force_is_hydrostatic(orc):
+    """K2 face force at a bed step (hydrostatic reconstruction):
+    water on a ledge (b=1, H=0.2) above a lower pool (b=0, H=0.5) is pushed
+    over the edge by its own pressure g H^2/2 only, not by the drop height:
+    Phi_x = g 0.2^2/(4h) on both cells of the step face, 0 elsewhere."""
+    nx, ny, k = 12, 3, 6
+    x = np.arange(nx)
+    b = np.where(x < k, 1.0, 0.0)[None, :].repeat(ny, 0)
+    h = np.where(x < k, 0.2, 0.5)[None, :].repeat(ny, 0)
+    z = np.zeros((ny, nx))
+    o = orc.Oracle(nx, ny, 1.0, orc.Params())
+    o.set_state(h, z, z, b)
+    o.step(1)
+    phix = o.debug_interior("phix")
+    f = G * 0.2 ** 2 / 4.0
+    assert rel(phix[1, k - 1], f) < 1e-14 and rel(phix[1, k], f) < 1e-14
+    other = np.delete(phix[1], [k - 1, k])
+    assert np.all(other == 0.0)
+    assert np.all(o.debug_interior("phiy") == 0.0)
