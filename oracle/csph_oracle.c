@@ -103,14 +103,12 @@ double orc_gamma(const orc_params* p, double H, double u, double v) {
 
 /* Face pressure term of K2/K5 (Eq.6 row 2, -gH grad(H+b), reading #1;
  * DESIGN.md 3.3) in hydrostatic-reconstruction form:
- *   b* = max(b_L, b_R), H*_s = max(0, eta_s - b*),
+ *   b* = max(b_L, b_R) (cell beds), H*_s = max(0, eta_s - b*),
  *   P  = (c_P * (0.5*(H*_L + H*_R))) * (H*_R - H*_L).
  * The wet flags are not needed: a dry cell whose bed is above the water has
  * H* = 0 on both sides of the face (a wall), a lower dry cell drives the flow. */
-static double face_force(double cP, double etaL, double HL, int wL,
-                         double etaR, double HR, int wR) {
-  (void)wL; (void)wR;
-  double bs = sel_max(etaL - HL, etaR - HR);
+static double face_force(double cP, double etaL, double bL, double etaR, double bR) {
+  double bs = sel_max(bL, bR);
   double HsL = sel_max(0.0, etaL - bs);
   double HsR = sel_max(0.0, etaR - bs);
   return (cP * (0.5 * (HsL + HsR))) * (HsR - HsL);
@@ -414,10 +412,10 @@ int orc_step_tau(orc_t* o, double tau) {
       size_t c = IDX(o, i, j);
       if (!o->w[c]) { o->phix[c] = 0.0; o->phiy[c] = 0.0; o->gam[c] = 0.0; continue; }
       size_t e = c + sx, wv = c - sx, nn = c + sy, s = c - sy;
-      double PE = face_force(o->cP, o->eta[c], H[c], o->w[c], o->eta[e], H[e], o->w[e]);
-      double PW = face_force(o->cP, o->eta[wv], H[wv], o->w[wv], o->eta[c], H[c], o->w[c]);
-      double PN = face_force(o->cP, o->eta[c], H[c], o->w[c], o->eta[nn], H[nn], o->w[nn]);
-      double PS = face_force(o->cP, o->eta[s], H[s], o->w[s], o->eta[c], H[c], o->w[c]);
+      double PE = face_force(o->cP, o->eta[c], b[c], o->eta[e], b[e]);
+      double PW = face_force(o->cP, o->eta[wv], b[wv], o->eta[c], b[c]);
+      double PN = face_force(o->cP, o->eta[c], b[c], o->eta[nn], b[nn]);
+      double PS = face_force(o->cP, o->eta[s], b[s], o->eta[c], b[c]);
       o->phix[c] = -(PE + PW);
       o->phiy[c] = -(PN + PS);
       if (fric) {
@@ -447,10 +445,10 @@ int orc_step_tau(orc_t* o, double tau) {
       if (!o->w[c]) { o->phix2[c] = 0.0; o->phiy2[c] = 0.0; continue; }
       size_t e = c + sx, wv = c - sx, nn = c + sy, s = c - sy;
       double ec = o->Hh[c] + b[c];
-      double PE = face_force(o->cP, ec, o->Hh[c], 1, o->Hh[e] + b[e], o->Hh[e], o->w[e]);
-      double PW = face_force(o->cP, o->Hh[wv] + b[wv], o->Hh[wv], o->w[wv], ec, o->Hh[c], 1);
-      double PN = face_force(o->cP, ec, o->Hh[c], 1, o->Hh[nn] + b[nn], o->Hh[nn], o->w[nn]);
-      double PS = face_force(o->cP, o->Hh[s] + b[s], o->Hh[s], o->w[s], ec, o->Hh[c], 1);
+      double PE = face_force(o->cP, ec, b[c], o->Hh[e] + b[e], b[e]);
+      double PW = face_force(o->cP, o->Hh[wv] + b[wv], b[wv], ec, b[c]);
+      double PN = face_force(o->cP, ec, b[c], o->Hh[nn] + b[nn], b[nn]);
+      double PS = face_force(o->cP, o->Hh[s] + b[s], b[s], ec, b[c]);
       o->phix2[c] = -(PE + PW);
       o->phiy2[c] = -(PN + PS);
     }
