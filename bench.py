@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""Benchmark of the CSPH-TVD step (BASELINE.json metric: Gcell-updates/s of the fp64
+step at 1/2/4/8 B200, and % of HBM peak).
+
+  python bench.py [--gpus N --steps K --warmup W]            # our CUDA path
+  python bench.py --impl reference [--steps K --warmup W]    # the CPU oracle (reference arm)
+  torchrun --nproc-per-node N bench.py --gpus N ...          # N > 1: row strips over NCCL
+
+Workload: C5, the synthetic river-floodplain flood with sediment
+transport on a 16384 x 16384 grid (268 M cells, ~30 % wet, heterogeneous psi), the
+largest configuration of BASELINE.json that fits one GPU.  N > 1 splits the same grid
+into N row strips (strong scaling).  A "step" is one full CSPH-TVD step (K1..K8 + Eq.7 +
+halo exchange).  Inputs (19 GB of state) are larger than the 126 MB L2, so no flush is
+needed between steps.  Prints one JSON line from rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Gcell-updates/s (fp64 CSPH-TVD step) at 1/2/4/8 B200; % of HBM peak"
+UNIT = "Gcell-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--n", type=int, default=None, help="override the grid size (n x n)")
+    ap.add_argument("--path", choices=["fused", "staged"], default="fused")
+    ap.add_argument("--tile-rows", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=100,
+                    help="steps between host saves in the end-to-end run (P:131: 100-1000)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-crop", type=int, default=2048)
+    ap.add_argument("--cpu-steps", type=int, default=15)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_substr: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(p))
+        for k, v in d.get("kernels", {}).items():
+            if kernel_substr in k:
+                return v
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_baseline(cfg_name, n, crop, steps):
+    """The oracle as it stands, single-threaded, on a centre crop of the workload run as
+    its own walled domain."""
+    import oracle
+    import synth
+    c = synth.config(cfg_name, n)
+    j0 = (c.ny - crop) // 2
+    i0 = (c.nx - crop) // 2
+    f = synth.fill(c, j0, j0 + crop)
+    f = [a[:, i0:i0 + crop].copy() for a in f]
+    o = oracle.Oracle(crop, crop, c.dx, oracle.Params(**c.params))
+    assert o.set_state(*f) == 0
+    t = time.perf_counter()
+    st, dt, _ = o.step(steps)
+    el = time.perf_counter() - t
+    return {"value": crop * crop * len(dt) / el / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{cfg_name} {c.nx}x{c.ny} centre crop {crop}x{crop} as its own walled "
+                      f"domain, {len(dt)} steps, {el:.1f} s, single thread (status {st})"}
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    c = synth.config(a.config, a.n)
+    crop = a.cpu_crop
+    j0 = (c.ny - crop) // 2
+    i0 = (c.nx - crop) // 2
+    f = [x[:, i0:i0 + crop].copy() for x in synth.fill(c, j0, j0 + crop)]
+    o = oracle.Oracle(crop, crop, c.dx, oracle.Params(**c.params))
+    assert o.set_state(*f) == 0
+    o.step(a.warmup)
+    t = time.perf_counter()
+    st, dt, _ = o.step(a.steps)
+    el = time.perf_counter() - t
+    v = crop * crop * len(dt) / el / 1e9
+    sample = (f"each step = one oracle step on the {crop}x{crop} centre crop of {a.config} "
+              f"{c.nx}x{c.ny} (own walled domain), single thread")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": el / max(len(dt), 1) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{a.config} crop {crop}x{crop}", "grid": [crop, crop]},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2103_15196_b200 import csph
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = synth.config(a.config, a.n)
+    path = csph.CSPH_PATH_FUSED if a.path == "fused" else csph.CSPH_PATH_STAGED
+    p = csph.params_from(c.params, path=path, device=local, tile_rows=a.tile_rows)
+    j0, j1 = csph.csph_strip_rows(c.ny, world, rank)
+    wa, wb = max(0, j0 - 3), min(c.ny, j1 + 3)
+    fields = synth.fill(c, wa, wb)
+    wet_local = float(np.count_nonzero(fields[0][j0 - wa:j1 - wa] > 1e-6))
+    if world > 1:
+        idt = torch.zeros(csph.csph_nccl_id_bytes(), dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(csph.csph_make_nccl_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        g = csph.csph_create_dist(c.nx, c.ny, c.dx, p, rank, world, local,
+                                  bytes(idt.cpu().numpy().tobytes()))
+    else:
+        g = csph.csph_create(c.nx, c.ny, c.dx, p)
+    stream = torch.cuda.current_stream()
+    g.set_stream(stream.cuda_stream)
+    g.set_state_rows(wa, wb, *fields)
+    psi_field = not np.all(fields[4] == fields[4].flat[0])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- warm-up, then exactly K timed steps ----
+    g.step(a.warmup)
+    torch.cuda.synchronize()
+    barrier()
+    g.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(stream)
+        g.step(a.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = g.last_launch_count()
+    kern_ms, kern_steps = g.get_profile()
+    g.profile(False)
+    cells = c.nx * c.ny
+    value = cells * a.steps / (ms / 1e3) / 1e9
+    t_sim, steps_done, _ = g.get_time()
+    dtl, liml = g.get_dt_log(min(steps_done, 100000))
+    wet = sum_over_ranks(wet_local) / cells
+
+    # ---- roofline of the dominant kernel (the fused step kernel) ----
+    peak, peak_src = peaks()
+    bpc = 72 if psi_field else 64  # algorithmic bytes per cell-update
+    own_cells = c.nx * (j1 - j0)
+    kern_ms_per = kern_ms / max(kern_steps, 1)
+    achieved = bpc * own_cells / (kern_ms_per / 1e3) / 1e9
+    tr = ncu_traffic("fused_step_kernel" if path == csph.CSPH_PATH_FUSED else "k7_fluxes")
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": (tr or {}).get("dram_bytes_per_launch"),
+            "kernel": "fused_step_kernel" if path == csph.CSPH_PATH_FUSED else "staged K1..K8",
+            "algorithmic_bytes_per_cell": bpc, "kernel_ms_per_launch": kern_ms_per,
+            "kernel_share_of_step": kern_ms_per / (ms / a.steps), "peak_source": peak_src}
+    fp64 = None
+    if tr and tr.get("fp64_inst_per_launch"):
+        # fp64 pipe: 64 DFMA lanes/clk/SM x 148 SMs at the sampled SM clock
+        inst_per_cell = tr["fp64_inst_per_launch"] / own_cells
+        fp64 = {"bound": "alu", "unit": "fp64 thread-inst/s",
+                "inst_per_cell": inst_per_cell,
+                "achieved": tr["fp64_inst_per_launch"] / (kern_ms_per / 1e3),
+                "pipe_active_pct": tr.get("fp64_pipe_pct")}
+
+    # ---- end to end through the public API: host (pinned) -> device -> host ----
+    e2e = None
+    if not a.no_e2e:
+        pin = [torch.from_numpy(x).pin_memory() for x in fields]
+        outp = [torch.empty((j1 - j0, c.nx), dtype=torch.float64).pin_memory() for _ in range(4)]
+        pin_np = [x.numpy() for x in pin]
+        E = a.e2e_steps
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        g.set_state_rows(wa, wb, *pin_np)
+        g.step(E)
+        res = csph.lib().csph_get_state_rows(g.h, j0, j1, *[csph._p(x.numpy()) for x in outp])
+        f1.record(stream)
+        torch.cuda.synchronize()
+        host_s = time.perf_counter() - t0
+        barrier()
+        assert res == 0
+        ems = max_over_ranks(max(f0.elapsed_time(f1), host_s * 1e3))
+        h2d = sum_over_ranks(5 * 8 * fields[0].size) / E
+        d2h = sum_over_ranks(4 * 8 * c.nx * (j1 - j0)) / E
+        e2e = {"value": cells * E / (ems / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "how": f"csph_set_state_rows(pinned host) + csph_step({E}) + "
+                      f"csph_get_state_rows(pinned host) per save interval (P:131)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(a.config, a.n, min(a.cpu_crop, c.nx, c.ny), a.cpu_steps)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"{a.config} river-floodplain flood + sediment transport"
+                            if a.config == "C5" else a.config,
+                "grid": [c.nx, c.ny], "cells": cells, "dx_m": c.dx, "wet_fraction": wet,
+                "psi": "field" if psi_field else "uniform", "physics": c.params,
+                "path": a.path, "parallelism": f"row strips x{world} (NCCL halos + allreduce)"
+                if world > 1 else "single GPU",
+                "l2": "state (>= 19 GB) larger than the 126 MB L2; no flush needed",
+                "tau_mean": float(np.mean(dtl)) if len(dtl) else None,
+                "limiter_hist": np.bincount(liml, minlength=4).tolist() if len(liml) else None,
+            },
+            "roofline": roof,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        if fp64:
+            line["roofline_fp64"] = fp64
+        print(json.dumps(line), flush=True)
+    g.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus and world > 1:
+        a.gpus = world
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if a.n is None and a.config == "C5":
+        a.n = 16384
+    run_ours(a, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

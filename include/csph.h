@@ -1,0 +1,165 @@
+/*
+ * csph.h -- C-ABI of the B200-native CSPH-TVD step (arXiv 2103.15196).
+ *
+ * The library computes the per-timestep CSPH-TVD update of the coupled
+ * Saint-Venant + Exner system (Eq.6, with the Exner
+ * equation Eq.1) on a 2D structured grid, in the discrete
+ * reading R of DESIGN.md section 3, entirely in CUDA kernels for sm_100a:
+ *   K1 wet mask, K2 forces at t_n (:226), K3 timestep
+ *   Eq.7 (:114-119, :228), K4 predictor (:230), K5 forces at t_{n+1/2} (:232),
+ *   K6 corrector (:234), K7 face fluxes: minmod reconstruction + HLL in x and
+ *   y (:236, :261-263) with the bedload flux Eqs.2,3,5 (:54-73), K8 update
+ *   (:238).
+ *
+ * Conventions
+ *  - Host arrays are fp64, row-major [ny][nx] (x fastest, index j*nx + i),
+ *    owned by the caller, read or written only during the call (synchronous
+ *    copies).  The handle owns all device memory, streams, graphs and NCCL
+ *    communicators; csph_destroy frees them.  A handle is not thread-safe.
+ *  - State U = (H, Hu, Hv, b) of Eq.6: h = water depth [m],
+ *    hu, hv = momenta [m^2/s], b = bed elevation [m]; psi = bed porosity of
+ *    Eq.1 (0 <= psi < 1), may be NULL (psi = 0).
+ *  - Boundaries: solid reflective walls on the four global edges (DESIGN.md
+ *    reading #14).
+ *  - Every function returns 0 (CSPH_OK) or a negative CSPH_E* code; the
+ *    thread-local csph_last_error() describes the last failure.
+ *  - There is no CPU fallback: with no CUDA device every call that needs one
+ *    fails with CSPH_ECUDA.
+ */
+#ifndef CSPH_H
+#define CSPH_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSPH_OK          0
+#define CSPH_EINVAL     -1  /* bad argument, NaN/Inf or negative depth input, psi not in [0,1) */
+#define CSPH_ENOSTATE   -2  /* step/get before set_state */
+#define CSPH_ENOMEM     -3  /* device allocation failed */
+#define CSPH_ECUDA      -4  /* CUDA runtime error (message in csph_last_error) */
+#define CSPH_ENCCL      -5  /* NCCL error */
+#define CSPH_ENEGDEPTH  -6  /* H' < -neg_tol after a step; the state after that step is kept */
+#define CSPH_ENONFINITE -7  /* a maximum of Eq.7 is NaN or Inf */
+#define CSPH_EDRY       -8  /* no wet cell and dt_max = +inf: Eq.7 gives no finite tau */
+
+#define CSPH_PATH_FUSED  0  /* one y-marching kernel per step (default) */
+#define CSPH_PATH_STAGED 1  /* the paper's kernel split K1..K8, intermediates in HBM */
+
+typedef struct csph csph_t;
+
+typedef struct {
+  double g;          /* gravity [m/s^2], default 9.81 */
+  double K;          /* Courant number of Eq.7, 0 < K < 1, default 0.25 (reading #13) */
+  double eps_dry;    /* a cell is wet iff h > eps_dry ("H>Eps"), default 1e-6 m */
+  double dt_max;     /* cap on tau, default +INF */
+  double neg_tol;    /* h' < -neg_tol -> CSPH_ENEGDEPTH, default 1e-12 m */
+  double n_manning;  /* Manning n_M [s m^-1/3]; 0 disables friction */
+  double A_J;        /* Grass coefficient of Eq.3; 0 disables transport */
+  int    m_grass;    /* Grass exponent; this build implements 2 */
+  double C_J;        /* Eq.2 slope coefficient (1.5..2.3, up to 5) */
+  double C_Sh;       /* Eq.5 Shamov constant; 0 disables the gate */
+  double d50;        /* Eq.5 median grain size [m] (> 0 when C_Sh > 0) */
+  double q_plus;     /* Eq.1 deposition source [m/s], default 0 */
+  double q_minus;    /* Eq.1 erosion drain [m/s], default 0 */
+  int    precision;  /* 64 (fp64; the only mode of this build) */
+  int    device;     /* CUDA ordinal for csph_create (single-process use) */
+  int    path;       /* CSPH_PATH_FUSED (default) or CSPH_PATH_STAGED */
+  int    tile_rows;  /* fused path: rows marched per CTA (0 = auto) */
+} csph_params;
+
+/* Fill *p with the defaults above. */
+void        csph_default_params(csph_params* p);
+
+/* One grid of nx x ny cells of size dx [m] on one GPU (p->device).
+ * Returns NULL on error (nx or ny < 3, dx <= 0, bad params, no CUDA device,
+ * allocation failure) -> csph_last_error(). */
+csph_t*     csph_create(int nx, int ny, double dx, const csph_params* p);
+
+/* Upload the full state (global arrays [ny][nx]); computes W = 1/(1-psi),
+ * the wall ghosts and the Eq.7 maxima of the initial state.  Validates
+ * inputs: CSPH_EINVAL on NaN/Inf, h < 0 or psi outside [0,1).  In a
+ * distributed handle each rank copies its own strip plus halo rows. */
+int         csph_set_state(csph_t*, const double* h, const double* hu, const double* hv,
+                           const double* b, const double* psi);
+
+/* As csph_set_state, but the arrays hold only global rows [j_begin, j_end)
+ * ([j_end-j_begin][nx]); they must cover this handle's owned rows and the 3
+ * halo rows on each strip side that has a neighbour.  Lets each rank of a
+ * distributed run generate only its own strip. */
+int         csph_set_state_rows(csph_t*, int j_begin, int j_end, const double* h,
+                                const double* hu, const double* hv, const double* b,
+                                const double* psi);
+
+/* Advance exactly nsteps CSPH-TVD steps, each with its own Eq.7 tau computed
+ * on the device.  No host synchronisation inside the call except one status
+ * readback at its end.  On CSPH_ENEGDEPTH/ENONFINITE/EDRY the steps up to the
+ * failing one are done (see csph_get_time) and later calls return the same code. */
+int         csph_step(csph_t*, int nsteps);
+
+/* Download the state into global-layout arrays [ny][nx] (any may be NULL).
+ * A distributed handle writes only its owned rows. */
+int         csph_get_state(csph_t*, double* h, double* hu, double* hv, double* b);
+
+/* Download global rows [j_begin, j_end) that this handle owns into
+ * [j_end-j_begin][nx] arrays. */
+int         csph_get_state_rows(csph_t*, int j_begin, int j_end, double* h, double* hu,
+                                double* hv, double* b);
+
+/* Simulated time t = sum of tau, steps done, last tau. */
+int         csph_get_time(csph_t*, double* t, long long* steps_done, double* last_dt);
+
+/* Copy the last min(cap, steps done) entries of the device dt log (tau of
+ * each step, in order) and the Eq.7 limiter of each (0: h/(2 v_p),
+ * 1: h/v_s, 2: h^2/(2D), 3: dt_max); *n = entries copied. */
+int         csph_get_dt_log(csph_t*, double* dt, int* limiter, int cap, int* n);
+
+/* Eq.7 maxima (M1 = max |v|^2, M2 = max(|v| + sqrt(gH)), M3 = max |J0|/(1-psi))
+ * of the current state (after the allreduce in a distributed handle). */
+int         csph_get_maxima(csph_t*, double M[3]);
+
+/* Use the caller's cudaStream_t (e.g. torch's current stream) for all work. */
+int         csph_set_stream(csph_t*, void* cuda_stream);
+
+/* Rows [j0, j1) owned by `rank` of `nranks` in the row-strip partition of ny
+ * rows ("Ny_dev"): the first ny % nranks ranks get one extra row.
+ * Host-only; CSPH_EINVAL if a strip would have fewer than 3 rows. */
+int         csph_strip_rows(int ny, int nranks, int rank, int* j0, int* j1);
+
+void        csph_destroy(csph_t*);
+const char* csph_strerror(int code);
+const char* csph_last_error(void);
+
+/* ---- multi-GPU: one process per GPU, row strips, NCCL over NVLink ------- */
+/* Rank 0 makes the NCCL unique id; the harness broadcasts it (e.g. through
+ * torch.distributed) and every rank calls csph_create_dist with it.  Halo
+ * rows (3 per side x 4 fields) go by ncclSend/ncclRecv to ranks r-1, r+1
+ * (no wrap-around, reading #18) and the Eq.7 maxima by ncclAllReduce(max). */
+int         csph_nccl_id_bytes(void);
+int         csph_make_nccl_id(void* out);
+csph_t*     csph_create_dist(int nx, int ny, double dx, const csph_params* p,
+                             int rank, int nranks, int local_device, const void* nccl_id);
+
+/* Single-process row-strip decomposition: nstrips strips on the devices
+ * listed in `devices` (strips may share a device), halos copied with
+ * cudaMemcpyPeerAsync and the maxima combined on the first device.  The same
+ * strip kernels and halo layout as csph_create_dist (PAPER.md:198-218's
+ * one-host-thread-drives-all-GPUs arrangement). */
+csph_t*     csph_create_multi(int nx, int ny, double dx, const csph_params* p,
+                              int nstrips, const int* devices);
+
+/* Kernel timing (bench): when enabled, csph_step records CUDA events on the
+ * handle's stream around each step's main kernel(s) (the fused step kernel, or
+ * K1..K8 of the staged path) and accumulates their device time. */
+int         csph_profile(csph_t*, int enable);
+/* Accumulated main-kernel device time [ms] and number of steps timed since
+ * profiling was enabled. */
+int         csph_get_profile(csph_t*, double* main_kernel_ms, long long* steps_timed);
+
+/* Number of kernel launches the last csph_step issued (for the bench). */
+long long   csph_last_launch_count(csph_t*);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSPH_H */

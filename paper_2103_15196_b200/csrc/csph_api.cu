@@ -1,0 +1,994 @@
+// csph_api.cu -- the C-ABI of include/csph.h: handle lifecycle, HBM layout,
+// set/get state, the per-step control kernel (Eq.7 on the device), wall ghosts,
+// and the row-strip decomposition over NCCL (one process per GPU) or over
+// cudaMemcpyPeer (one process driving several strips).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/csph.h"
+#include "csph_launch.h"
+
+using namespace ck;
+
+// ---------------------------------------------------------------- errors
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(CSPH_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                           \
+  } while (0)
+
+// ---------------------------------------------------------------- NCCL (lazy)
+
+namespace {
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+};
+NcclApi g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.ok) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    fail(CSPH_ENCCL, "cannot load libnccl.so.2: %s", dlerror());
+    return false;
+  }
+#define SYM(field, name)                                                \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
+  if (!g_nccl.field) {                                                  \
+    fail(CSPH_ENCCL, "libnccl lacks %s", name);                         \
+    return false;                                                       \
+  }
+  SYM(GetUniqueId, "ncclGetUniqueId");
+  SYM(CommInitRank, "ncclCommInitRank");
+  SYM(CommDestroy, "ncclCommDestroy");
+  SYM(Send, "ncclSend");
+  SYM(Recv, "ncclRecv");
+  SYM(AllReduce, "ncclAllReduce");
+  SYM(GroupStart, "ncclGroupStart");
+  SYM(GroupEnd, "ncclGroupEnd");
+  SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+  g_nccl.ok = true;
+  return true;
+}
+}  // namespace
+
+#define NK(call)                                                                    \
+  do {                                                                              \
+    ncclResult_t r_ = (call);                                                       \
+    if (r_ != ncclSuccess)                                                          \
+      return fail(CSPH_ENCCL, "%s: %s", #call, g_nccl.GetErrorString(r_));          \
+  } while (0)
+
+// ---------------------------------------------------------------- handle
+
+namespace {
+
+struct Strip {
+  int dev = 0;
+  int gj0 = 0;           // global row of the first owned row
+  StripView v{};
+  Scratch scr{};
+  bool has_scr = false;
+  Ctrl* ctrl = nullptr;              // device
+  unsigned long long* gM = nullptr;  // device accumulator [4]
+  double* Mlast = nullptr;           // device [4]
+  double* dtlog = nullptr;           // device [LOGCAP]
+  int* limlog = nullptr;             // device [LOGCAP]
+  int* dflags = nullptr;             // device validation flags
+  double* Wbuf = nullptr;            // device psi -> W field (when psi varies)
+  cudaStream_t st = nullptr;
+  bool own_stream = true;
+  cudaEvent_t ev = nullptr;
+  std::vector<void*> allocs;
+};
+
+enum Mode { SINGLE = 0, DIST = 1, MULTI = 2 };
+
+}  // namespace
+
+struct csph {
+  int nx = 0, ny = 0;
+  double dx = 1.0;
+  csph_params p{};
+  Phys P{};
+  Mode mode = SINGLE;
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  std::vector<Strip> s;
+  bool have_state = false;
+  int host_parity = 0;  // buffer the next step reads (as launched)
+  long long launches = 0;
+  unsigned long long* gather = nullptr;  // MULTI: [nstrips*4] on strip 0's device
+  bool profiling = false;
+  std::vector<cudaEvent_t> evs;  // pairs around the main kernel of each step (strip 0)
+  double prof_ms = 0.0;
+  long long prof_steps = 0;
+};
+
+// ---------------------------------------------------------------- kernels
+
+namespace {
+
+constexpr int kStatusFlagNeg = 1;
+
+__global__ void ctrl_kernel(Ctrl* C, unsigned long long* gM, double* Mlast, double* dtlog,
+                            int* limlog, Phys P, int advance) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (advance) {
+    if (C->status == 0) {
+      C->parity ^= 1;
+      C->step += 1;
+      C->t += C->tau;
+      if (C->flags & kStatusFlagNeg) C->status = CSPH_ENEGDEPTH;
+    }
+  }
+  double M[3];
+  for (int k = 0; k < 3; ++k) {
+    M[k] = __longlong_as_double((long long)gM[k]);
+    Mlast[k] = M[k];
+    gM[k] = 0ull;
+  }
+  if (C->status) return;
+  if (!isfinite(M[0]) || !isfinite(M[1]) || !isfinite(M[2])) {
+    C->status = CSPH_ENONFINITE;
+    return;
+  }
+  // Step 0 -- K3, Eq.7
+  double h = P.h;
+  double t1 = h / (2.0 * sqrt(M[0]));
+  double t2 = h / M[1];
+  double t3 = (h * h) / (2.0 * M[2]);
+  double m = t1;
+  int lim = 0;
+  if (t2 < m) { m = t2; lim = 1; }
+  if (t3 < m) { m = t3; lim = 2; }
+  double tau = P.K * m;
+  if (P.dt_max < tau) { tau = P.dt_max; lim = 3; }
+  if (!isfinite(tau)) {
+    C->status = CSPH_EDRY;
+    return;
+  }
+  C->tau = tau;
+  C->lim = lim;
+  long long k = C->step % LOGCAP;
+  dtlog[k] = tau;
+  limlog[k] = lim;
+}
+
+// Wall ghosts of buffer (parity ^ flip): x-ghosts on owned rows, y-ghosts on
+// wall sides (full padded width, so corners are double mirrors).
+__global__ void mirror_kernel(StripView S, const Ctrl* C, int flip) {
+  const int q = C->parity ^ flip;
+  if (flip && C->status) return;  // a skipped step leaves the next buffer alone
+  double *H = S.H[q], *Qx = S.Qx[q], *Qy = S.Qy[q], *b = S.b[q];
+  const int nx = S.nx, ny = S.ny;
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  // phase 1: x-ghosts of owned rows (3 per side per row)
+  if (t < ny * 6) {
+    int j = t / 6, k = t % 6;
+    int gi, si;
+    if (k < 3) { gi = -1 - k; si = k; }
+    else { gi = nx + (k - 3); si = nx - 1 - (k - 3); }
+    size_t d = off(S.pitch, gi, j), s = off(S.pitch, si, j);
+    H[d] = H[s]; b[d] = b[s]; Qx[d] = -Qx[s]; Qy[d] = Qy[s];
+  }
+}
+
+__global__ void mirror_y_kernel(StripView S, const Ctrl* C, int flip) {
+  const int q = C->parity ^ flip;
+  if (flip && C->status) return;
+  double *H = S.H[q], *Qx = S.Qx[q], *Qy = S.Qy[q], *b = S.b[q];
+  const int nx = S.nx, ny = S.ny;
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int w = nx + 6;
+  if (t >= w * 6) return;
+  int i = t % w - 3, k = t / w;  // k 0..2: low side, 3..5: high side
+  int gj, sj;
+  if (k < 3) {
+    if (!S.wall_lo) return;
+    gj = -1 - k; sj = k;
+  } else {
+    if (!S.wall_hi) return;
+    gj = ny + (k - 3); sj = ny - 1 - (k - 3);
+  }
+  size_t d = off(S.pitch, i, gj), s = off(S.pitch, i, sj);
+  H[d] = H[s]; b[d] = b[s]; Qx[d] = Qx[s]; Qy[d] = -Qy[s];
+}
+
+__global__ void w_from_psi_kernel(double* W, const double* psi, size_t n) {  // in place ok
+  size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) W[k] = 1.0 / (1.0 - psi[k]);
+}
+
+// Step 9 on a freshly set state: maxima over owned wet cells of buffer `parity`.
+__global__ void maxima_kernel(StripView S, const Ctrl* C, Phys P, unsigned long long* gM) {
+  const int p = C->parity;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int j = blockIdx.y * blockDim.y + threadIdx.y;
+  unsigned long long m0 = 0, m1 = 0, m2 = 0;
+  if (i < S.nx && j < S.ny) {
+    size_t c = off(S.pitch, i, j);
+    double H = S.H[p][c];
+    if (H > P.eps) {
+      double t1, t2, t3;
+      dt_terms(P, H, S.Qx[p][c], S.Qy[p][c], S.W ? S.W[c] : S.Wc, t1, t2, t3);
+      m0 = dbits(t1); m1 = dbits(t2); m2 = dbits(t3);
+    }
+  }
+  block_max3_atomic<8>(m0, m1, m2, gM);
+}
+
+__global__ void max_gather_kernel(unsigned long long* dst, const unsigned long long* src,
+                                  int n) {
+  if (threadIdx.x < 3) {
+    unsigned long long m = 0;
+    for (int k = 0; k < n; ++k) {
+      unsigned long long v = src[4 * k + threadIdx.x];
+      m = v > m ? v : m;
+    }
+    dst[threadIdx.x] = m;
+  }
+}
+
+__global__ void init_ctrl_kernel(Ctrl* C) {
+  C->tau = 0.0; C->t = 0.0; C->step = 0; C->lim = -1; C->status = 0; C->parity = 0;
+  C->flags = 0;
+}
+
+__global__ void clear_flags_kernel(Ctrl* C) { C->flags = 0; }
+
+}  // namespace
+
+namespace ck {
+void launch_mirror(const StripView& S, const Ctrl* C, int flip, cudaStream_t st,
+                   long long* nlaunch) {
+  int n1 = S.ny * 6;
+  mirror_kernel<<<(n1 + 255) / 256, 256, 0, st>>>(S, C, flip);
+  int n2 = (S.nx + 6) * 6;
+  mirror_y_kernel<<<(n2 + 255) / 256, 256, 0, st>>>(S, C, flip);
+  *nlaunch += 2;
+}
+}  // namespace ck
+
+// ---------------------------------------------------------------- helpers
+
+static Phys make_phys(double dx, const csph_params& p) {
+  Phys P{};
+  P.g = p.g;
+  P.eps = p.eps_dry;
+  P.neg_tol = p.neg_tol;
+  P.A_J = p.A_J;
+  P.C_J = p.C_J;
+  P.C_Sh = p.C_Sh;
+  double c2 = p.C_Sh * p.C_Sh;
+  P.kappa = ((c2 * c2) * c2) * (p.d50 * p.d50);
+  P.cP = p.g / (2.0 * dx);
+  P.cgam = p.g * (p.n_manning * p.n_manning);
+  P.inv_h = 1.0 / dx;
+  P.inv_2h = 1.0 / (2.0 * dx);
+  P.h = dx;
+  P.K = p.K;
+  P.dt_max = p.dt_max;
+  P.src = p.q_plus - p.q_minus;
+  P.fric = p.n_manning > 0.0;
+  P.transport = p.A_J > 0.0;
+  return P;
+}
+
+static int check_params(int nx, int ny, double dx, const csph_params* p) {
+  if (!p) return fail(CSPH_EINVAL, "params is NULL");
+  if (nx < 3 || ny < 3) return fail(CSPH_EINVAL, "nx, ny must be >= 3 (got %d, %d)", nx, ny);
+  if (!(dx > 0.0) || !std::isfinite(dx)) return fail(CSPH_EINVAL, "dx must be > 0");
+  if (!(p->g > 0.0) || !std::isfinite(p->g)) return fail(CSPH_EINVAL, "g must be > 0");
+  if (!(p->K > 0.0 && p->K < 1.0)) return fail(CSPH_EINVAL, "K must be in (0,1)");
+  if (!(p->eps_dry >= 0.0) || !std::isfinite(p->eps_dry)) return fail(CSPH_EINVAL, "eps_dry");
+  if (!(p->dt_max > 0.0)) return fail(CSPH_EINVAL, "dt_max must be > 0");
+  if (!(p->neg_tol >= 0.0)) return fail(CSPH_EINVAL, "neg_tol must be >= 0");
+  if (!(p->n_manning >= 0.0) || !std::isfinite(p->n_manning)) return fail(CSPH_EINVAL, "n_manning");
+  if (!(p->A_J >= 0.0) || !std::isfinite(p->A_J)) return fail(CSPH_EINVAL, "A_J");
+  if (p->m_grass != 2) return fail(CSPH_EINVAL, "m_grass must be 2 in the fp64 hot path");
+  if (!std::isfinite(p->C_J)) return fail(CSPH_EINVAL, "C_J");
+  if (!(p->C_Sh >= 0.0) || !std::isfinite(p->C_Sh)) return fail(CSPH_EINVAL, "C_Sh");
+  if (p->C_Sh > 0.0 && !(p->d50 > 0.0)) return fail(CSPH_EINVAL, "d50 must be > 0 when C_Sh > 0");
+  if (!std::isfinite(p->q_plus) || !std::isfinite(p->q_minus)) return fail(CSPH_EINVAL, "q_plus/q_minus");
+  if (p->precision != 64) return fail(CSPH_EINVAL, "precision must be 64");
+  if (p->path != CSPH_PATH_FUSED && p->path != CSPH_PATH_STAGED) return fail(CSPH_EINVAL, "path");
+  return CSPH_OK;
+}
+
+static int dalloc(Strip& s, void** ptr, size_t bytes) {
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) {
+    *ptr = nullptr;
+    return fail(CSPH_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+  }
+  s.allocs.push_back(*ptr);
+  return CSPH_OK;
+}
+
+static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged) {
+  s.dev = dev;
+  s.gj0 = gj0;
+  CK(cudaSetDevice(dev));
+  StripView& v = s.v;
+  v.nx = H->nx;
+  v.ny = rows;
+  v.pitch = ((H->nx + GX + 3) + 31) / 32 * 32;
+  v.wall_lo = gj0 == 0;
+  v.wall_hi = gj0 + rows == H->ny;
+  v.W = nullptr;
+  v.Wc = 1.0;
+  size_t n = (size_t)(rows + 2 * GY) * v.pitch;
+  int st;
+  for (int k = 0; k < 2; ++k) {
+    if ((st = dalloc(s, (void**)&v.H[k], n * 8))) return st;
+    if ((st = dalloc(s, (void**)&v.Qx[k], n * 8))) return st;
+    if ((st = dalloc(s, (void**)&v.Qy[k], n * 8))) return st;
+    if ((st = dalloc(s, (void**)&v.b[k], n * 8))) return st;
+    CK(cudaMemset(v.H[k], 0, n * 8));
+    CK(cudaMemset(v.Qx[k], 0, n * 8));
+    CK(cudaMemset(v.Qy[k], 0, n * 8));
+    CK(cudaMemset(v.b[k], 0, n * 8));
+  }
+  if ((st = dalloc(s, (void**)&s.ctrl, sizeof(Ctrl)))) return st;
+  if ((st = dalloc(s, (void**)&s.gM, 4 * sizeof(unsigned long long)))) return st;
+  if ((st = dalloc(s, (void**)&s.Mlast, 4 * sizeof(double)))) return st;
+  if ((st = dalloc(s, (void**)&s.dtlog, LOGCAP * sizeof(double)))) return st;
+  if ((st = dalloc(s, (void**)&s.limlog, LOGCAP * sizeof(int)))) return st;
+  if ((st = dalloc(s, (void**)&s.dflags, 4 * sizeof(int)))) return st;
+  CK(cudaMemset(s.gM, 0, 4 * sizeof(unsigned long long)));
+  CK(cudaMemset(s.Mlast, 0, 4 * sizeof(double)));
+  if (staged) {
+    Scratch& T = s.scr;
+    double** arr[] = {&T.eta, &T.r, &T.u, &T.v, &T.phix, &T.phiy, &T.gam, &T.Hh, &T.ut,
+                      &T.vt, &T.phix2, &T.phiy2, &T.QLx, &T.QLy, &T.J0x, &T.J0y, &T.J0a,
+                      &T.FH, &T.FQx, &T.FQy, &T.FJ, &T.GH, &T.GQx, &T.GQy, &T.GJ};
+    for (auto a : arr) {
+      if ((st = dalloc(s, (void**)a, n * 8))) return st;
+      CK(cudaMemset(*a, 0, n * 8));
+    }
+    if ((st = dalloc(s, (void**)&T.w, n))) return st;
+    CK(cudaMemset(T.w, 0, n));
+    s.has_scr = true;
+  }
+  CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+  s.own_stream = true;
+  CK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+  init_ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s.st));
+  return CSPH_OK;
+}
+
+static void strip_free(Strip& s) {
+  cudaSetDevice(s.dev);
+  if (s.st) cudaStreamSynchronize(s.st);
+  for (void* p : s.allocs) cudaFree(p);
+  s.allocs.clear();
+  if (s.st && s.own_stream) cudaStreamDestroy(s.st);
+  if (s.ev) cudaEventDestroy(s.ev);
+  s.st = nullptr;
+  s.ev = nullptr;
+}
+
+// ---------------------------------------------------------------- C-ABI
+
+extern "C" {
+
+void csph_default_params(csph_params* p) {
+  if (!p) return;
+  p->g = 9.81;
+  p->K = 0.25;
+  p->eps_dry = 1e-6;
+  p->dt_max = INFINITY;
+  p->neg_tol = 1e-12;
+  p->n_manning = 0.0;
+  p->A_J = 0.0;
+  p->m_grass = 2;
+  p->C_J = 0.0;
+  p->C_Sh = 0.0;
+  p->d50 = 1e-3;
+  p->q_plus = 0.0;
+  p->q_minus = 0.0;
+  p->precision = 64;
+  p->device = 0;
+  p->path = CSPH_PATH_FUSED;
+  p->tile_rows = 0;
+}
+
+const char* csph_last_error(void) { return g_err.c_str(); }
+
+const char* csph_strerror(int code) {
+  switch (code) {
+    case CSPH_OK: return "ok";
+    case CSPH_EINVAL: return "invalid argument";
+    case CSPH_ENOSTATE: return "no state (call csph_set_state first)";
+    case CSPH_ENOMEM: return "device out of memory";
+    case CSPH_ECUDA: return "CUDA error";
+    case CSPH_ENCCL: return "NCCL error";
+    case CSPH_ENEGDEPTH: return "negative depth below -neg_tol";
+    case CSPH_ENONFINITE: return "non-finite Eq.7 maximum";
+    case CSPH_EDRY: return "no wet cell and dt_max = inf";
+    default: return "unknown error";
+  }
+}
+
+int csph_strip_rows(int ny, int nranks, int rank, int* j0, int* j1) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || ny < 3)
+    return fail(CSPH_EINVAL, "bad strip request");
+  int base = ny / nranks, extra = ny % nranks;
+  int a = rank * base + (rank < extra ? rank : extra);
+  int n = base + (rank < extra ? 1 : 0);
+  if (n < GY) return fail(CSPH_EINVAL, "strip of %d rows < %d (too many ranks for ny=%d)", n, GY, ny);
+  if (j0) *j0 = a;
+  if (j1) *j1 = a + n;
+  return CSPH_OK;
+}
+
+static csph* make_handle(int nx, int ny, double dx, const csph_params* p) {
+  if (check_params(nx, ny, dx, p)) return nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev < 1) {
+    fail(CSPH_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    return nullptr;
+  }
+  csph* H = new csph();
+  H->nx = nx;
+  H->ny = ny;
+  H->dx = dx;
+  H->p = *p;
+  H->P = make_phys(dx, *p);
+  return H;
+}
+
+csph_t* csph_create(int nx, int ny, double dx, const csph_params* p) {
+  csph* H = make_handle(nx, ny, dx, p);
+  if (!H) return nullptr;
+  H->mode = SINGLE;
+  H->s.resize(1);
+  if (strip_init(H, H->s[0], p->device, 0, ny, p->path == CSPH_PATH_STAGED)) {
+    std::string keep = g_err;
+    csph_destroy(H);
+    g_err = keep;
+    return nullptr;
+  }
+  return H;
+}
+
+csph_t* csph_create_multi(int nx, int ny, double dx, const csph_params* p, int nstrips,
+                          const int* devices) {
+  if (nstrips < 1 || !devices) {
+    fail(CSPH_EINVAL, "nstrips < 1 or devices NULL");
+    return nullptr;
+  }
+  csph* H = make_handle(nx, ny, dx, p);
+  if (!H) return nullptr;
+  H->mode = MULTI;
+  H->nranks = nstrips;
+  H->s.resize(nstrips);
+  for (int r = 0; r < nstrips; ++r) {
+    int j0, j1;
+    if (csph_strip_rows(ny, nstrips, r, &j0, &j1) ||
+        strip_init(H, H->s[r], devices[r], j0, j1 - j0, p->path == CSPH_PATH_STAGED)) {
+      std::string keep = g_err;
+      csph_destroy(H);
+      g_err = keep;
+      return nullptr;
+    }
+  }
+  // peer access where devices differ (ignore "already enabled")
+  for (int a = 0; a < nstrips; ++a)
+    for (int b = 0; b < nstrips; ++b)
+      if (H->s[a].dev != H->s[b].dev) {
+        cudaSetDevice(H->s[a].dev);
+        cudaDeviceEnablePeerAccess(H->s[b].dev, 0);
+        cudaGetLastError();
+      }
+  cudaSetDevice(H->s[0].dev);
+  if (cudaMalloc((void**)&H->gather, (size_t)nstrips * 4 * sizeof(unsigned long long)) !=
+      cudaSuccess) {
+    fail(CSPH_ENOMEM, "gather buffer");
+    csph_destroy(H);
+    return nullptr;
+  }
+  return H;
+}
+
+int csph_nccl_id_bytes(void) { return (int)sizeof(ncclUniqueId); }
+
+int csph_make_nccl_id(void* out) {
+  if (!out) return fail(CSPH_EINVAL, "out is NULL");
+  if (!load_nccl()) return CSPH_ENCCL;
+  ncclUniqueId id;
+  NK(g_nccl.GetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return CSPH_OK;
+}
+
+csph_t* csph_create_dist(int nx, int ny, double dx, const csph_params* p, int rank,
+                         int nranks, int local_device, const void* nccl_id) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !nccl_id) {
+    fail(CSPH_EINVAL, "bad rank/nranks/nccl_id");
+    return nullptr;
+  }
+  int j0, j1;
+  if (csph_strip_rows(ny, nranks, rank, &j0, &j1)) return nullptr;
+  if (!load_nccl()) return nullptr;
+  csph* H = make_handle(nx, ny, dx, p);
+  if (!H) return nullptr;
+  H->mode = DIST;
+  H->rank = rank;
+  H->nranks = nranks;
+  H->s.resize(1);
+  if (strip_init(H, H->s[0], local_device, j0, j1 - j0, p->path == CSPH_PATH_STAGED)) {
+    std::string keep = g_err;
+    csph_destroy(H);
+    g_err = keep;
+    return nullptr;
+  }
+  ncclUniqueId id;
+  memcpy(&id, nccl_id, sizeof id);
+  cudaSetDevice(local_device);
+  ncclResult_t r = g_nccl.CommInitRank(&H->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    fail(CSPH_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+    H->comm = nullptr;
+    std::string keep = g_err;
+    csph_destroy(H);
+    g_err = keep;
+    return nullptr;
+  }
+  return H;
+}
+
+void csph_destroy(csph_t* H) {
+  if (!H) return;
+  if (!H->s.empty()) cudaSetDevice(H->s[0].dev);
+  for (auto e : H->evs) cudaEventDestroy(e);
+  for (auto& s : H->s) strip_free(s);
+  if (H->gather) {
+    cudaSetDevice(H->s.empty() ? 0 : H->s[0].dev);
+    cudaFree(H->gather);
+  }
+  if (H->comm && g_nccl.ok) g_nccl.CommDestroy(H->comm);
+  delete H;
+}
+
+int csph_set_stream(csph_t* H, void* stream) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  if (H->s.size() != 1) return fail(CSPH_EINVAL, "set_stream needs a single-strip handle");
+  Strip& s = H->s[0];
+  CK(cudaSetDevice(s.dev));
+  CK(cudaStreamSynchronize(s.st));
+  if (s.own_stream) cudaStreamDestroy(s.st);
+  s.st = (cudaStream_t)stream;
+  s.own_stream = false;
+  return CSPH_OK;
+}
+
+long long csph_last_launch_count(csph_t* H) { return H ? H->launches : 0; }
+
+int csph_profile(csph_t* H, int enable) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  H->profiling = enable != 0;
+  H->prof_ms = 0.0;
+  H->prof_steps = 0;
+  return CSPH_OK;
+}
+
+int csph_get_profile(csph_t* H, double* ms, long long* steps) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  if (ms) *ms = H->prof_ms;
+  if (steps) *steps = H->prof_steps;
+  return CSPH_OK;
+}
+
+// -------- collective pieces of a step
+
+// Halo exchange of buffer q (3 owned edge rows x 4 fields, full padded width)
+// and the maxima combine.  NCCL for DIST, peer copies for MULTI.
+static int exchange(csph* H, int q) {
+  const size_t rowbytes = (size_t)H->s[0].v.pitch * 8;
+  if (H->mode == DIST) {
+    Strip& s = H->s[0];
+    const StripView& v = s.v;
+    const size_t cnt = (size_t)GY * v.pitch;
+    double* f[4] = {v.H[q], v.Qx[q], v.Qy[q], v.b[q]};
+    NK(g_nccl.GroupStart());
+    for (int k = 0; k < 4; ++k) {
+      if (H->rank > 0) {
+        NK(g_nccl.Send(f[k] + off(v.pitch, -GX, 0), cnt, ncclFloat64, H->rank - 1, H->comm, s.st));
+        NK(g_nccl.Recv(f[k] + off(v.pitch, -GX, -GY), cnt, ncclFloat64, H->rank - 1, H->comm, s.st));
+      }
+      if (H->rank < H->nranks - 1) {
+        NK(g_nccl.Send(f[k] + off(v.pitch, -GX, v.ny - GY), cnt, ncclFloat64, H->rank + 1, H->comm, s.st));
+        NK(g_nccl.Recv(f[k] + off(v.pitch, -GX, v.ny), cnt, ncclFloat64, H->rank + 1, H->comm, s.st));
+      }
+    }
+    NK(g_nccl.AllReduce(s.gM, s.gM, 3, ncclUint64, ncclMax, H->comm, s.st));
+    NK(g_nccl.GroupEnd());
+    (void)rowbytes;
+    return CSPH_OK;
+  }
+  if (H->mode == MULTI) {
+    const int n = (int)H->s.size();
+    for (int r = 0; r < n; ++r) {
+      CK(cudaSetDevice(H->s[r].dev));
+      CK(cudaEventRecord(H->s[r].ev, H->s[r].st));
+    }
+    Strip& s0 = H->s[0];
+    CK(cudaSetDevice(s0.dev));
+    for (int r = 0; r < n; ++r) {
+      CK(cudaStreamWaitEvent(s0.st, H->s[r].ev, 0));
+      CK(cudaMemcpyPeerAsync(H->gather + 4 * r, s0.dev, H->s[r].gM, H->s[r].dev,
+                             4 * sizeof(unsigned long long), s0.st));
+    }
+    max_gather_kernel<<<1, 32, 0, s0.st>>>(s0.gM, H->gather, n);
+    H->launches += 1;
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s0.ev, s0.st));
+    for (int r = 0; r < n; ++r) {
+      Strip& s = H->s[r];
+      CK(cudaSetDevice(s.dev));
+      CK(cudaStreamWaitEvent(s.st, s0.ev, 0));
+      if (r > 0)
+        CK(cudaMemcpyPeerAsync(s.gM, s.dev, s0.gM, s0.dev, 3 * sizeof(unsigned long long), s.st));
+      const StripView& v = s.v;
+      const size_t bytes = (size_t)GY * v.pitch * 8;
+      double* f[4] = {v.H[q], v.Qx[q], v.Qy[q], v.b[q]};
+      if (r > 0) {
+        const Strip& o = H->s[r - 1];
+        const double* g[4] = {o.v.H[q], o.v.Qx[q], o.v.Qy[q], o.v.b[q]};
+        for (int k = 0; k < 4; ++k)
+          CK(cudaMemcpyPeerAsync(f[k] + off(v.pitch, -GX, -GY), s.dev,
+                                 g[k] + off(o.v.pitch, -GX, o.v.ny - GY), o.dev, bytes, s.st));
+      }
+      if (r < n - 1) {
+        const Strip& o = H->s[r + 1];
+        const double* g[4] = {o.v.H[q], o.v.Qx[q], o.v.Qy[q], o.v.b[q]};
+        for (int k = 0; k < 4; ++k)
+          CK(cudaMemcpyPeerAsync(f[k] + off(v.pitch, -GX, v.ny), s.dev,
+                                 g[k] + off(o.v.pitch, -GX, 0), o.dev, bytes, s.st));
+      }
+    }
+    // every strip must finish reading its neighbours before they run ahead
+    for (int r = 0; r < n; ++r) {
+      CK(cudaSetDevice(H->s[r].dev));
+      CK(cudaEventRecord(H->s[r].ev, H->s[r].st));
+    }
+    for (int r = 0; r < n; ++r) {
+      CK(cudaSetDevice(H->s[r].dev));
+      if (r > 0) CK(cudaStreamWaitEvent(H->s[r].st, H->s[r - 1].ev, 0));
+      if (r < n - 1) CK(cudaStreamWaitEvent(H->s[r].st, H->s[r + 1].ev, 0));
+    }
+    (void)rowbytes;
+    return CSPH_OK;
+  }
+  return CSPH_OK;
+}
+
+// Input validation on the device (CSPH_EINVAL on NaN/Inf, h < 0, psi
+// outside [0,1)); bit 3 = psi is not uniform over this strip's rows.
+__global__ void validate_kernel(StripView S, int jlo, int jhi, const double* psi, double psi0,
+                                int* flags) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int j = jlo + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+  int f = 0;
+  if (i < S.nx && j < jhi) {
+    size_t c = off(S.pitch, i, j);
+    double H = S.H[0][c], qx = S.Qx[0][c], qy = S.Qy[0][c], b = S.b[0][c];
+    if (!isfinite(H) || !isfinite(qx) || !isfinite(qy) || !isfinite(b)) f |= 1;
+    if (H < 0.0) f |= 2;
+    if (psi) {
+      double p = psi[c];
+      if (!(p >= 0.0 && p < 1.0)) f |= 4;
+      if (p != psi0) f |= 8;
+    }
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+}
+
+static int upload_rows(csph* H, Strip& s, int j_begin, int j_end, const double* h,
+                       const double* hu, const double* hv, const double* b, const double* psi) {
+  // rows of this strip incl. halo rows where a neighbour exists
+  StripView& v = s.v;
+  int lo = s.gj0 - (v.wall_lo ? 0 : GY);
+  int hi = s.gj0 + v.ny + (v.wall_hi ? 0 : GY);
+  if (lo < j_begin || hi > j_end)
+    return fail(CSPH_EINVAL, "rows [%d,%d) do not cover strip rows [%d,%d) + halo", j_begin,
+                j_end, lo, hi);
+  const int nx = H->nx;
+  const double* src[4] = {h, hu, hv, b};
+  double* dst[4] = {v.H[0], v.Qx[0], v.Qy[0], v.b[0]};
+  for (int k = 0; k < 4; ++k) {
+    const double* a = src[k] + (size_t)(lo - j_begin) * nx;
+    double* d = dst[k] + off(v.pitch, 0, lo - s.gj0);
+    CK(cudaMemcpy2DAsync(d, (size_t)v.pitch * 8, a, (size_t)nx * 8, (size_t)nx * 8, hi - lo,
+                         cudaMemcpyHostToDevice, s.st));
+  }
+  double* psid = nullptr;
+  double psi0 = 0.0;
+  if (psi) {
+    size_t n = (size_t)(v.ny + 2 * GY) * v.pitch;
+    if (!s.Wbuf) {
+      int st = dalloc(s, (void**)&s.Wbuf, n * 8);
+      if (st) return st;
+      CK(cudaMemsetAsync(s.Wbuf, 0, n * 8, s.st));
+    }
+    psid = s.Wbuf;
+    psi0 = psi[(size_t)(lo - j_begin) * nx];
+    CK(cudaMemcpy2DAsync(psid + off(v.pitch, 0, lo - s.gj0), (size_t)v.pitch * 8,
+                         psi + (size_t)(lo - j_begin) * nx, (size_t)nx * 8, (size_t)nx * 8,
+                         hi - lo, cudaMemcpyHostToDevice, s.st));
+  }
+  CK(cudaMemsetAsync(s.dflags, 0, sizeof(int), s.st));
+  {
+    dim3 blk(32, 8), grd((nx + 31) / 32, (hi - lo + 7) / 8);
+    validate_kernel<<<grd, blk, 0, s.st>>>(v, lo - s.gj0, hi - s.gj0, psid, psi0, s.dflags);
+    CK(cudaGetLastError());
+  }
+  int flags = 0;
+  CK(cudaMemcpyAsync(&flags, s.dflags, sizeof(int), cudaMemcpyDeviceToHost, s.st));
+  CK(cudaStreamSynchronize(s.st));
+  if (flags & 1) return fail(CSPH_EINVAL, "non-finite input value");
+  if (flags & 2) return fail(CSPH_EINVAL, "negative depth in input");
+  if (flags & 4) return fail(CSPH_EINVAL, "psi outside [0,1)");
+  if (!psi || !(flags & 8)) {
+    // uniform porosity: W is a scalar (64 B/cell instead of 72 B/cell)
+    v.W = nullptr;
+    v.Wc = 1.0 / (1.0 - psi0);
+  } else {
+    size_t n = (size_t)(v.ny + 2 * GY) * v.pitch;
+    w_from_psi_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s.st>>>(s.Wbuf, s.Wbuf, n);
+    CK(cudaGetLastError());
+    v.W = s.Wbuf;
+  }
+  return CSPH_OK;
+}
+
+int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, const double* hu,
+                        const double* hv, const double* b, const double* psi) {
+  if (!H || !h || !hu || !hv || !b) return fail(CSPH_EINVAL, "NULL argument");
+  if (j_begin < 0 || j_end > H->ny || j_end <= j_begin) return fail(CSPH_EINVAL, "bad row range");
+  H->have_state = false;
+  int st;
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    if ((st = upload_rows(H, s, j_begin, j_end, h, hu, hv, b, psi))) return st;
+    init_ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
+    CK(cudaMemsetAsync(s.gM, 0, 4 * sizeof(unsigned long long), s.st));
+    // walls: ghosts of buffer 0 (W is read only on owned cells: no ghosts needed)
+    launch_mirror(s.v, s.ctrl, 0, s.st, &H->launches);
+    CK(cudaGetLastError());
+  }
+  // maxima of the initial state, combined across strips / ranks
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    dim3 blk(32, 8), grd((s.v.nx + 31) / 32, (s.v.ny + 7) / 8);
+    maxima_kernel<<<grd, blk, 0, s.st>>>(s.v, s.ctrl, H->P, s.gM);
+    CK(cudaGetLastError());
+  }
+  if (H->mode == DIST) {
+    Strip& s = H->s[0];
+    NK(g_nccl.AllReduce(s.gM, s.gM, 3, ncclUint64, ncclMax, H->comm, s.st));
+  } else if (H->mode == MULTI) {
+    if ((st = exchange(H, 0))) return st;  // also refreshes halos of buffer 0
+  }
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 0);
+    CK(cudaGetLastError());
+  }
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.st));
+  }
+  H->have_state = true;
+  H->host_parity = 0;
+  return CSPH_OK;
+}
+
+int csph_set_state(csph_t* H, const double* h, const double* hu, const double* hv,
+                   const double* b, const double* psi) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  return csph_set_state_rows(H, 0, H->ny, h, hu, hv, b, psi);
+}
+
+int csph_step(csph_t* H, int nsteps) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  if (nsteps < 0) return fail(CSPH_EINVAL, "nsteps < 0");
+  if (!H->have_state) return fail(CSPH_ENOSTATE, "csph_step before csph_set_state");
+  H->launches = 0;
+  if (H->profiling && H->evs.size() < (size_t)nsteps * 2) {
+    CK(cudaSetDevice(H->s[0].dev));
+    while (H->evs.size() < (size_t)nsteps * 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      H->evs.push_back(e);
+    }
+  }
+  for (int n = 0; n < nsteps; ++n) {
+    const int q = H->host_parity ^ 1;
+    for (size_t si = 0; si < H->s.size(); ++si) {
+      Strip& s = H->s[si];
+      CK(cudaSetDevice(s.dev));
+      clear_flags_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
+      H->launches += 1;
+      if (H->profiling && si == 0) CK(cudaEventRecord(H->evs[2 * n], s.st));
+      if (H->p.path == CSPH_PATH_STAGED)
+        launch_staged_step(s.v, s.ctrl, s.scr, H->P, s.gM, s.st, &H->launches);
+      else
+        launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, H->p.tile_rows, s.st,
+                          &H->launches);  // writes the wall ghosts in its epilogue
+      if (H->profiling && si == 0) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
+      if (H->p.path == CSPH_PATH_STAGED) launch_mirror(s.v, s.ctrl, 1, s.st, &H->launches);
+      CK(cudaGetLastError());
+    }
+    int st = exchange(H, q);
+    if (st) return st;
+    for (auto& s : H->s) {
+      CK(cudaSetDevice(s.dev));
+      ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 1);
+      H->launches += 1;
+      CK(cudaGetLastError());
+    }
+    H->host_parity = q;
+  }
+  int status = 0;
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    Ctrl c;
+    CK(cudaMemcpyAsync(&c, s.ctrl, sizeof c, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    if (c.status && !status) status = c.status;
+  }
+  if (H->profiling) {
+    CK(cudaSetDevice(H->s[0].dev));
+    for (int n = 0; n < nsteps; ++n) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, H->evs[2 * n], H->evs[2 * n + 1]));
+      H->prof_ms += ms;
+    }
+    H->prof_steps += nsteps;
+  }
+  if (status) return fail(status, "%s", csph_strerror(status));
+  return CSPH_OK;
+}
+
+static int read_ctrl(csph* H, Ctrl* c) {
+  Strip& s = H->s[0];
+  CK(cudaSetDevice(s.dev));
+  CK(cudaMemcpyAsync(c, s.ctrl, sizeof *c, cudaMemcpyDeviceToHost, s.st));
+  CK(cudaStreamSynchronize(s.st));
+  return CSPH_OK;
+}
+
+int csph_get_state_rows(csph_t* H, int j_begin, int j_end, double* h, double* hu, double* hv,
+                        double* b) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  if (!H->have_state) return fail(CSPH_ENOSTATE, "no state");
+  if (j_begin < 0 || j_end > H->ny || j_end <= j_begin) return fail(CSPH_EINVAL, "bad row range");
+  for (auto& s : H->s) {
+    Ctrl c;
+    CK(cudaSetDevice(s.dev));
+    CK(cudaMemcpyAsync(&c, s.ctrl, sizeof c, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    const StripView& v = s.v;
+    int lo = s.gj0 > j_begin ? s.gj0 : j_begin;
+    int hi = s.gj0 + v.ny < j_end ? s.gj0 + v.ny : j_end;
+    if (hi <= lo) continue;
+    const int p = c.parity;
+    double* dst[4] = {h, hu, hv, b};
+    const double* src[4] = {v.H[p], v.Qx[p], v.Qy[p], v.b[p]};
+    for (int k = 0; k < 4; ++k) {
+      if (!dst[k]) continue;
+      CK(cudaMemcpy2DAsync(dst[k] + (size_t)(lo - j_begin) * H->nx, (size_t)H->nx * 8,
+                           src[k] + off(v.pitch, 0, lo - s.gj0), (size_t)v.pitch * 8,
+                           (size_t)H->nx * 8, hi - lo, cudaMemcpyDeviceToHost, s.st));
+    }
+    CK(cudaStreamSynchronize(s.st));
+  }
+  return CSPH_OK;
+}
+
+int csph_get_state(csph_t* H, double* h, double* hu, double* hv, double* b) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  return csph_get_state_rows(H, 0, H->ny, h, hu, hv, b);
+}
+
+int csph_get_time(csph_t* H, double* t, long long* steps_done, double* last_dt) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  if (!H->have_state) {
+    if (t) *t = 0.0;
+    if (steps_done) *steps_done = 0;
+    if (last_dt) *last_dt = 0.0;
+    return CSPH_OK;
+  }
+  Ctrl c;
+  int st = read_ctrl(H, &c);
+  if (st) return st;
+  if (t) *t = c.t;
+  if (steps_done) *steps_done = c.step;
+  if (last_dt && c.step > 0) {
+    Strip& s = H->s[0];
+    CK(cudaMemcpy(last_dt, s.dtlog + (c.step - 1) % LOGCAP, 8, cudaMemcpyDeviceToHost));
+  } else if (last_dt) {
+    *last_dt = 0.0;
+  }
+  return CSPH_OK;
+}
+
+int csph_get_dt_log(csph_t* H, double* dt, int* limiter, int cap, int* n) {
+  if (!H || cap < 0) return fail(CSPH_EINVAL, "bad argument");
+  if (!H->have_state) {
+    if (n) *n = 0;
+    return CSPH_OK;
+  }
+  Ctrl c;
+  int st = read_ctrl(H, &c);
+  if (st) return st;
+  long long done = c.step;
+  long long m = done < cap ? done : cap;
+  if (m > LOGCAP) m = LOGCAP;
+  Strip& s = H->s[0];
+  long long first = (done - m) % LOGCAP;
+  long long n1 = m < LOGCAP - first ? m : LOGCAP - first;  // up to the ring end
+  if (dt) {
+    CK(cudaMemcpy(dt, s.dtlog + first, n1 * 8, cudaMemcpyDeviceToHost));
+    if (m > n1) CK(cudaMemcpy(dt + n1, s.dtlog, (m - n1) * 8, cudaMemcpyDeviceToHost));
+  }
+  if (limiter) {
+    CK(cudaMemcpy(limiter, s.limlog + first, n1 * 4, cudaMemcpyDeviceToHost));
+    if (m > n1) CK(cudaMemcpy(limiter + n1, s.limlog, (m - n1) * 4, cudaMemcpyDeviceToHost));
+  }
+  if (n) *n = (int)m;
+  return CSPH_OK;
+}
+
+int csph_get_maxima(csph_t* H, double M[3]) {
+  if (!H || !M) return fail(CSPH_EINVAL, "bad argument");
+  if (!H->have_state) return fail(CSPH_ENOSTATE, "no state");
+  Strip& s = H->s[0];
+  CK(cudaSetDevice(s.dev));
+  CK(cudaStreamSynchronize(s.st));
+  CK(cudaMemcpy(M, s.Mlast, 3 * 8, cudaMemcpyDeviceToHost));
+  return CSPH_OK;
+}
+
+}  // extern "C"

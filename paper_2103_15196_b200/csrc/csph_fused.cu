@@ -1,0 +1,417 @@
+// csph_fused.cu -- one CUDA kernel per CSPH-TVD step (K1..K8 of PAPER.md:224-238 fused).
+//
+// Design:
+//  * A CTA owns a column tile of TX = NT - 8 output cells and marches down a chunk of
+//    TY rows ("2.5D" y-march).  Thread t owns padded column x0 - 4 + t for the whole march.
+//  * Input rows (H, Qx, Qy, b [, W]) are staged into a D-slot shared-memory ring by 1D TMA
+//    bulk copies (cp.async.bulk ... mbarrier::complete_tx), PF rows ahead of use.
+//  * Every stage of R is computed once per cell: x-neighbour values are exchanged through
+//    shared memory (three barriers per row), y-neighbour values are carried in registers.
+//    The update of row L-3 is produced when row L is loaded (stencil radius 3).
+//  * Epilogue: stores of (H, Qx, Qy, b) for row L-3, wall-mirror ghosts, the next step's
+//    Eq.7 maxima (warp shuffle + block max + one atomicMax per CTA) and the negative-depth flag.
+// The arithmetic per cell is the same sequence of IEEE operations as the oracle (-fmad=false).
+#include <climits>
+
+#include "csph_launch.h"
+
+namespace ck {
+
+namespace {
+
+constexpr int D = 8;   // ring slots
+constexpr int PF = 3;  // rows prefetched ahead (D >= PF + 5: rows L-4..L are live)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_row(void* dst, const void* src, unsigned bytes,
+                                        unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int NT, bool HASW>
+struct Smem {
+  static constexpr int NF = HASW ? 5 : 4;
+  static constexpr int RW = NT + 4;  // ring row: data at [2, 2+NT), 16 B aligned
+  static constexpr int XW = NT + 2;  // exchange row: element t at [t+1]
+  alignas(128) double ring[D][NF][RW];
+  double U[2][XW];      // u of the last two rows (div)
+  double PE[XW];        // K2 x-face force (t|t+1), row L
+  double X2[5][XW];     // row L-1: H_half, u~, v~, J0x, |J0|
+  double X3[5][XW];     // row L-1: K5 x-face force, sigma_x (eta, H, u~, v~)
+  double X4[4][XW];     // row L-1: x-face fluxes (t|t+1): F^H, F^Qx, F^Qy, F^J
+  alignas(8) unsigned long long bar[D];
+  unsigned long long red[3][NT / 32];
+};
+
+enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
+
+template <int NT, bool HASW>
+__global__ void __launch_bounds__(NT) fused_step_kernel(StripView S, Ctrl* __restrict__ C, Phys P,
+                                                        unsigned long long* __restrict__ gM,
+                                                        int row0, int row1, int TY) {
+  constexpr int TX = NT - 8;
+  using SM = Smem<NT, HASW>;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  SM& sm = *reinterpret_cast<SM*>(smraw);
+
+  const int status = C->status;
+  if (status) return;
+  const int par = C->parity;
+  const double tau = C->tau;
+  const double theta = 0.5 * tau;
+  const double lam = tau / P.h;
+  const double* __restrict__ gin[5] = {par ? S.H[1] : S.H[0], par ? S.Qx[1] : S.Qx[0],
+                                       par ? S.Qy[1] : S.Qy[0], par ? S.b[1] : S.b[0], S.W};
+  double* __restrict__ oH = par ? S.H[0] : S.H[1];
+  double* __restrict__ oQx = par ? S.Qx[0] : S.Qx[1];
+  double* __restrict__ oQy = par ? S.Qy[0] : S.Qy[1];
+  double* __restrict__ ob = par ? S.b[0] : S.b[1];
+
+  const int t = threadIdx.x;
+  const int nx = S.nx, ny = S.ny, pitch = S.pitch;
+  const int x0 = blockIdx.x * TX;
+  const int col = x0 - 4 + t;
+  const int y0 = row0 + blockIdx.y * TY;
+  const int y1 = min(y0 + TY, row1);
+  if (y0 >= y1) return;
+  const int rfirst = y0 - GY;       // first input row
+  const int niter = (y1 + 2) - rfirst + 1;  // input rows y0-3 .. y1+2
+  // columns copied per row: [x0-4, min(x0-4+NT, nx+4)), even count
+  int ncopy = min(NT, nx + 8 - x0);
+  ncopy = (ncopy + 1) & ~1;
+  const unsigned row_bytes = (unsigned)ncopy * 8u;
+  const unsigned tx_bytes = row_bytes * SM::NF;
+
+  // zero the exchange and ring memory once (edge threads read never-written slots)
+  {
+    double* z = reinterpret_cast<double*>(smraw);
+    const int nd = (int)(offsetof(SM, bar) / sizeof(double));
+    for (int k = t; k < nd; k += NT) z[k] = 0.0;
+  }
+  if (t == 0) {
+    for (int s = 0; s < D; ++s) mbar_init(&sm.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int k) {  // load input row rfirst + k into slot k % D
+    const int s = k % D;
+    const size_t go = off(pitch, x0 - 4, rfirst + k);
+    mbar_expect_tx(&sm.bar[s], tx_bytes);
+#pragma unroll
+    for (int f = 0; f < SM::NF; ++f) tma_row(&sm.ring[s][f][2], gin[f] + go, row_bytes, &sm.bar[s]);
+  };
+  if (t == 0) {
+    fence_proxy_async();
+    for (int k = 0; k < PF && k < niter; ++k) issue(k);
+  }
+
+  // ring access: value of field f at iteration-row k, thread column t + dt
+#define RG(f, k, dt) sm.ring[(k) % D][f][(t) + 2 + (dt)]
+#define XG(a, dt) a[(t) + 1 + (dt)]
+
+  // ---- carried registers (row offsets relative to the newest row L) ----
+  double v1 = 0, v2 = 0;          // v(L-1), v(L-2)
+  double r1 = 0;                  // r(L-1)
+  double gam1 = 0, gam2 = 0;      // gamma(L-1), gamma(L-2)
+  double eta1 = 0, b1c = 0;       // eta(L-1), b(L-1)
+  double PS1 = 0;                 // K2 y-face force (L-2|L-1)
+  double phix1 = 0;               // Phi_x(L-1)
+  double Hh2 = 0;                 // H_half(L-2)
+  double PhS2 = 0;                // K5 y-face force (L-3|L-2)
+  double phx2h = 0;               // Phi_half_x(L-2)
+  double QLx3 = 0, QLy3 = 0;      // Q^L(L-3)
+  double ut2 = 0, vt2 = 0, ut3 = 0, vt3 = 0;  // u~, v~ of rows L-2, L-3
+  double J0y2 = 0, J0a2 = 0, J0y3 = 0, J0a3 = 0;
+  double sy3[4] = {0, 0, 0, 0};   // sigma_y of row L-3 (eta, H, v~, u~)
+  double Fo[4] = {0, 0, 0, 0};    // own x-face flux of row L-2 (t|t+1)
+  double dF3[4] = {0, 0, 0, 0};   // Delta F_x of row L-3
+  double Gs[4] = {0, 0, 0, 0};    // y-face flux (L-4|L-3)
+  unsigned long long m0 = 0, m1 = 0, m2 = 0;
+  bool neg = false;
+
+  const bool col_out = (t >= 4) && (t < 4 + TX) && (col < nx);
+
+  for (int k = 0; k < niter; ++k) {
+    const int L = rfirst + k;  // newest row (strip-local index)
+    // ================= phase A: K1 + K2 x-face + K2 y-face (row L) =================
+    mbar_wait(&sm.bar[k % D], (unsigned)((k / D) & 1));
+    const double H0 = RG(F_H, k, 0), b0 = RG(F_B, k, 0);
+    const double Qx0 = RG(F_QX, k, 0), Qy0 = RG(F_QY, k, 0);
+    const bool w0 = H0 > P.eps;
+    const double eta0 = H0 + b0;
+    double r0 = 0.0, u0 = 0.0, v0 = 0.0, gam0 = 0.0;
+    if (w0) {
+      r0 = 1.0 / H0;
+      u0 = Qx0 * r0;
+      v0 = Qy0 * r0;
+      if (P.fric) {
+        double sp = sqrt(u0 * u0 + v0 * v0);
+        gam0 = (P.cgam * sp) * (r0 * icbrt(H0));
+      }
+    }
+    double PE0;
+    {
+      const double bR = RG(F_B, k, 1);
+      const double etaR = RG(F_H, k, 1) + bR;
+      PE0 = face_force(P.cP, eta0, b0, etaR, bR);
+    }
+    const double PN1 = face_force(P.cP, eta1, b1c, eta0, b0);  // face (L-1|L)
+    const double H1 = RG(F_H, k - 1 + D, 0);
+    const bool w1 = H1 > P.eps;
+    const double phiy1 = w1 ? -(PN1 + PS1) : 0.0;
+    XG(sm.U[k & 1], 0) = u0;
+    XG(sm.PE, 0) = PE0;
+    __syncthreads();  // ---------------------------------------------------- barrier 1
+    if (t == 0 && k + PF < niter) {
+      fence_proxy_async();
+      issue(k + PF);
+    }
+    // ================= phase B: K4 predictor + J0 (row L-1) =================
+    const double phix0 = w0 ? -(PE0 + XG(sm.PE, -1)) : 0.0;
+    double Hh1, ut1 = 0.0, vt1 = 0.0;
+    const int km1 = k - 1 + D;  // k-1 as a non-negative ring index
+    if (w1) {
+      const double* Up = sm.U[(k - 1) & 1];
+      double div = ((XG(Up, 1) - XG(Up, -1)) + (v0 - v2)) * P.inv_2h;
+      Hh1 = H1 * (1.0 - theta * div);
+      double f = P.fric ? 1.0 / (1.0 + theta * gam1) : 1.0;
+      ut1 = ((RG(F_QX, km1, 0) + theta * phix1) * f) * r1;
+      vt1 = ((RG(F_QY, km1, 0) + theta * phiy1) * f) * r1;
+    } else {
+      Hh1 = H1;
+    }
+    double J0x1 = 0.0, J0y1 = 0.0, J0a1 = 0.0;
+    if (P.transport) grass_gated(P, ut1, vt1, H1, J0x1, J0y1, J0a1);
+    // Delta F_x of row L-2 from the own face (t|t+1) and the west face (t-1|t)
+    double dF2[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dF2[q] = Fo[q] - XG(sm.X4[q], -1);
+    XG(sm.X2[0], 0) = Hh1;
+    XG(sm.X2[1], 0) = ut1;
+    XG(sm.X2[2], 0) = vt1;
+    XG(sm.X2[3], 0) = J0x1;
+    XG(sm.X2[4], 0) = J0a1;
+    __syncthreads();  // ---------------------------------------------------- barrier 2
+    // ================= phase C: K5, sigma_x, K6 (row L-2), y-face flux (L-3|L-2) ======
+    const double b1 = RG(F_B, km1, 0);
+    const double eta1n = H1 + b1;  // eta(L-1) (== eta1 carried)
+    double PhE1;
+    {
+      const double bR = RG(F_B, km1, 1);
+      PhE1 = face_force(P.cP, Hh1 + b1, b1, XG(sm.X2[0], 1) + bR, bR);
+    }
+    double sx1[4];
+    {
+      const double HLm = RG(F_H, km1, -1), HRp = RG(F_H, km1, 1);
+      const double eL = HLm + RG(F_B, km1, -1), eR = HRp + RG(F_B, km1, 1);
+      sx1[0] = minmod(eta1n - eL, eR - eta1n);
+      sx1[1] = minmod(H1 - HLm, HRp - H1);
+      sx1[2] = minmod(ut1 - XG(sm.X2[1], -1), XG(sm.X2[1], 1) - ut1);
+      sx1[3] = minmod(vt1 - XG(sm.X2[2], -1), XG(sm.X2[2], 1) - vt1);
+    }
+    const int km2 = k - 2 + D, km3 = k - 3 + D;
+    const double H2 = RG(F_H, km2, 0), b2 = RG(F_B, km2, 0);
+    const bool w2 = H2 > P.eps;
+    const double PhN2 = face_force(P.cP, Hh2 + b2, b2, Hh1 + b1, b1);  // face (L-2|L-1)
+    double QLx2 = 0.0, QLy2 = 0.0;
+    if (w2) {
+      const double phy2h = -(PhN2 + PhS2);
+      double f1 = P.fric ? 1.0 / (1.0 + tau * gam2) : 1.0;
+      QLx2 = (RG(F_QX, km2, 0) + tau * phx2h) * f1;
+      QLy2 = (RG(F_QY, km2, 0) + tau * phy2h) * f1;
+    }
+    // y-face (L-3|L-2): sigma_y of row L-2 (always, it is carried), then HLL + sediment
+    const double H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
+    const bool w3 = H3 > P.eps;
+    const double eta2 = H2 + b2, eta3 = H3 + b3;
+    double sy2[4];
+    sy2[0] = minmod(eta2 - eta3, eta1n - eta2);
+    sy2[1] = minmod(H2 - H3, H1 - H2);
+    sy2[2] = minmod(vt2 - vt3, vt1 - vt2);
+    sy2[3] = minmod(ut2 - ut3, ut1 - ut2);
+    double Gn[4] = {0.0, 0.0, 0.0, 0.0};  // (G^H, G^Qx, G^Qy, G^J) at (L-3|L-2)
+    if (w3 || w2) {
+      double F0, F1, F2;
+      hll_face(P.g, eta3 + 0.5 * sy3[0], H3 + 0.5 * sy3[1], vt3 + 0.5 * sy3[2],
+               ut3 + 0.5 * sy3[3], eta2 - 0.5 * sy2[0], H2 - 0.5 * sy2[1], vt2 - 0.5 * sy2[2],
+               ut2 - 0.5 * sy2[3], F0, F1, F2);
+      Gn[0] = F0;
+      Gn[2] = F1;  // normal momentum of a y-face -> Qy
+      Gn[1] = F2;  // tangential -> Qx
+      Gn[3] = P.transport ? sed_face(P, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2) : 0.0;
+    }
+    XG(sm.X3[0], 0) = PhE1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) XG(sm.X3[1 + q], 0) = sx1[q];
+    __syncthreads();  // ---------------------------------------------------- barrier 3
+    // ================= phase D: Phi_half_x (row L-1), x-face flux (row L-1), K8 (row L-3) ===
+    const double phx1h = w1 ? -(PhE1 + XG(sm.X3[0], -1)) : 0.0;
+    double Fn[4] = {0.0, 0.0, 0.0, 0.0};
+    {
+      const double HR = RG(F_H, km1, 1);
+      const bool wR = HR > P.eps;
+      if (w1 || wR) {
+        const double bR = RG(F_B, km1, 1);
+        const double eR = HR + bR;
+        const double uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
+        double F0, F1, F2;
+        hll_face(P.g, eta1n + 0.5 * sx1[0], H1 + 0.5 * sx1[1], ut1 + 0.5 * sx1[2],
+                 vt1 + 0.5 * sx1[3], eR - 0.5 * XG(sm.X3[1], 1), HR - 0.5 * XG(sm.X3[2], 1),
+                 uR - 0.5 * XG(sm.X3[3], 1), vR - 0.5 * XG(sm.X3[4], 1), F0, F1, F2);
+        Fn[0] = F0;
+        Fn[1] = F1;  // normal momentum of an x-face -> Qx
+        Fn[2] = F2;  // tangential -> Qy
+        Fn[3] = P.transport ? sed_face(P, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
+                                       XG(sm.X2[4], 1), b1, bR)
+                            : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = Fn[q];
+    // ---- K8 update of row L-3 ----
+    const int j = L - 3;
+    if (col_out && j >= y0 && j < y1) {
+      const double W3 = HASW ? RG(F_W, km3, 0) : S.Wc;
+      const double dH = dF3[0] + (Gn[0] - Gs[0]);
+      const double dQx = dF3[1] + (Gn[1] - Gs[1]);
+      const double dQy = dF3[2] + (Gn[2] - Gs[2]);
+      const double dJ = dF3[3] + (Gn[3] - Gs[3]);
+      const double Hn = H3 - lam * dH;
+      double Qxn = QLx3 - lam * dQx;
+      double Qyn = QLy3 - lam * dQy;
+      const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
+      const bool wet = Hn > P.eps;
+      if (!wet) { Qxn = 0.0; Qyn = 0.0; }
+      if (Hn < -P.neg_tol) neg = true;
+      const size_t o = off(pitch, col, j);
+      oH[o] = Hn; oQx[o] = Qxn; oQy[o] = Qyn; ob[o] = bn;
+      // wall ghosts: x mirror, y mirror, corners.  A cell within 3 of
+      // both walls of a small grid mirrors into both sides.
+      {
+        int gc[3] = {col, col < 3 ? -1 - col : INT_MIN, col >= nx - 3 ? 2 * nx - 1 - col : INT_MIN};
+        int gr[3] = {j, (S.wall_lo && j < 3) ? -1 - j : INT_MIN,
+                     (S.wall_hi && j >= ny - 3) ? 2 * ny - 1 - j : INT_MIN};
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int c2 = 0; c2 < 3; ++c2) {
+            if ((a | c2) == 0 || gc[a] == INT_MIN || gr[c2] == INT_MIN) continue;
+            const size_t g = off(pitch, gc[a], gr[c2]);
+            oH[g] = Hn; ob[g] = bn;
+            oQx[g] = a ? -Qxn : Qxn;
+            oQy[g] = c2 ? -Qyn : Qyn;
+          }
+      }
+      if (wet) {
+        double t1, t2, t3;
+        dt_terms(P, Hn, Qxn, Qyn, W3, t1, t2, t3);
+        unsigned long long a = dbits(t1), b = dbits(t2), c = dbits(t3);
+        m0 = a > m0 ? a : m0; m1 = b > m1 ? b : m1; m2 = c > m2 ? c : m2;
+      }
+    }
+    // ---- rotate the carried window ----
+    v2 = v1; v1 = v0;
+    r1 = r0;
+    gam2 = gam1; gam1 = gam0;
+    eta1 = eta0; b1c = b0;
+    PS1 = PN1;
+    phix1 = phix0;
+    Hh2 = Hh1;
+    PhS2 = PhN2;
+    phx2h = phx1h;
+    QLx3 = QLx2; QLy3 = QLy2;
+    ut3 = ut2; vt3 = vt2; ut2 = ut1; vt2 = vt1;
+    J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = J0a1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      sy3[q] = sy2[q];
+      Fo[q] = Fn[q];
+      dF3[q] = dF2[q];
+      Gs[q] = Gn[q];
+    }
+  }
+#undef RG
+#undef XG
+  if (neg) atomicOr(&C->flags, 1);
+  // block max of the Eq.7 terms, one atomicMax per CTA and term
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long a = __shfl_xor_sync(0xffffffffu, m0, o);
+    unsigned long long b = __shfl_xor_sync(0xffffffffu, m1, o);
+    unsigned long long c = __shfl_xor_sync(0xffffffffu, m2, o);
+    m0 = a > m0 ? a : m0; m1 = b > m1 ? b : m1; m2 = c > m2 ? c : m2;
+  }
+  if ((t & 31) == 0) {
+    sm.red[0][t >> 5] = m0; sm.red[1][t >> 5] = m1; sm.red[2][t >> 5] = m2;
+  }
+  __syncthreads();
+  if (t < 3) {
+    unsigned long long m = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) m = sm.red[t][w] > m ? sm.red[t][w] : m;
+    if (m) atomicMax(&gM[t], m);
+  }
+}
+
+template <int NT, bool HASW>
+void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM, int row0,
+              int row1, int TY, cudaStream_t st) {
+  using SM = Smem<NT, HASW>;
+  constexpr int TX = NT - 8;
+  static bool configured = false;
+  const size_t smem = sizeof(SM);
+  if (!configured) {
+    cudaFuncSetAttribute(fused_step_kernel<NT, HASW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = true;
+  }
+  dim3 grid((unsigned)((S.nx + TX - 1) / TX), (unsigned)((row1 - row0 + TY - 1) / TY));
+  fused_step_kernel<NT, HASW><<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY);
+}
+
+}  // namespace
+
+void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM,
+                       int row0, int row1, int tile_rows, cudaStream_t st, long long* nlaunch) {
+  if (row1 <= row0) return;
+  int TY = tile_rows > 0 ? tile_rows : 128;
+  if (S.W)
+    launch_t<128, true>(S, C, P, gM, row0, row1, TY, st);
+  else
+    launch_t<128, false>(S, C, P, gM, row0, row1, TY, st);
+  *nlaunch += 1;
+}
+
+}  // namespace ck

@@ -1,0 +1,163 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle on the same
+seeded inputs.  Bar (north_star): err_F <= 1e-9 after 100
+fp64 steps, identical step count, bitwise-identical dt sequence.  Under the
+arithmetic contract the fields are in fact bitwise equal,
+which is asserted as well."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+G = 9.81
+PATHS = {"fused": 0, "staged": 1}
+
+
+@pytest.fixture(scope="module")
+def cs():
+    from paper_2103_15196_b200 import build, csph
+    build.build()
+    return csph
+
+
+def parity_err(gpu, ref):
+    h, hu, hv, b = ref
+    sh = np.max(np.abs(h))
+    sq = max(np.max(np.abs(hu)), np.max(np.abs(hv)), sh * math.sqrt(G * sh))
+    sb = max(np.max(np.abs(b)), sh)
+    scales = [sh, sq, sq, sb]
+    return [float(np.max(np.abs(g - r)) / s) for g, r, s in zip(gpu, ref, scales)]
+
+
+def run_both(cs, c, steps, path, fields=None):
+    h, hu, hv, b, psi = fields if fields is not None else synth.fill(c)
+    ref = oracle.Oracle(c.nx, c.ny, c.dx, oracle.Params(**c.params))
+    assert ref.set_state(h, hu, hv, b, psi) == 0
+    st_ref, dt_ref, lim_ref = ref.step(steps)
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, path=PATHS[path]))
+    g.set_state(h, hu, hv, b, psi)
+    st = g.step(steps, check=False)
+    dt, lim = g.get_dt_log(steps)
+    out = g.get_state()
+    tg = g.get_time()
+    g.destroy()
+    return (st, dt, lim, out, tg), (st_ref, dt_ref, lim_ref, ref.get_state(), ref.time())
+
+
+def assert_parity(gpu, ref, tol=1e-9, bitwise=True):
+    st, dt, lim, out, tg = gpu
+    st_r, dt_r, lim_r, out_r, tr = ref
+    assert st == st_r
+    assert len(dt) == len(dt_r) and np.array_equal(dt, dt_r), "dt sequence differs"
+    assert np.array_equal(lim, lim_r)
+    errs = parity_err(out, out_r)
+    assert max(errs) <= tol, errs
+    assert tg[1] == tr[1]
+    if bitwise:
+        for a, r in zip(out, out_r):
+            assert np.array_equal(a, r)
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+def test_C1_dam_break_100_steps(cs, path):
+    c = synth.config("C1")
+    gpu, ref = run_both(cs, c, 100, path)
+    assert_parity(gpu, ref)
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+def test_C2_lake_at_rest_100_steps(cs, path):
+    c = synth.config("C2", 256)
+    gpu, ref = run_both(cs, c, 100, path)
+    assert_parity(gpu, ref)
+    h, hu, hv, b, psi = synth.fill(c)
+    assert np.array_equal(gpu[3][0], h) and np.all(gpu[3][1] == 0.0)
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+@pytest.mark.parametrize("name,n,ny", [("C3", 256, 200), ("C4", 192, 256), ("C5", 300, 260)])
+def test_dam_and_flood_configs_100_steps(cs, path, name, n, ny):
+    """Several tiles and ragged tails (sizes not multiples of the tile)."""
+    c = synth.config(name, n, ny)
+    gpu, ref = run_both(cs, c, 100, path)
+    assert_parity(gpu, ref)
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+def test_random_wet_dry_films(cs, path):
+    """Thin films, random currents, heterogeneous psi, all physics on."""
+    c = synth.Config("rand", 0, 131, 77, params=dict(n_manning=0.03, A_J=0.01, C_J=2.0,
+                                                    C_Sh=4.0, d50=1e-3))
+    f = synth.random_state(c.nx, c.ny, seed=5, wet_frac=0.6, vel=1.0, film=0.2)
+    gpu, ref = run_both(cs, c, 60, path, fields=f)
+    assert_parity(gpu, ref)
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+def test_minimum_grid_3x3(cs, path):
+    c = synth.Config("tiny", 0, 3, 3, params={})
+    h = np.array([[1.0, 0.5, 0.0], [0.2, 0.0, 0.0], [1.0, 1.0, 1.0]])
+    z = np.zeros((3, 3))
+    gpu, ref = run_both(cs, c, 10, path, fields=(h, z, z, z, np.full((3, 3), 0.4)))
+    assert_parity(gpu, ref)
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+def test_all_dry_is_EDRY(cs, path):
+    z = np.zeros((8, 8))
+    g = cs.csph_create(8, 8, 1.0, cs.csph_default_params(path=PATHS[path]))
+    g.set_state(z, z, z, z, None)
+    assert g.step(1, check=False) == cs.CSPH_EDRY
+    assert g.get_time()[1] == 0
+
+
+def test_input_validation(cs):
+    g = cs.csph_create(8, 8, 1.0)
+    z = np.zeros((8, 8))
+    bad = z.copy(); bad[2, 3] = np.nan
+    with pytest.raises(cs.CsphError) as e:
+        g.set_state(bad, z, z, z)
+    assert e.value.code == cs.CSPH_EINVAL
+    with pytest.raises(cs.CsphError):
+        g.set_state(z - 1.0, z, z, z)
+    with pytest.raises(cs.CsphError):
+        g.set_state(z, z, z, z, np.full((8, 8), 1.0))
+    with pytest.raises(cs.CsphError) as e:
+        cs.csph_create(8, 8, 1.0).step(1)
+    assert e.value.code == cs.CSPH_ENOSTATE
+
+
+def test_checkpoint_resume_bitwise(cs):
+    c = synth.config("C3", 128)
+    h, hu, hv, b, psi = synth.fill(c)
+    p = cs.params_from(c.params)
+    a = cs.csph_create(c.nx, c.ny, 1.0, p)
+    a.set_state(h, hu, hv, b, psi)
+    a.step(40)
+    full = a.get_state()
+    x = cs.csph_create(c.nx, c.ny, 1.0, p)
+    x.set_state(h, hu, hv, b, psi)
+    x.step(25)
+    mid = x.get_state()
+    y = cs.csph_create(c.nx, c.ny, 1.0, p)
+    y.set_state(*mid, psi)
+    y.step(15)
+    for u, v in zip(full, y.get_state()):
+        assert np.array_equal(u, v)
+
+
+def test_staged_and_fused_agree_on_dt_and_state(cs):
+    c = synth.config("C5", 512)
+    h, hu, hv, b, psi = synth.fill(c)
+    outs = []
+    for path in PATHS.values():
+        g = cs.csph_create(c.nx, c.ny, 1.0, cs.params_from(c.params, path=path))
+        g.set_state(h, hu, hv, b, psi)
+        g.step(30)
+        outs.append((g.get_dt_log(30)[0], g.get_state()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    for u, v in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(u, v)
