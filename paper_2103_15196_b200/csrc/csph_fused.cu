@@ -12,6 +12,7 @@
 //    Eq.7 maxima (warp shuffle + block max + one atomicMax per CTA) and the negative-depth flag.
 // The arithmetic per cell is the same sequence of IEEE operations as the oracle (-fmad=false).
 #include <climits>
+#include <cstdlib>
 
 #include "csph_launch.h"
 
@@ -19,8 +20,7 @@ namespace ck {
 
 namespace {
 
-constexpr int D = 8;   // ring slots
-constexpr int PF = 3;  // rows prefetched ahead (D >= PF + 5: rows L-4..L are live)
+// Ring of D slots with rows prefetched PF ahead; rows L-4..L are live, so D >= PF + 5.
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -60,7 +60,7 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-template <int NT, bool HASW>
+template <int NT, bool HASW, int D>
 struct Smem {
   static constexpr int NF = HASW ? 5 : 4;
   static constexpr int RW = NT + 4;  // ring row: data at [2, 2+NT), 16 B aligned
@@ -77,12 +77,22 @@ struct Smem {
 
 enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
 
-template <int NT, bool HASW>
-__global__ void __launch_bounds__(NT) fused_step_kernel(StripView S, Ctrl* __restrict__ C, Phys P,
-                                                        unsigned long long* __restrict__ gM,
-                                                        int row0, int row1, int TY) {
+// minmod without branches, bitwise equal to R's select form: when a and b are
+// both > 0 (or both < 0) the result is the one of smaller magnitude, exactly
+// copysign(min(|a|,|b|), a); otherwise +0.
+__device__ __forceinline__ double minmod_bf(double a, double b) {
+  const bool same = (a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0);
+  const double m = copysign(fmin(fabs(a), fabs(b)), a);
+  return same ? m : 0.0;
+}
+
+template <int NT, bool HASW, int D, int PF, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    fused_step_kernel(StripView S, Ctrl* __restrict__ C, Phys P,
+                      unsigned long long* __restrict__ gM, int row0, int row1, int TY) {
+  static_assert(D >= PF + 5, "ring too shallow");
   constexpr int TX = NT - 8;
-  using SM = Smem<NT, HASW>;
+  using SM = Smem<NT, HASW, D>;
   extern __shared__ __align__(128) unsigned char smraw[];
   SM& sm = *reinterpret_cast<SM*>(smraw);
 
@@ -142,40 +152,73 @@ __global__ void __launch_bounds__(NT) fused_step_kernel(StripView S, Ctrl* __res
 #define XG(a, dt) a[(t) + 1 + (dt)]
 
   // ---- carried registers (row offsets relative to the newest row L) ----
+  // Depth-1 carries are overwritten in place right after their last use, so the
+  // register allocator needs no moves for them.
   double v1 = 0, v2 = 0;          // v(L-1), v(L-2)
   double r1 = 0;                  // r(L-1)
   double gam1 = 0, gam2 = 0;      // gamma(L-1), gamma(L-2)
-  double eta1 = 0, b1c = 0;       // eta(L-1), b(L-1)
-  double PS1 = 0;                 // K2 y-face force (L-2|L-1)
+  double PS = 0;                  // K2 y-face force (L-2|L-1)
   double phix1 = 0;               // Phi_x(L-1)
   double Hh2 = 0;                 // H_half(L-2)
-  double PhS2 = 0;                // K5 y-face force (L-3|L-2)
+  double PhS = 0;                 // K5 y-face force (L-3|L-2)
   double phx2h = 0;               // Phi_half_x(L-2)
   double QLx3 = 0, QLy3 = 0;      // Q^L(L-3)
   double ut2 = 0, vt2 = 0, ut3 = 0, vt3 = 0;  // u~, v~ of rows L-2, L-3
   double J0y2 = 0, J0a2 = 0, J0y3 = 0, J0a3 = 0;
   double sy3[4] = {0, 0, 0, 0};   // sigma_y of row L-3 (eta, H, v~, u~)
-  double Fo[4] = {0, 0, 0, 0};    // own x-face flux of row L-2 (t|t+1)
   double dF3[4] = {0, 0, 0, 0};   // Delta F_x of row L-3
   double Gs[4] = {0, 0, 0, 0};    // y-face flux (L-4|L-3)
   unsigned long long m0 = 0, m1 = 0, m2 = 0;
   bool neg = false;
+  unsigned hist = 0;  // wet flags of rows L..L-4 of this column (bit 0 = row L)
 
   const bool col_out = (t >= 4) && (t < 4 + TX) && (col < nx);
 
+  // K8 epilogue for one cell: dry-momentum zeroing, negative-depth flag, stores,
+  // wall ghosts and the next step's Eq.7 terms.
+  auto store_update = [&](double Hn, double Qxn, double Qyn, double bn, double W3, int j) {
+    const bool wet = Hn > P.eps;
+    if (!wet) { Qxn = 0.0; Qyn = 0.0; }
+    if (Hn < -P.neg_tol) neg = true;
+    const size_t o = off(pitch, col, j);
+    oH[o] = Hn; oQx[o] = Qxn; oQy[o] = Qyn; ob[o] = bn;
+    // a cell within 3 of both walls of a small grid mirrors into both sides
+    const bool gx = col < 3 || col >= nx - 3;
+    const bool gy = (S.wall_lo && j < 3) || (S.wall_hi && j >= ny - 3);
+    if (gx || gy) {
+      int gc[3] = {col, col < 3 ? -1 - col : INT_MIN, col >= nx - 3 ? 2 * nx - 1 - col : INT_MIN};
+      int gr[3] = {j, (S.wall_lo && j < 3) ? -1 - j : INT_MIN,
+                   (S.wall_hi && j >= ny - 3) ? 2 * ny - 1 - j : INT_MIN};
+      for (int a = 0; a < 3; ++a)
+        for (int c2 = 0; c2 < 3; ++c2) {
+          if ((a | c2) == 0 || gc[a] == INT_MIN || gr[c2] == INT_MIN) continue;
+          const size_t g = off(pitch, gc[a], gr[c2]);
+          oH[g] = Hn; ob[g] = bn;
+          oQx[g] = a ? -Qxn : Qxn;
+          oQy[g] = c2 ? -Qyn : Qyn;
+        }
+    }
+    if (wet) {
+      double t1, t2, t3;
+      dt_terms(P, Hn, Qxn, Qyn, W3, t1, t2, t3);
+      unsigned long long a = dbits(t1), b = dbits(t2), c = dbits(t3);
+      m0 = a > m0 ? a : m0; m1 = b > m1 ? b : m1; m2 = c > m2 ? c : m2;
+    }
+  };
+
   for (int k = 0; k < niter; ++k) {
     const int L = rfirst + k;  // newest row (strip-local index)
+    const int km1 = k - 1 + D, km2 = k - 2 + D, km3 = k - 3 + D;  // non-negative ring rows
     // ================= phase A: K1 + K2 x-face + K2 y-face (row L) =================
     mbar_wait(&sm.bar[k % D], (unsigned)((k / D) & 1));
     const double H0 = RG(F_H, k, 0), b0 = RG(F_B, k, 0);
-    const double Qx0 = RG(F_QX, k, 0), Qy0 = RG(F_QY, k, 0);
     const bool w0 = H0 > P.eps;
     const double eta0 = H0 + b0;
     double r0 = 0.0, u0 = 0.0, v0 = 0.0, gam0 = 0.0;
     if (w0) {
       r0 = 1.0 / H0;
-      u0 = Qx0 * r0;
-      v0 = Qy0 * r0;
+      u0 = RG(F_QX, k, 0) * r0;
+      v0 = RG(F_QY, k, 0) * r0;
       if (P.fric) {
         double sp = sqrt(u0 * u0 + v0 * v0);
         gam0 = (P.cgam * sp) * (r0 * icbrt(H0));
@@ -184,125 +227,164 @@ __global__ void __launch_bounds__(NT) fused_step_kernel(StripView S, Ctrl* __res
     double PE0;
     {
       const double bR = RG(F_B, k, 1);
-      const double etaR = RG(F_H, k, 1) + bR;
-      PE0 = face_force(P.cP, eta0, b0, etaR, bR);
+      PE0 = face_force(P.cP, eta0, b0, RG(F_H, k, 1) + bR, bR);
     }
-    const double PN1 = face_force(P.cP, eta1, b1c, eta0, b0);  // face (L-1|L)
-    const double H1 = RG(F_H, k - 1 + D, 0);
+    const double H1 = RG(F_H, km1, 0), b1 = RG(F_B, km1, 0);
     const bool w1 = H1 > P.eps;
-    const double phiy1 = w1 ? -(PN1 + PS1) : 0.0;
+    const double eta1 = H1 + b1;
+    const double PN1 = face_force(P.cP, eta1, b1, eta0, b0);  // face (L-1|L)
+    const double phiy1 = w1 ? -(PN1 + PS) : 0.0;
+    PS = PN1;
     XG(sm.U[k & 1], 0) = u0;
     XG(sm.PE, 0) = PE0;
-    __syncthreads();  // ---------------------------------------------------- barrier 1
+    hist = ((hist << 1) | (w0 ? 1u : 0u)) & 31u;
+    // barrier 1; CTA-uniform: rows L-4..L are dry in every column of the tile
+    const bool cta_dry = __syncthreads_and(hist == 0u);
     if (t == 0 && k + PF < niter) {
       fence_proxy_async();
       issue(k + PF);
     }
-    // ================= phase B: K4 predictor + J0 (row L-1) =================
-    const double phix0 = w0 ? -(PE0 + XG(sm.PE, -1)) : 0.0;
-    double Hh1, ut1 = 0.0, vt1 = 0.0;
-    const int km1 = k - 1 + D;  // k-1 as a non-negative ring index
-    if (w1) {
-      const double* Up = sm.U[(k - 1) & 1];
-      double div = ((XG(Up, 1) - XG(Up, -1)) + (v0 - v2)) * P.inv_2h;
-      Hh1 = H1 * (1.0 - theta * div);
-      double f = P.fric ? 1.0 / (1.0 + theta * gam1) : 1.0;
-      ut1 = ((RG(F_QX, km1, 0) + theta * phix1) * f) * r1;
-      vt1 = ((RG(F_QY, km1, 0) + theta * phiy1) * f) * r1;
-    } else {
-      Hh1 = H1;
-    }
-    double J0x1 = 0.0, J0y1 = 0.0, J0a1 = 0.0;
-    if (P.transport) grass_gated(P, ut1, vt1, H1, J0x1, J0y1, J0a1);
-    // Delta F_x of row L-2 from the own face (t|t+1) and the west face (t-1|t)
-    double dF2[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) dF2[q] = Fo[q] - XG(sm.X4[q], -1);
-    XG(sm.X2[0], 0) = Hh1;
-    XG(sm.X2[1], 0) = ut1;
-    XG(sm.X2[2], 0) = vt1;
-    XG(sm.X2[3], 0) = J0x1;
-    XG(sm.X2[4], 0) = J0a1;
-    __syncthreads();  // ---------------------------------------------------- barrier 2
-    // ================= phase C: K5, sigma_x, K6 (row L-2), y-face flux (L-3|L-2) ======
-    const double b1 = RG(F_B, km1, 0);
-    const double eta1n = H1 + b1;  // eta(L-1) (== eta1 carried)
-    double PhE1;
-    {
-      const double bR = RG(F_B, km1, 1);
-      PhE1 = face_force(P.cP, Hh1 + b1, b1, XG(sm.X2[0], 1) + bR, bR);
-    }
-    double sx1[4];
-    {
-      const double HLm = RG(F_H, km1, -1), HRp = RG(F_H, km1, 1);
-      const double eL = HLm + RG(F_B, km1, -1), eR = HRp + RG(F_B, km1, 1);
-      sx1[0] = minmod(eta1n - eL, eR - eta1n);
-      sx1[1] = minmod(H1 - HLm, HRp - H1);
-      sx1[2] = minmod(ut1 - XG(sm.X2[1], -1), XG(sm.X2[1], 1) - ut1);
-      sx1[3] = minmod(vt1 - XG(sm.X2[2], -1), XG(sm.X2[2], 1) - vt1);
-    }
-    const int km2 = k - 2 + D, km3 = k - 3 + D;
-    const double H2 = RG(F_H, km2, 0), b2 = RG(F_B, km2, 0);
-    const bool w2 = H2 > P.eps;
-    const double PhN2 = face_force(P.cP, Hh2 + b2, b2, Hh1 + b1, b1);  // face (L-2|L-1)
-    double QLx2 = 0.0, QLy2 = 0.0;
-    if (w2) {
-      const double phy2h = -(PhN2 + PhS2);
-      double f1 = P.fric ? 1.0 / (1.0 + tau * gam2) : 1.0;
-      QLx2 = (RG(F_QX, km2, 0) + tau * phx2h) * f1;
-      QLy2 = (RG(F_QY, km2, 0) + tau * phy2h) * f1;
-    }
-    // y-face (L-3|L-2): sigma_y of row L-2 (always, it is carried), then HLL + sediment
-    const double H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
-    const bool w3 = H3 > P.eps;
-    const double eta2 = H2 + b2, eta3 = H3 + b3;
-    double sy2[4];
-    sy2[0] = minmod(eta2 - eta3, eta1n - eta2);
-    sy2[1] = minmod(H2 - H3, H1 - H2);
-    sy2[2] = minmod(vt2 - vt3, vt1 - vt2);
-    sy2[3] = minmod(ut2 - ut3, ut1 - ut2);
+    const int j = L - 3;  // row updated in this iteration
     double Gn[4] = {0.0, 0.0, 0.0, 0.0};  // (G^H, G^Qx, G^Qy, G^J) at (L-3|L-2)
-    if (w3 || w2) {
-      double F0, F1, F2;
-      hll_face(P.g, eta3 + 0.5 * sy3[0], H3 + 0.5 * sy3[1], vt3 + 0.5 * sy3[2],
-               ut3 + 0.5 * sy3[3], eta2 - 0.5 * sy2[0], H2 - 0.5 * sy2[1], vt2 - 0.5 * sy2[2],
-               ut2 - 0.5 * sy2[3], F0, F1, F2);
-      Gn[0] = F0;
-      Gn[2] = F1;  // normal momentum of a y-face -> Qy
-      Gn[1] = F2;  // tangential -> Qx
-      Gn[3] = P.transport ? sed_face(P, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2) : 0.0;
-    }
-    XG(sm.X3[0], 0) = PhE1;
+    if (cta_dry) {
+      // Dry fast path (exact): every quantity of R on rows L-4..L is either 0 or the
+      // identity, so only the carried window and the row L-3 update run.
+      phix1 = 0.0;
+      v2 = v1; v1 = 0.0;
+      r1 = 0.0;
+      gam2 = gam1; gam1 = 0.0;
+      Hh2 = H1;
+      phx2h = 0.0;
+      ut3 = ut2; vt3 = vt2; ut2 = 0.0; vt2 = 0.0;
+      J0y3 = J0y2; J0a3 = J0a2; J0y2 = 0.0; J0a2 = 0.0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) XG(sm.X3[1 + q], 0) = sx1[q];
-    __syncthreads();  // ---------------------------------------------------- barrier 3
-    // ================= phase D: Phi_half_x (row L-1), x-face flux (row L-1), K8 (row L-3) ===
-    const double phx1h = w1 ? -(PhE1 + XG(sm.X3[0], -1)) : 0.0;
-    double Fn[4] = {0.0, 0.0, 0.0, 0.0};
-    {
-      const double HR = RG(F_H, km1, 1);
-      const bool wR = HR > P.eps;
-      if (w1 || wR) {
-        const double bR = RG(F_B, km1, 1);
-        const double eR = HR + bR;
-        const double uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
-        double F0, F1, F2;
-        hll_face(P.g, eta1n + 0.5 * sx1[0], H1 + 0.5 * sx1[1], ut1 + 0.5 * sx1[2],
-                 vt1 + 0.5 * sx1[3], eR - 0.5 * XG(sm.X3[1], 1), HR - 0.5 * XG(sm.X3[2], 1),
-                 uR - 0.5 * XG(sm.X3[3], 1), vR - 0.5 * XG(sm.X3[4], 1), F0, F1, F2);
-        Fn[0] = F0;
-        Fn[1] = F1;  // normal momentum of an x-face -> Qx
-        Fn[2] = F2;  // tangential -> Qy
-        Fn[3] = P.transport ? sed_face(P, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
-                                       XG(sm.X2[4], 1), b1, bR)
-                            : 0.0;
+      for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = 0.0;
+    } else {
+      // ================= phase B: K4 predictor + J0 (row L-1) =================
+      const double phix0 = w0 ? -(PE0 + XG(sm.PE, -1)) : 0.0;
+      double Hh1 = H1, ut1 = 0.0, vt1 = 0.0;
+      if (w1) {
+        const double* Up = sm.U[(k - 1) & 1];
+        double div = ((XG(Up, 1) - XG(Up, -1)) + (v0 - v2)) * P.inv_2h;
+        Hh1 = H1 * (1.0 - theta * div);
+        double f = P.fric ? 1.0 / (1.0 + theta * gam1) : 1.0;
+        ut1 = ((RG(F_QX, km1, 0) + theta * phix1) * f) * r1;
+        vt1 = ((RG(F_QY, km1, 0) + theta * phiy1) * f) * r1;
       }
-    }
+      phix1 = phix0;
+      v2 = v1; v1 = v0;
+      r1 = r0;
+      double J0x1 = 0.0, J0y1 = 0.0, J0a1 = 0.0;
+      if (P.transport) grass_gated(P, ut1, vt1, H1, J0x1, J0y1, J0a1);
+      // Delta F_x of row L-2 from the own face (t|t+1) and the west face (t-1|t)
+      double dF2[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = Fn[q];
-    // ---- K8 update of row L-3 ----
-    const int j = L - 3;
+      for (int q = 0; q < 4; ++q) dF2[q] = XG(sm.X4[q], 0) - XG(sm.X4[q], -1);
+      XG(sm.X2[0], 0) = Hh1;
+      XG(sm.X2[1], 0) = ut1;
+      XG(sm.X2[2], 0) = vt1;
+      XG(sm.X2[3], 0) = J0x1;
+      XG(sm.X2[4], 0) = J0a1;
+      __syncthreads();  // -------------------------------------------------- barrier 2
+      // ============ phase C: K5, sigma_x (row L-1), K6 (row L-2), y-face (L-3|L-2) ====
+      double PhE1;
+      {
+        const double bR = RG(F_B, km1, 1);
+        PhE1 = face_force(P.cP, Hh1 + b1, b1, XG(sm.X2[0], 1) + bR, bR);
+      }
+      double sx1[4];
+      {
+        const double HLm = RG(F_H, km1, -1), HRp = RG(F_H, km1, 1);
+        const double eL = HLm + RG(F_B, km1, -1), eR = HRp + RG(F_B, km1, 1);
+        sx1[0] = minmod(eta1 - eL, eR - eta1);
+        sx1[1] = minmod(H1 - HLm, HRp - H1);
+        sx1[2] = minmod(ut1 - XG(sm.X2[1], -1), XG(sm.X2[1], 1) - ut1);
+        sx1[3] = minmod(vt1 - XG(sm.X2[2], -1), XG(sm.X2[2], 1) - vt1);
+      }
+      const double H2 = RG(F_H, km2, 0), b2 = RG(F_B, km2, 0);
+      const bool w2 = H2 > P.eps;
+      const double PhN2 = face_force(P.cP, Hh2 + b2, b2, Hh1 + b1, b1);  // face (L-2|L-1)
+      double QLx2 = 0.0, QLy2 = 0.0;
+      if (w2) {
+        const double phy2h = -(PhN2 + PhS);
+        double f1 = P.fric ? 1.0 / (1.0 + tau * gam2) : 1.0;
+        QLx2 = (RG(F_QX, km2, 0) + tau * phx2h) * f1;
+        QLy2 = (RG(F_QY, km2, 0) + tau * phy2h) * f1;
+      }
+      PhS = PhN2;
+      Hh2 = Hh1;
+      gam2 = gam1; gam1 = gam0;
+      // y-face (L-3|L-2): sigma_y of row L-2 (always: it is carried), HLL, sediment
+      const double H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
+      const bool w3 = H3 > P.eps;
+      const double eta2 = H2 + b2, eta3 = H3 + b3;
+      double sy2[4];
+      sy2[0] = minmod(eta2 - eta3, eta1 - eta2);
+      sy2[1] = minmod(H2 - H3, H1 - H2);
+      sy2[2] = minmod(vt2 - vt3, vt1 - vt2);
+      sy2[3] = minmod(ut2 - ut3, ut1 - ut2);
+      if (w3 || w2) {
+        double F0, F1, F2;
+        hll_face(P.g, eta3 + 0.5 * sy3[0], H3 + 0.5 * sy3[1], vt3 + 0.5 * sy3[2],
+                 ut3 + 0.5 * sy3[3], eta2 - 0.5 * sy2[0], H2 - 0.5 * sy2[1],
+                 vt2 - 0.5 * sy2[2], ut2 - 0.5 * sy2[3], F0, F1, F2);
+        Gn[0] = F0;
+        Gn[2] = F1;  // normal momentum of a y-face -> Qy
+        Gn[1] = F2;  // tangential -> Qx
+        Gn[3] = P.transport ? sed_face(P, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2) : 0.0;
+      }
+      ut3 = ut2; vt3 = vt2; ut2 = ut1; vt2 = vt1;
+      J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = J0a1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sy3[q] = sy2[q];
+      XG(sm.X3[0], 0) = PhE1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) XG(sm.X3[1 + q], 0) = sx1[q];
+      __syncthreads();  // -------------------------------------------------- barrier 3
+      // ====== phase D: Phi_half_x (row L-1), x-face flux (row L-1) ======
+      phx2h = w1 ? -(PhE1 + XG(sm.X3[0], -1)) : 0.0;
+      double Fn[4] = {0.0, 0.0, 0.0, 0.0};
+      {
+        const double HR = RG(F_H, km1, 1);
+        if (w1 || HR > P.eps) {
+          const double bR = RG(F_B, km1, 1);
+          const double eR = HR + bR;
+          const double uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
+          double F0, F1, F2;
+          hll_face(P.g, eta1 + 0.5 * sx1[0], H1 + 0.5 * sx1[1], ut1 + 0.5 * sx1[2],
+                   vt1 + 0.5 * sx1[3], eR - 0.5 * XG(sm.X3[1], 1), HR - 0.5 * XG(sm.X3[2], 1),
+                   uR - 0.5 * XG(sm.X3[3], 1), vR - 0.5 * XG(sm.X3[4], 1), F0, F1, F2);
+          Fn[0] = F0;
+          Fn[1] = F1;  // normal momentum of an x-face -> Qx
+          Fn[2] = F2;  // tangential -> Qy
+          Fn[3] = P.transport ? sed_face(P, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
+                                         XG(sm.X2[4], 1), b1, bR)
+                              : 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = Fn[q];
+      // ---- K8 update of row L-3 ----
+      if (col_out && j >= y0 && j < y1) {
+        const double W3 = HASW ? RG(F_W, km3, 0) : S.Wc;
+        const double dH = dF3[0] + (Gn[0] - Gs[0]);
+        const double dQx = dF3[1] + (Gn[1] - Gs[1]);
+        const double dQy = dF3[2] + (Gn[2] - Gs[2]);
+        const double dJ = dF3[3] + (Gn[3] - Gs[3]);
+        const double Hn = H3 - lam * dH;
+        double Qxn = QLx3 - lam * dQx;
+        double Qyn = QLy3 - lam * dQy;
+        const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
+        store_update(Hn, Qxn, Qyn, bn, W3, j);
+      }
+      QLx3 = QLx2; QLy3 = QLy2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { dF3[q] = dF2[q]; Gs[q] = Gn[q]; }
+      continue;
+    }
+    // ---- fast path: K8 update of row L-3 (all fluxes of the window are 0) ----
     if (col_out && j >= y0 && j < y1) {
+      const double H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
       const double W3 = HASW ? RG(F_W, km3, 0) : S.Wc;
       const double dH = dF3[0] + (Gn[0] - Gs[0]);
       const double dQx = dF3[1] + (Gn[1] - Gs[1]);
@@ -312,55 +394,11 @@ __global__ void __launch_bounds__(NT) fused_step_kernel(StripView S, Ctrl* __res
       double Qxn = QLx3 - lam * dQx;
       double Qyn = QLy3 - lam * dQy;
       const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
-      const bool wet = Hn > P.eps;
-      if (!wet) { Qxn = 0.0; Qyn = 0.0; }
-      if (Hn < -P.neg_tol) neg = true;
-      const size_t o = off(pitch, col, j);
-      oH[o] = Hn; oQx[o] = Qxn; oQy[o] = Qyn; ob[o] = bn;
-      // wall ghosts: x mirror, y mirror, corners.  A cell within 3 of
-      // both walls of a small grid mirrors into both sides.
-      {
-        int gc[3] = {col, col < 3 ? -1 - col : INT_MIN, col >= nx - 3 ? 2 * nx - 1 - col : INT_MIN};
-        int gr[3] = {j, (S.wall_lo && j < 3) ? -1 - j : INT_MIN,
-                     (S.wall_hi && j >= ny - 3) ? 2 * ny - 1 - j : INT_MIN};
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int c2 = 0; c2 < 3; ++c2) {
-            if ((a | c2) == 0 || gc[a] == INT_MIN || gr[c2] == INT_MIN) continue;
-            const size_t g = off(pitch, gc[a], gr[c2]);
-            oH[g] = Hn; ob[g] = bn;
-            oQx[g] = a ? -Qxn : Qxn;
-            oQy[g] = c2 ? -Qyn : Qyn;
-          }
-      }
-      if (wet) {
-        double t1, t2, t3;
-        dt_terms(P, Hn, Qxn, Qyn, W3, t1, t2, t3);
-        unsigned long long a = dbits(t1), b = dbits(t2), c = dbits(t3);
-        m0 = a > m0 ? a : m0; m1 = b > m1 ? b : m1; m2 = c > m2 ? c : m2;
-      }
+      store_update(Hn, Qxn, Qyn, bn, W3, j);
     }
-    // ---- rotate the carried window ----
-    v2 = v1; v1 = v0;
-    r1 = r0;
-    gam2 = gam1; gam1 = gam0;
-    eta1 = eta0; b1c = b0;
-    PS1 = PN1;
-    phix1 = phix0;
-    Hh2 = Hh1;
-    PhS2 = PhN2;
-    phx2h = phx1h;
-    QLx3 = QLx2; QLy3 = QLy2;
-    ut3 = ut2; vt3 = vt2; ut2 = ut1; vt2 = vt1;
-    J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = J0a1;
+    QLx3 = 0.0; QLy3 = 0.0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      sy3[q] = sy2[q];
-      Fo[q] = Fn[q];
-      dF3[q] = dF2[q];
-      Gs[q] = Gn[q];
-    }
+    for (int q = 0; q < 4; ++q) { dF3[q] = 0.0; Gs[q] = 0.0; sy3[q] = 0.0; }
   }
 #undef RG
 #undef XG
@@ -385,20 +423,38 @@ __global__ void __launch_bounds__(NT) fused_step_kernel(StripView S, Ctrl* __res
   }
 }
 
-template <int NT, bool HASW>
+template <int NT, bool HASW, int D, int PF, int MINB>
 void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM, int row0,
               int row1, int TY, cudaStream_t st) {
-  using SM = Smem<NT, HASW>;
+  using SM = Smem<NT, HASW, D>;
   constexpr int TX = NT - 8;
   static bool configured = false;
   const size_t smem = sizeof(SM);
   if (!configured) {
-    cudaFuncSetAttribute(fused_step_kernel<NT, HASW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(fused_step_kernel<NT, HASW, D, PF, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   dim3 grid((unsigned)((S.nx + TX - 1) / TX), (unsigned)((row1 - row0 + TY - 1) / TY));
-  fused_step_kernel<NT, HASW><<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY);
+  fused_step_kernel<NT, HASW, D, PF, MINB><<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY);
+}
+
+template <int NT, int D, int PF, int MINB>
+void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM, int row0,
+              int row1, int TY, cudaStream_t st) {
+  if (S.W)
+    launch_t<NT, true, D, PF, MINB>(S, C, P, gM, row0, row1, TY, st);
+  else
+    launch_t<NT, false, D, PF, MINB>(S, C, P, gM, row0, row1, TY, st);
+}
+
+int fused_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CSPH_FUSED_VARIANT");  // development knob
+    v = e ? atoi(e) : 5;
+  }
+  return v;
 }
 
 }  // namespace
@@ -407,10 +463,15 @@ void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long
                        int row0, int row1, int tile_rows, cudaStream_t st, long long* nlaunch) {
   if (row1 <= row0) return;
   int TY = tile_rows > 0 ? tile_rows : 128;
-  if (S.W)
-    launch_t<128, true>(S, C, P, gM, row0, row1, TY, st);
-  else
-    launch_t<128, false>(S, C, P, gM, row0, row1, TY, st);
+  switch (fused_variant()) {
+    case 0: launch_v<128, 8, 3, 1>(S, C, P, gM, row0, row1, TY, st); break;
+    case 2: launch_v<256, 6, 1, 2>(S, C, P, gM, row0, row1, TY, st); break;
+    case 3: launch_v<128, 7, 2, 4>(S, C, P, gM, row0, row1, TY, st); break;
+    case 4: launch_v<128, 6, 1, 3>(S, C, P, gM, row0, row1, TY, st); break;
+    case 5: launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, st); break;
+    case 6: launch_v<128, 10, 5, 3>(S, C, P, gM, row0, row1, TY, st); break;
+    default: launch_v<128, 6, 1, 4>(S, C, P, gM, row0, row1, TY, st); break;
+  }
   *nlaunch += 1;
 }
 
