@@ -156,6 +156,11 @@ int         csph_profile(csph_t*, int enable);
  * profiling was enabled. */
 int         csph_get_profile(csph_t*, double* main_kernel_ms, long long* steps_timed);
 
+/* Self-test: the kernels' branch-free correctly rounded reciprocal and square
+ * root against IEEE division and sqrt on n hashed inputs
+ * (and the tiny-argument square root on scaled ones); *mismatches must be 0. */
+int         csph_selftest_math(long long n, unsigned long long seed, long long* mismatches);
+
 /* Number of kernel launches the last csph_step issued (for the bench). */
 long long   csph_last_launch_count(csph_t*);
 

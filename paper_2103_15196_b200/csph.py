@@ -26,6 +26,7 @@ EXPORTS = [
     "csph_get_maxima", "csph_set_stream", "csph_strip_rows", "csph_destroy", "csph_strerror",
     "csph_last_error", "csph_nccl_id_bytes", "csph_make_nccl_id", "csph_create_dist",
     "csph_create_multi", "csph_last_launch_count", "csph_profile", "csph_get_profile",
+    "csph_selftest_math",
 ]
 
 
@@ -89,6 +90,8 @@ def lib():
         L.csph_make_nccl_id.argtypes = [ctypes.c_void_p]
         L.csph_profile.argtypes = [_vp, ctypes.c_int]
         L.csph_get_profile.argtypes = [_vp, _D, ctypes.POINTER(ctypes.c_longlong)]
+        L.csph_selftest_math.argtypes = [ctypes.c_longlong, ctypes.c_ulonglong,
+                                         ctypes.POINTER(ctypes.c_longlong)]
         L.csph_last_launch_count.argtypes = [_vp]
         L.csph_last_launch_count.restype = ctypes.c_longlong
         _lib = L
@@ -132,6 +135,12 @@ def csph_strip_rows(ny: int, nranks: int, rank: int):
     j0, j1 = ctypes.c_int(), ctypes.c_int()
     _check(lib().csph_strip_rows(ny, nranks, rank, ctypes.byref(j0), ctypes.byref(j1)), "csph_strip_rows")
     return j0.value, j1.value
+
+
+def csph_selftest_math(n: int, seed: int = 1) -> int:
+    bad = ctypes.c_longlong()
+    _check(lib().csph_selftest_math(n, seed, ctypes.byref(bad)), "csph_selftest_math")
+    return bad.value
 
 
 def csph_nccl_id_bytes() -> int:

@@ -271,6 +271,28 @@ __global__ void init_ctrl_kernel(Ctrl* C) {
 
 __global__ void clear_flags_kernel(Ctrl* C) { C->flags = 0; }
 
+// Self-test of the branch-free reciprocal / square root against IEEE / and sqrt
+// on counter-hashed positive normal inputs with exponents in [-lo, +lo].
+__global__ void selftest_math_kernel(long long n, unsigned long long seed, int lo,
+                                     unsigned long long* bad) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long st = (long long)gridDim.x * blockDim.x;
+  unsigned long long nb = 0;
+  for (; i < n; i += st) {
+    unsigned long long z = seed + (unsigned long long)i * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    unsigned long long e = 1023 - lo + (z >> 52) % (2 * lo + 1);
+    double x = __longlong_as_double((long long)((e << 52) | (z & 0xFFFFFFFFFFFFFull)));
+    if (rcp_nb(x) != 1.0 / x) nb++;
+    if (sqrt_nb(x) != sqrt(x)) nb++;
+    double t = x * 0x1p-1000;  // tiny and subnormal arguments of sqrt0nb
+    if (sqrt0nb(t) != sqrt(t)) nb++;
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
 }  // namespace
 
 namespace ck {
@@ -315,7 +337,8 @@ static int check_params(int nx, int ny, double dx, const csph_params* p) {
   if (!(dx > 0.0) || !std::isfinite(dx)) return fail(CSPH_EINVAL, "dx must be > 0");
   if (!(p->g > 0.0) || !std::isfinite(p->g)) return fail(CSPH_EINVAL, "g must be > 0");
   if (!(p->K > 0.0 && p->K < 1.0)) return fail(CSPH_EINVAL, "K must be in (0,1)");
-  if (!(p->eps_dry >= 0.0) || !std::isfinite(p->eps_dry)) return fail(CSPH_EINVAL, "eps_dry");
+  if (!(p->eps_dry >= 1e-200) || !(p->eps_dry < 1e200))
+    return fail(CSPH_EINVAL, "eps_dry must be in [1e-200, 1e200) (wet depths are divided by)");
   if (!(p->dt_max > 0.0)) return fail(CSPH_EINVAL, "dt_max must be > 0");
   if (!(p->neg_tol >= 0.0)) return fail(CSPH_EINVAL, "neg_tol must be >= 0");
   if (!(p->n_manning >= 0.0) || !std::isfinite(p->n_manning)) return fail(CSPH_EINVAL, "n_manning");
@@ -602,6 +625,22 @@ int csph_set_stream(csph_t* H, void* stream) {
 }
 
 long long csph_last_launch_count(csph_t* H) { return H ? H->launches : 0; }
+
+int csph_selftest_math(long long n, unsigned long long seed, long long* mismatches) {
+  if (n < 0 || !mismatches) return fail(CSPH_EINVAL, "bad argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return fail(CSPH_ECUDA, "no CUDA device");
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc((void**)&d, 8));
+  CK(cudaMemset(d, 0, 8));
+  selftest_math_kernel<<<1024, 256>>>(n, seed, 300, d);
+  CK(cudaGetLastError());
+  unsigned long long h = 0;
+  CK(cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost));
+  CK(cudaFree(d));
+  *mismatches = (long long)h;
+  return CSPH_OK;
+}
 
 int csph_profile(csph_t* H, int enable) {
   if (!H) return fail(CSPH_EINVAL, "handle is NULL");

@@ -77,6 +77,36 @@ struct Smem {
 
 enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
 
+// K7 hydrostatic step + HLL without branches: every case of
+// hll_face() is evaluated with the same operations and the result selected, so
+// the value is bitwise identical.  Callers have already excluded both-dry cells.
+__device__ __forceinline__ void hll_bf(double g, double eta_m, double H_m, double un_m,
+                                       double ut_m, double eta_p, double H_p, double un_p,
+                                       double ut_p, double& F0, double& F1, double& F2) {
+  const double bs = smax(eta_m - H_m, eta_p - H_p);
+  const double Hm = smax(0.0, eta_m - bs);
+  const double Hp = smax(0.0, eta_p - bs);
+  const bool dm = !(Hm > 0.0), dp = !(Hp > 0.0);
+  const double mm = Hm * un_m, mp = Hp * un_p;
+  const double cm = sqrt0nb(g * Hm), cp = sqrt0nb(g * Hp);
+  double SL, SR;
+  if (!dm && !dp) { SL = smin(un_m - cm, un_p - cp); SR = smax(un_m + cm, un_p + cp); }
+  else if (dp) { SL = un_m - cm; SR = un_m + 2.0 * cm; }
+  else { SL = un_p - 2.0 * cp; SR = un_p + cp; }
+  const bool none = dm && dp;
+  const double den = none ? 1.0 : (SR - SL);
+  const double inv = rcp_nb(den);
+  const double SLSR = SL * SR;
+  const double fl1 = mm * un_m, fl2 = mm * ut_m, fr1 = mp * un_p, fr2 = mp * ut_p;
+  const double h0 = ((SR * mm - SL * mp) + SLSR * (Hp - Hm)) * inv;
+  const double h1 = ((SR * fl1 - SL * fr1) + SLSR * (mp - mm)) * inv;
+  const double h2 = ((SR * fl2 - SL * fr2) + SLSR * (Hp * ut_p - Hm * ut_m)) * inv;
+  const bool up = SL >= 0.0, dn = SR <= 0.0;
+  F0 = none ? 0.0 : (up ? mm : (dn ? mp : h0));
+  F1 = none ? 0.0 : (up ? fl1 : (dn ? fr1 : h1));
+  F2 = none ? 0.0 : (up ? fl2 : (dn ? fr2 : h2));
+}
+
 // minmod without branches, bitwise equal to R's select form: when a and b are
 // both > 0 (or both < 0) the result is the one of smaller magnitude, exactly
 // copysign(min(|a|,|b|), a); otherwise +0.
@@ -215,14 +245,13 @@ __global__ void __launch_bounds__(NT, MINB)
     const bool w0 = H0 > P.eps;
     const double eta0 = H0 + b0;
     double r0 = 0.0, u0 = 0.0, v0 = 0.0, gam0 = 0.0;
-    if (w0) {
-      r0 = 1.0 / H0;
-      u0 = RG(F_QX, k, 0) * r0;
-      v0 = RG(F_QY, k, 0) * r0;
-      if (P.fric) {
-        double sp = sqrt(u0 * u0 + v0 * v0);
-        gam0 = (P.cgam * sp) * (r0 * icbrt(H0));
-      }
+    if (__any_sync(0xffffffffu, w0)) {  // warp-uniform; dry lanes compute on H = 1
+      const double Hs = w0 ? H0 : 1.0;
+      const double rr = rcp_nb(Hs);
+      const double uu = RG(F_QX, k, 0) * rr, vv = RG(F_QY, k, 0) * rr;
+      double gg = 0.0;
+      if (P.fric) gg = (P.cgam * sqrt0nb(uu * uu + vv * vv)) * (rr * icbrt(Hs));
+      r0 = w0 ? rr : 0.0; u0 = w0 ? uu : 0.0; v0 = w0 ? vv : 0.0; gam0 = w0 ? gg : 0.0;
     }
     double PE0;
     {
@@ -263,13 +292,14 @@ __global__ void __launch_bounds__(NT, MINB)
       // ================= phase B: K4 predictor + J0 (row L-1) =================
       const double phix0 = w0 ? -(PE0 + XG(sm.PE, -1)) : 0.0;
       double Hh1 = H1, ut1 = 0.0, vt1 = 0.0;
-      if (w1) {
+      if (__any_sync(0xffffffffu, w1)) {
         const double* Up = sm.U[(k - 1) & 1];
         double div = ((XG(Up, 1) - XG(Up, -1)) + (v0 - v2)) * P.inv_2h;
-        Hh1 = H1 * (1.0 - theta * div);
-        double f = P.fric ? 1.0 / (1.0 + theta * gam1) : 1.0;
-        ut1 = ((RG(F_QX, km1, 0) + theta * phix1) * f) * r1;
-        vt1 = ((RG(F_QY, km1, 0) + theta * phiy1) * f) * r1;
+        const double hh = H1 * (1.0 - theta * div);
+        const double f = P.fric ? rcp_nb(1.0 + theta * gam1) : 1.0;  // gam1 = 0 when dry
+        const double uu = ((RG(F_QX, km1, 0) + theta * phix1) * f) * r1;
+        const double vv = ((RG(F_QY, km1, 0) + theta * phiy1) * f) * r1;
+        Hh1 = w1 ? hh : H1; ut1 = w1 ? uu : 0.0; vt1 = w1 ? vv : 0.0;
       }
       phix1 = phix0;
       v2 = v1; v1 = v0;
@@ -305,11 +335,12 @@ __global__ void __launch_bounds__(NT, MINB)
       const bool w2 = H2 > P.eps;
       const double PhN2 = face_force(P.cP, Hh2 + b2, b2, Hh1 + b1, b1);  // face (L-2|L-1)
       double QLx2 = 0.0, QLy2 = 0.0;
-      if (w2) {
+      if (__any_sync(0xffffffffu, w2)) {
         const double phy2h = -(PhN2 + PhS);
-        double f1 = P.fric ? 1.0 / (1.0 + tau * gam2) : 1.0;
-        QLx2 = (RG(F_QX, km2, 0) + tau * phx2h) * f1;
-        QLy2 = (RG(F_QY, km2, 0) + tau * phy2h) * f1;
+        const double f1 = P.fric ? rcp_nb(1.0 + tau * gam2) : 1.0;
+        const double qx = (RG(F_QX, km2, 0) + tau * phx2h) * f1;
+        const double qy = (RG(F_QY, km2, 0) + tau * phy2h) * f1;
+        QLx2 = w2 ? qx : 0.0; QLy2 = w2 ? qy : 0.0;
       }
       PhS = PhN2;
       Hh2 = Hh1;
@@ -323,15 +354,17 @@ __global__ void __launch_bounds__(NT, MINB)
       sy2[1] = minmod(H2 - H3, H1 - H2);
       sy2[2] = minmod(vt2 - vt3, vt1 - vt2);
       sy2[3] = minmod(ut2 - ut3, ut1 - ut2);
-      if (w3 || w2) {
+      if (__any_sync(0xffffffffu, w3 || w2)) {
         double F0, F1, F2;
-        hll_face(P.g, eta3 + 0.5 * sy3[0], H3 + 0.5 * sy3[1], vt3 + 0.5 * sy3[2],
+        hll_bf(P.g, eta3 + 0.5 * sy3[0], H3 + 0.5 * sy3[1], vt3 + 0.5 * sy3[2],
                  ut3 + 0.5 * sy3[3], eta2 - 0.5 * sy2[0], H2 - 0.5 * sy2[1],
                  vt2 - 0.5 * sy2[2], ut2 - 0.5 * sy2[3], F0, F1, F2);
-        Gn[0] = F0;
-        Gn[2] = F1;  // normal momentum of a y-face -> Qy
-        Gn[1] = F2;  // tangential -> Qx
-        Gn[3] = P.transport ? sed_face(P, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2) : 0.0;
+        const bool any = w3 || w2;
+        Gn[0] = any ? F0 : 0.0;
+        Gn[2] = any ? F1 : 0.0;  // normal momentum of a y-face -> Qy
+        Gn[1] = any ? F2 : 0.0;  // tangential -> Qx
+        Gn[3] = (any && P.transport) ? sed_face(P, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2)
+                                     : 0.0;
       }
       ut3 = ut2; vt3 = vt2; ut2 = ut1; vt2 = vt1;
       J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = J0a1;
@@ -346,20 +379,21 @@ __global__ void __launch_bounds__(NT, MINB)
       double Fn[4] = {0.0, 0.0, 0.0, 0.0};
       {
         const double HR = RG(F_H, km1, 1);
-        if (w1 || HR > P.eps) {
+        const bool any = w1 || HR > P.eps;
+        if (__any_sync(0xffffffffu, any)) {
           const double bR = RG(F_B, km1, 1);
           const double eR = HR + bR;
           const double uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
           double F0, F1, F2;
-          hll_face(P.g, eta1 + 0.5 * sx1[0], H1 + 0.5 * sx1[1], ut1 + 0.5 * sx1[2],
+          hll_bf(P.g, eta1 + 0.5 * sx1[0], H1 + 0.5 * sx1[1], ut1 + 0.5 * sx1[2],
                    vt1 + 0.5 * sx1[3], eR - 0.5 * XG(sm.X3[1], 1), HR - 0.5 * XG(sm.X3[2], 1),
                    uR - 0.5 * XG(sm.X3[3], 1), vR - 0.5 * XG(sm.X3[4], 1), F0, F1, F2);
-          Fn[0] = F0;
-          Fn[1] = F1;  // normal momentum of an x-face -> Qx
-          Fn[2] = F2;  // tangential -> Qy
-          Fn[3] = P.transport ? sed_face(P, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
-                                         XG(sm.X2[4], 1), b1, bR)
-                              : 0.0;
+          Fn[0] = any ? F0 : 0.0;
+          Fn[1] = any ? F1 : 0.0;  // normal momentum of an x-face -> Qx
+          Fn[2] = any ? F2 : 0.0;  // tangential -> Qy
+          Fn[3] = (any && P.transport) ? sed_face(P, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
+                                                  XG(sm.X2[4], 1), b1, bR)
+                                       : 0.0;
         }
       }
 #pragma unroll

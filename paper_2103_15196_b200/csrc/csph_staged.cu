@@ -58,7 +58,7 @@ __global__ void k2_forces(StripView S, const Ctrl* __restrict__ C, Scratch T, Ra
   T.phiy[c] = -(PN + PS);
   if (P.fric) {
     double u = T.u[c], v = T.v[c];
-    double sp = sqrt(u * u + v * v);
+    double sp = sqrt0(u * u + v * v);
     T.gam[c] = (P.cgam * sp) * (T.r[c] * icbrt(S.H[p][c]));
   } else {
     T.gam[c] = 0.0;

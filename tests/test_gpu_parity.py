@@ -161,3 +161,9 @@ def test_staged_and_fused_agree_on_dt_and_state(cs):
     assert np.array_equal(outs[0][0], outs[1][0])
     for u, v in zip(outs[0][1], outs[1][1]):
         assert np.array_equal(u, v)
+
+
+def test_branch_free_rcp_sqrt_match_ieee(cs):
+    """the kernels' branch-free reciprocal and square root are
+    bitwise IEEE-correct on 2^28 hashed inputs (exponents -300..300)."""
+    assert cs.csph_selftest_math(1 << 28, 7) == 0
