@@ -223,12 +223,12 @@ int orc_set_walls(orc_t* o, int xlo, int xhi, int ylo, int yhi) {
 }
 
 /* Solid walls (reading #14): 3-layer mirror ghosts.  H, b, W copied, the
- * normal momentum negated, the tangential copied.  x-ghosts first on the
- * interior rows, then y-ghosts over the full padded width (corners = double
- * mirror). */
+ * normal momentum negated, the tangential copied.  x-ghosts first on every
+ * padded row (owned rows and any caller-supplied halo rows), then y-ghosts
+ * over the full padded width on wall sides (corners = double mirror). */
 static void mirror_fill(orc_t* o) {
   int nx = o->nx, ny = o->ny;
-  for (int j = 0; j < ny; ++j) {
+  for (int j = -G; j < ny + G; ++j) {
     for (int k = 0; k < G; ++k) {
       if (o->wall[0]) {
         size_t d = IDX(o, -1 - k, j), s = IDX(o, k, j);

@@ -113,6 +113,8 @@ struct Strip {
   cudaStream_t st = nullptr;
   bool own_stream = true;
   cudaEvent_t ev = nullptr;
+  cudaStream_t cst = nullptr;                        // NCCL stream (DIST)
+  cudaEvent_t ev_edge = nullptr, ev_int = nullptr, ev_comm = nullptr;
   std::vector<void*> allocs;
 };
 
@@ -197,9 +199,10 @@ __global__ void mirror_kernel(StripView S, const Ctrl* C, int flip) {
   double *H = S.H[q], *Qx = S.Qx[q], *Qy = S.Qy[q], *b = S.b[q];
   const int nx = S.nx, ny = S.ny;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
-  // phase 1: x-ghosts of owned rows (3 per side per row)
-  if (t < ny * 6) {
-    int j = t / 6, k = t % 6;
+  // x-ghosts (3 per side) of every padded row: owned rows and the halo/ghost rows
+  // (wall ghost rows are rewritten by mirror_y_kernel; halo rows by the exchange)
+  if (t < (ny + 2 * GY) * 6) {
+    int j = t / 6 - GY, k = t % 6;
     int gi, si;
     if (k < 3) { gi = -1 - k; si = k; }
     else { gi = nx + (k - 3); si = nx - 1 - (k - 3); }
@@ -298,7 +301,7 @@ __global__ void selftest_math_kernel(long long n, unsigned long long seed, int l
 namespace ck {
 void launch_mirror(const StripView& S, const Ctrl* C, int flip, cudaStream_t st,
                    long long* nlaunch) {
-  int n1 = S.ny * 6;
+  int n1 = (S.ny + 2 * GY) * 6;
   mirror_kernel<<<(n1 + 255) / 256, 256, 0, st>>>(S, C, flip);
   int n2 = (S.nx + 6) * 6;
   mirror_y_kernel<<<(n2 + 255) / 256, 256, 0, st>>>(S, C, flip);
@@ -411,6 +414,10 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
   CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
   s.own_stream = true;
   CK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&s.cst, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&s.ev_edge, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&s.ev_int, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&s.ev_comm, cudaEventDisableTiming));
   init_ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s.st));
@@ -424,6 +431,13 @@ static void strip_free(Strip& s) {
   s.allocs.clear();
   if (s.st && s.own_stream) cudaStreamDestroy(s.st);
   if (s.ev) cudaEventDestroy(s.ev);
+  if (s.cst) {
+    cudaStreamSynchronize(s.cst);
+    cudaStreamDestroy(s.cst);
+  }
+  for (cudaEvent_t e : {s.ev_edge, s.ev_int, s.ev_comm})
+    if (e) cudaEventDestroy(e);
+  s.cst = nullptr;
   s.st = nullptr;
   s.ev = nullptr;
 }
@@ -659,30 +673,47 @@ int csph_get_profile(csph_t* H, double* ms, long long* steps) {
 
 // -------- collective pieces of a step
 
+// NCCL halo exchange of buffer q: the 3 owned edge rows of each field (full padded
+// width, so x-ghosts travel too) to ranks r-1 / r+1 and the neighbours' rows into
+// the ghost rows.  No wrap-around (reading #18).
+static int halo_nccl(csph* H, int q, cudaStream_t stream) {
+  Strip& s = H->s[0];
+  const StripView& v = s.v;
+  const size_t cnt = (size_t)GY * v.pitch;
+  double* f[4] = {v.H[q], v.Qx[q], v.Qy[q], v.b[q]};
+  if (H->nranks == 1) return CSPH_OK;
+  NK(g_nccl.GroupStart());
+  for (int k = 0; k < 4; ++k) {
+    if (H->rank > 0) {
+      NK(g_nccl.Send(f[k] + off(v.pitch, -GX, 0), cnt, ncclFloat64, H->rank - 1, H->comm, stream));
+      NK(g_nccl.Recv(f[k] + off(v.pitch, -GX, -GY), cnt, ncclFloat64, H->rank - 1, H->comm, stream));
+    }
+    if (H->rank < H->nranks - 1) {
+      NK(g_nccl.Send(f[k] + off(v.pitch, -GX, v.ny - GY), cnt, ncclFloat64, H->rank + 1, H->comm,
+                     stream));
+      NK(g_nccl.Recv(f[k] + off(v.pitch, -GX, v.ny), cnt, ncclFloat64, H->rank + 1, H->comm,
+                     stream));
+    }
+  }
+  NK(g_nccl.GroupEnd());
+  return CSPH_OK;
+}
+
+// Eq.7 maxima over all ranks: max of the u64 bit patterns (exact, order-free).
+static int allreduce_nccl(csph* H, cudaStream_t stream) {
+  Strip& s = H->s[0];
+  NK(g_nccl.AllReduce(s.gM, s.gM, 3, ncclUint64, ncclMax, H->comm, stream));
+  return CSPH_OK;
+}
+
 // Halo exchange of buffer q (3 owned edge rows x 4 fields, full padded width)
 // and the maxima combine.  NCCL for DIST, peer copies for MULTI.
 static int exchange(csph* H, int q) {
   const size_t rowbytes = (size_t)H->s[0].v.pitch * 8;
   if (H->mode == DIST) {
-    Strip& s = H->s[0];
-    const StripView& v = s.v;
-    const size_t cnt = (size_t)GY * v.pitch;
-    double* f[4] = {v.H[q], v.Qx[q], v.Qy[q], v.b[q]};
-    NK(g_nccl.GroupStart());
-    for (int k = 0; k < 4; ++k) {
-      if (H->rank > 0) {
-        NK(g_nccl.Send(f[k] + off(v.pitch, -GX, 0), cnt, ncclFloat64, H->rank - 1, H->comm, s.st));
-        NK(g_nccl.Recv(f[k] + off(v.pitch, -GX, -GY), cnt, ncclFloat64, H->rank - 1, H->comm, s.st));
-      }
-      if (H->rank < H->nranks - 1) {
-        NK(g_nccl.Send(f[k] + off(v.pitch, -GX, v.ny - GY), cnt, ncclFloat64, H->rank + 1, H->comm, s.st));
-        NK(g_nccl.Recv(f[k] + off(v.pitch, -GX, v.ny), cnt, ncclFloat64, H->rank + 1, H->comm, s.st));
-      }
-    }
-    NK(g_nccl.AllReduce(s.gM, s.gM, 3, ncclUint64, ncclMax, H->comm, s.st));
-    NK(g_nccl.GroupEnd());
-    (void)rowbytes;
-    return CSPH_OK;
+    int st = halo_nccl(H, q, H->s[0].st);
+    if (st) return st;
+    return allreduce_nccl(H, H->s[0].st);
   }
   if (H->mode == MULTI) {
     const int n = (int)H->s.size();
@@ -882,8 +913,37 @@ int csph_step(csph_t* H, int nsteps) {
       H->evs.push_back(e);
     }
   }
+  const bool overlap = H->mode == DIST && H->nranks > 1 && H->p.path == CSPH_PATH_FUSED &&
+                       H->s[0].v.ny >= 2 * GY + 1;
   for (int n = 0; n < nsteps; ++n) {
     const int q = H->host_parity ^ 1;
+    if (overlap) {
+      // boundary rows first; their halo exchange (NCCL stream) overlaps the interior
+      Strip& s = H->s[0];
+      const int ny = s.v.ny, ty = H->p.tile_rows;
+      clear_flags_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
+      H->launches += 1;
+      if (H->profiling) CK(cudaEventRecord(H->evs[2 * n], s.st));
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, GY, ty, s.st, &H->launches);
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, ny - GY, ny, ty, s.st, &H->launches);
+      CK(cudaEventRecord(s.ev_edge, s.st));
+      CK(cudaStreamWaitEvent(s.cst, s.ev_edge, 0));
+      int st = halo_nccl(H, q, s.cst);
+      if (st) return st;
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, GY, ny - GY, ty, s.st, &H->launches);
+      if (H->profiling) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(s.ev_int, s.st));
+      CK(cudaStreamWaitEvent(s.cst, s.ev_int, 0));
+      if ((st = allreduce_nccl(H, s.cst))) return st;
+      CK(cudaEventRecord(s.ev_comm, s.cst));
+      CK(cudaStreamWaitEvent(s.st, s.ev_comm, 0));
+      ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 1);
+      H->launches += 1;
+      CK(cudaGetLastError());
+      H->host_parity = q;
+      continue;
+    }
     for (size_t si = 0; si < H->s.size(); ++si) {
       Strip& s = H->s[si];
       CK(cudaSetDevice(s.dev));

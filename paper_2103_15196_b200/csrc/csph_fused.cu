@@ -504,6 +504,8 @@ void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long
     case 4: launch_v<128, 6, 1, 3>(S, C, P, gM, row0, row1, TY, st); break;
     case 5: launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, st); break;
     case 6: launch_v<128, 10, 5, 3>(S, C, P, gM, row0, row1, TY, st); break;
+    case 7: launch_v<64, 8, 3, 6>(S, C, P, gM, row0, row1, TY, st); break;
+    case 8: launch_v<96, 8, 3, 4>(S, C, P, gM, row0, row1, TY, st); break;
     default: launch_v<128, 6, 1, 4>(S, C, P, gM, row0, row1, TY, st); break;
   }
   *nlaunch += 1;

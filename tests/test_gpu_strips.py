@@ -1,0 +1,69 @@
+"""Row-strip decomposition on one GPU.
+
+csph_create_multi puts several strips on the same device and moves the 3 halo
+rows with cudaMemcpyPeerAsync; csph_create_dist with one rank exercises the NCCL
+communicator and the allreduce-max of the Eq.7 maxima.  Max is exact and
+order-free, so every decomposition must be bitwise equal to the single grid."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cs():
+    from paper_2103_15196_b200 import build, csph
+    build.build()
+    return csph
+
+
+def single(cs, c, f, steps, path):
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, path=path))
+    g.set_state(*f)
+    g.step(steps)
+    return g.get_dt_log(steps)[0], g.get_state()
+
+
+@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("nstrips", [2, 3, 5])
+def test_multi_strips_bitwise(cs, nstrips, path):
+    c = synth.config("C4", 160, 203)
+    f = synth.fill(c)
+    dt0, ref = single(cs, c, f, 60, path)
+    g = cs.csph_create_multi(c.nx, c.ny, c.dx, cs.params_from(c.params, path=path), [0] * nstrips)
+    g.set_state(*f)
+    g.step(60)
+    dt, _ = g.get_dt_log(60)
+    assert np.array_equal(dt, dt0)
+    for a, r in zip(g.get_state(), ref):
+        assert np.array_equal(a, r)
+
+
+def test_multi_strips_set_state_rows(cs):
+    """Each strip can be fed from a row window covering its rows + halo."""
+    c = synth.config("C5", 144, 150)
+    f = synth.fill(c)
+    dt0, ref = single(cs, c, f, 30, 0)
+    g = cs.csph_create_multi(c.nx, c.ny, c.dx, cs.params_from(c.params), [0, 0])
+    g.set_state_rows(0, c.ny, *f)
+    g.step(30)
+    for a, r in zip(g.get_state(), ref):
+        assert np.array_equal(a, r)
+
+
+def test_dist_single_rank_nccl(cs):
+    """NCCL communicator of one rank: allreduce path, bitwise equal to single."""
+    c = synth.config("C3", 128, 96)
+    f = synth.fill(c)
+    dt0, ref = single(cs, c, f, 40, 0)
+    nid = cs.csph_make_nccl_id()
+    g = cs.csph_create_dist(c.nx, c.ny, c.dx, cs.params_from(c.params), 0, 1, 0, nid)
+    g.set_state(*f)
+    g.step(40)
+    dt, _ = g.get_dt_log(40)
+    assert np.array_equal(dt, dt0)
+    for a, r in zip(g.get_state(), ref):
+        assert np.array_equal(a, r)
+    g.destroy()
