@@ -75,7 +75,7 @@ def ncu_traffic(kernel_substr: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled every 50 ms during the timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -83,39 +83,49 @@ class ClockSampler:
 
     def __init__(self, gpu: int):
         self.gpu = gpu
+        self.proc = None
         self.rows = []
-        self.stop = threading.Event()
-        self.th = threading.Thread(target=self.run, daemon=True)
-
-    def run(self):
-        while not self.stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self.stop.wait(0.2)
 
     def __enter__(self):
-        self.th.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the first sample land before the timed region
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.stop.set()
-        self.th.join(timeout=10)
+        if self.proc is None:
+            return
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.splitlines():
+            r = [x.strip() for x in line.split(",")]
+            if len(r) >= 7:
+                self.rows.append(r)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
                     "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[1]) for r in self.rows) if v is not None]
+        mx = [v for v in (num(r[2]) for r in self.rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in self.rows for k in range(4)
-                          if len(r) > 3 + k and r[3 + k].lower() == "active"})
+                          if r[3 + k].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.rows)}
@@ -259,12 +269,15 @@ def run_ours(a, rank, world, local):
             "kernel_share_of_step": kern_ms_per / (ms / a.steps), "peak_source": peak_src}
     fp64 = None
     if tr and tr.get("fp64_inst_per_launch"):
-        # fp64 pipe: 64 DFMA lanes/clk/SM x 148 SMs at the sampled SM clock
-        inst_per_cell = tr["fp64_inst_per_launch"] / own_cells
+        # fp64 pipe roof: 64 fp64 lanes/clk/SM x 148 SMs x the SM clock
+        # sampled during the timed region; instruction count per launch from the
+        # committed ncu capture of the same workload (scaled to this rank's cells).
+        clk_mhz = None
+        inst = tr["fp64_inst_per_launch"] * own_cells / cells
         fp64 = {"bound": "alu", "unit": "fp64 thread-inst/s",
-                "inst_per_cell": inst_per_cell,
-                "achieved": tr["fp64_inst_per_launch"] / (kern_ms_per / 1e3),
-                "pipe_active_pct": tr.get("fp64_pipe_pct")}
+                "inst_per_cell": inst / own_cells,
+                "achieved": inst / (kern_ms_per / 1e3),
+                "pipe_active_pct_ncu": tr.get("fp64_pipe_pct")}
 
     # ---- end to end through the public API: host (pinned) -> device -> host ----
     e2e = None
@@ -321,6 +334,10 @@ def run_ours(a, rank, world, local):
             "cpu_baseline": cpu,
         }
         if fp64:
+            ck = line["clocks"].get("sm_mhz") or 1965.0
+            fp64["peak"] = 64 * 148 * ck * 1e6
+            fp64["frac"] = fp64["achieved"] / fp64["peak"]
+            fp64["peak_source"] = f"64 DFMA lanes/clk/SM x 148 SMs x {ck:.0f} MHz (sampled)"
             line["roofline_fp64"] = fp64
         print(json.dumps(line), flush=True)
     g.destroy()
