@@ -236,11 +236,64 @@ __global__ void __launch_bounds__(NT, MINB)
     }
   };
 
+  // The dry decision for iteration k is made at the last barrier of iteration k-1
+  // (a __syncthreads_and over "rows L-4..L of my column are dry").
+  mbar_wait(&sm.bar[0], 0u);
+  hist = RG(F_H, 0, 0) > P.eps ? 1u : 0u;
+  bool cta_dry = __syncthreads_and(hist == 0u);
+
   for (int k = 0; k < niter; ++k) {
     const int L = rfirst + k;  // newest row (strip-local index)
     const int km1 = k - 1 + D, km2 = k - 2 + D, km3 = k - 3 + D;  // non-negative ring rows
+    // the slot of row k+PF last held row k+PF-D <= k-5, last read before the previous
+    // iteration's barriers
+    if (t == 0 && k + PF < niter) {
+      fence_proxy_async();
+      issue(k + PF);
+    }
+    auto next_hist = [&]() {
+      if (k + 1 < niter) {
+        mbar_wait(&sm.bar[(k + 1) % D], (unsigned)(((k + 1) / D) & 1));
+        hist = ((hist << 1) | (RG(F_H, k + 1, 0) > P.eps ? 1u : 0u)) & 31u;
+      }
+    };
+    const int j = L - 3;  // row updated in this iteration
+    double Gn[4] = {0.0, 0.0, 0.0, 0.0};  // (G^H, G^Qx, G^Qy, G^J) at (L-3|L-2)
+    if (cta_dry) {
+      // Dry fast path (exact): every quantity of R on rows L-4..L is either 0 or the
+      // identity (DESIGN.md 7.1), so only the carried window and the row L-3 update run.
+      const double H1 = RG(F_H, km1, 0);
+      phix1 = 0.0;
+      v2 = v1; v1 = 0.0;
+      r1 = 0.0;
+      gam2 = gam1; gam1 = 0.0;
+      Hh2 = H1;
+      phx2h = 0.0;
+      ut3 = ut2; vt3 = vt2; ut2 = 0.0; vt2 = 0.0;
+      J0y3 = J0y2; J0a3 = J0a2; J0y2 = 0.0; J0a2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = 0.0;
+      if (col_out && j >= y0 && j < y1) {
+        const double H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
+        const double W3 = HASW ? RG(F_W, km3, 0) : S.Wc;
+        const double dH = dF3[0] + (Gn[0] - Gs[0]);
+        const double dQx = dF3[1] + (Gn[1] - Gs[1]);
+        const double dQy = dF3[2] + (Gn[2] - Gs[2]);
+        const double dJ = dF3[3] + (Gn[3] - Gs[3]);
+        const double Hn = H3 - lam * dH;
+        double Qxn = QLx3 - lam * dQx;
+        double Qyn = QLy3 - lam * dQy;
+        const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
+        store_update(Hn, Qxn, Qyn, bn, W3, j);
+      }
+      QLx3 = 0.0; QLy3 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { dF3[q] = 0.0; Gs[q] = 0.0; sy3[q] = 0.0; }
+      next_hist();
+      cta_dry = __syncthreads_and(hist == 0u);
+      continue;
+    }
     // ================= phase A: K1 + K2 x-face + K2 y-face (row L) =================
-    mbar_wait(&sm.bar[k % D], (unsigned)((k / D) & 1));
     const double H0 = RG(F_H, k, 0), b0 = RG(F_B, k, 0);
     const bool w0 = H0 > P.eps;
     const double eta0 = H0 + b0;
@@ -266,29 +319,8 @@ __global__ void __launch_bounds__(NT, MINB)
     PS = PN1;
     XG(sm.U[k & 1], 0) = u0;
     XG(sm.PE, 0) = PE0;
-    hist = ((hist << 1) | (w0 ? 1u : 0u)) & 31u;
-    // barrier 1; CTA-uniform: rows L-4..L are dry in every column of the tile
-    const bool cta_dry = __syncthreads_and(hist == 0u);
-    if (t == 0 && k + PF < niter) {
-      fence_proxy_async();
-      issue(k + PF);
-    }
-    const int j = L - 3;  // row updated in this iteration
-    double Gn[4] = {0.0, 0.0, 0.0, 0.0};  // (G^H, G^Qx, G^Qy, G^J) at (L-3|L-2)
-    if (cta_dry) {
-      // Dry fast path (exact): every quantity of R on rows L-4..L is either 0 or the
-      // identity (DESIGN.md 7.3), so only the carried window and the row L-3 update run.
-      phix1 = 0.0;
-      v2 = v1; v1 = 0.0;
-      r1 = 0.0;
-      gam2 = gam1; gam1 = 0.0;
-      Hh2 = H1;
-      phx2h = 0.0;
-      ut3 = ut2; vt3 = vt2; ut2 = 0.0; vt2 = 0.0;
-      J0y3 = J0y2; J0a3 = J0a2; J0y2 = 0.0; J0a2 = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = 0.0;
-    } else {
+    __syncthreads();  // ---------------------------------------------------- barrier 1
+    {
       // ================= phase B: K4 predictor + J0 (row L-1) =================
       const double phix0 = w0 ? -(PE0 + XG(sm.PE, -1)) : 0.0;
       double Hh1 = H1, ut1 = 0.0, vt1 = 0.0;
@@ -373,7 +405,8 @@ __global__ void __launch_bounds__(NT, MINB)
       XG(sm.X3[0], 0) = PhE1;
 #pragma unroll
       for (int q = 0; q < 4; ++q) XG(sm.X3[1 + q], 0) = sx1[q];
-      __syncthreads();  // -------------------------------------------------- barrier 3
+      next_hist();
+      const bool dry_next = __syncthreads_and(hist == 0u);  // ---------------- barrier 3
       // ====== phase D: Phi_half_x (row L-1), x-face flux (row L-1) ======
       phx2h = w1 ? -(PhE1 + XG(sm.X3[0], -1)) : 0.0;
       double Fn[4] = {0.0, 0.0, 0.0, 0.0};
@@ -414,25 +447,8 @@ __global__ void __launch_bounds__(NT, MINB)
       QLx3 = QLx2; QLy3 = QLy2;
 #pragma unroll
       for (int q = 0; q < 4; ++q) { dF3[q] = dF2[q]; Gs[q] = Gn[q]; }
-      continue;
+      cta_dry = dry_next;
     }
-    // ---- fast path: K8 update of row L-3 (all fluxes of the window are 0) ----
-    if (col_out && j >= y0 && j < y1) {
-      const double H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
-      const double W3 = HASW ? RG(F_W, km3, 0) : S.Wc;
-      const double dH = dF3[0] + (Gn[0] - Gs[0]);
-      const double dQx = dF3[1] + (Gn[1] - Gs[1]);
-      const double dQy = dF3[2] + (Gn[2] - Gs[2]);
-      const double dJ = dF3[3] + (Gn[3] - Gs[3]);
-      const double Hn = H3 - lam * dH;
-      double Qxn = QLx3 - lam * dQx;
-      double Qyn = QLy3 - lam * dQy;
-      const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
-      store_update(Hn, Qxn, Qyn, bn, W3, j);
-    }
-    QLx3 = 0.0; QLy3 = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) { dF3[q] = 0.0; Gs[q] = 0.0; sy3[q] = 0.0; }
   }
 #undef RG
 #undef XG
@@ -506,6 +522,8 @@ void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long
     case 6: launch_v<128, 10, 5, 3>(S, C, P, gM, row0, row1, TY, st); break;
     case 7: launch_v<64, 8, 3, 6>(S, C, P, gM, row0, row1, TY, st); break;
     case 8: launch_v<96, 8, 3, 4>(S, C, P, gM, row0, row1, TY, st); break;
+    case 9: launch_v<128, 12, 7, 2>(S, C, P, gM, row0, row1, TY, st); break;
+    case 10: launch_v<128, 9, 4, 3>(S, C, P, gM, row0, row1, TY, st); break;
     default: launch_v<128, 6, 1, 4>(S, C, P, gM, row0, row1, TY, st); break;
   }
   *nlaunch += 1;
