@@ -322,6 +322,7 @@ static Phys make_phys(double dx, const csph_params& p) {
   double c2 = p.C_Sh * p.C_Sh;
   P.kappa = ((c2 * c2) * c2) * (p.d50 * p.d50);
   P.cP = p.g / (2.0 * dx);
+  P.cPh = 0.5 * P.cP;
   P.cgam = p.g * (p.n_manning * p.n_manning);
   P.inv_h = 1.0 / dx;
   P.inv_2h = 1.0 / (2.0 * dx);

@@ -91,8 +91,8 @@ __device__ __forceinline__ void hll_bf(double g, double eta_m, double H_m, doubl
   const double cm = sqrt0nb(g * Hm), cp = sqrt0nb(g * Hp);
   double SL, SR;
   if (!dm && !dp) { SL = smin(un_m - cm, un_p - cp); SR = smax(un_m + cm, un_p + cp); }
-  else if (dp) { SL = un_m - cm; SR = un_m + 2.0 * cm; }
-  else { SL = un_p - 2.0 * cp; SR = un_p + cp; }
+  else if (dp) { SL = un_m - cm; SR = fma(2.0, cm, un_m); }
+  else { SL = fma(-2.0, cp, un_p); SR = un_p + cp; }
   const bool none = dm && dp;
   const double den = none ? 1.0 : (SR - SL);
   const double inv = rcp_nb(den);
@@ -309,12 +309,12 @@ __global__ void __launch_bounds__(NT, MINB)
     double PE0;
     {
       const double bR = RG(F_B, k, 1);
-      PE0 = face_force(P.cP, eta0, b0, RG(F_H, k, 1) + bR, bR);
+      PE0 = face_force_h(P.cPh, eta0, b0, RG(F_H, k, 1) + bR, bR);
     }
     const double H1 = RG(F_H, km1, 0), b1 = RG(F_B, km1, 0);
     const bool w1 = H1 > P.eps;
     const double eta1 = H1 + b1;
-    const double PN1 = face_force(P.cP, eta1, b1, eta0, b0);  // face (L-1|L)
+    const double PN1 = face_force_h(P.cPh, eta1, b1, eta0, b0);  // face (L-1|L)
     const double phiy1 = w1 ? -(PN1 + PS) : 0.0;
     PS = PN1;
     XG(sm.U[k & 1], 0) = u0;
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(NT, MINB)
       double PhE1;
       {
         const double bR = RG(F_B, km1, 1);
-        PhE1 = face_force(P.cP, Hh1 + b1, b1, XG(sm.X2[0], 1) + bR, bR);
+        PhE1 = face_force_h(P.cPh, Hh1 + b1, b1, XG(sm.X2[0], 1) + bR, bR);
       }
       double sx1[4];
       {
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(NT, MINB)
       }
       const double H2 = RG(F_H, km2, 0), b2 = RG(F_B, km2, 0);
       const bool w2 = H2 > P.eps;
-      const double PhN2 = face_force(P.cP, Hh2 + b2, b2, Hh1 + b1, b1);  // face (L-2|L-1)
+      const double PhN2 = face_force_h(P.cPh, Hh2 + b2, b2, Hh1 + b1, b1);  // face (L-2|L-1)
       double QLx2 = 0.0, QLy2 = 0.0;
       if (__any_sync(0xffffffffu, w2)) {
         const double phy2h = -(PhN2 + PhS);
@@ -388,9 +388,9 @@ __global__ void __launch_bounds__(NT, MINB)
       sy2[3] = minmod(ut2 - ut3, ut1 - ut2);
       if (__any_sync(0xffffffffu, w3 || w2)) {
         double F0, F1, F2;
-        hll_bf(P.g, eta3 + 0.5 * sy3[0], H3 + 0.5 * sy3[1], vt3 + 0.5 * sy3[2],
-                 ut3 + 0.5 * sy3[3], eta2 - 0.5 * sy2[0], H2 - 0.5 * sy2[1],
-                 vt2 - 0.5 * sy2[2], ut2 - 0.5 * sy2[3], F0, F1, F2);
+        hll_bf(P.g, fma(0.5, sy3[0], eta3), fma(0.5, sy3[1], H3), fma(0.5, sy3[2], vt3),
+                 fma(0.5, sy3[3], ut3), fma(-0.5, sy2[0], eta2), fma(-0.5, sy2[1], H2),
+                 fma(-0.5, sy2[2], vt2), fma(-0.5, sy2[3], ut2), F0, F1, F2);
         const bool any = w3 || w2;
         Gn[0] = any ? F0 : 0.0;
         Gn[2] = any ? F1 : 0.0;  // normal momentum of a y-face -> Qy
@@ -418,9 +418,9 @@ __global__ void __launch_bounds__(NT, MINB)
           const double eR = HR + bR;
           const double uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
           double F0, F1, F2;
-          hll_bf(P.g, eta1 + 0.5 * sx1[0], H1 + 0.5 * sx1[1], ut1 + 0.5 * sx1[2],
-                   vt1 + 0.5 * sx1[3], eR - 0.5 * XG(sm.X3[1], 1), HR - 0.5 * XG(sm.X3[2], 1),
-                   uR - 0.5 * XG(sm.X3[3], 1), vR - 0.5 * XG(sm.X3[4], 1), F0, F1, F2);
+          hll_bf(P.g, fma(0.5, sx1[0], eta1), fma(0.5, sx1[1], H1), fma(0.5, sx1[2], ut1),
+                   fma(0.5, sx1[3], vt1), fma(-0.5, XG(sm.X3[1], 1), eR), fma(-0.5, XG(sm.X3[2], 1), HR),
+                   fma(-0.5, XG(sm.X3[3], 1), uR), fma(-0.5, XG(sm.X3[4], 1), vR), F0, F1, F2);
           Fn[0] = any ? F0 : 0.0;
           Fn[1] = any ? F1 : 0.0;  // normal momentum of an x-face -> Qx
           Fn[2] = any ? F2 : 0.0;  // tangential -> Qy
