@@ -236,6 +236,7 @@ def run_ours(a, rank, world, local):
     torch.cuda.synchronize()
     barrier()
     g.profile(True)
+    g.reset_tile_stats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -247,6 +248,7 @@ def run_ours(a, rank, world, local):
         barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
     launches = g.last_launch_count()
+    tiles = g.tile_stats()
     kern_ms, kern_steps = g.get_profile()
     g.profile(False)
     cells = c.nx * c.ny
@@ -260,12 +262,21 @@ def run_ours(a, rank, world, local):
     bpc = 72 if psi_field else 64  # algorithmic bytes per cell-update
     own_cells = c.nx * (j1 - j0)
     kern_ms_per = kern_ms / max(kern_steps, 1)
-    achieved = bpc * own_cells / (kern_ms_per / 1e3) / 1e9
+    # HGS: marched tiles move bpc B/cell, identity-copied tiles read H, b (+W) and write
+    # 4 fields, skipped tiles move nothing
+    ntile = max(sum(tiles), 1)
+    f_march, f_copy, f_skip = (x / ntile for x in tiles)
+    bpc_copy = (24 if psi_field else 16) + 32
+    bytes_per_step = own_cells * (bpc * f_march + bpc_copy * f_copy)
+    achieved = bytes_per_step / (kern_ms_per / 1e3) / 1e9
     tr = ncu_traffic("fused_step_kernel" if path == csph.CSPH_PATH_FUSED else "k7_fluxes")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": (tr or {}).get("dram_bytes_per_launch"),
             "kernel": "fused_step_kernel" if path == csph.CSPH_PATH_FUSED else "staged K1..K8",
-            "algorithmic_bytes_per_cell": bpc, "kernel_ms_per_launch": kern_ms_per,
+            "algorithmic_bytes_per_cell": bpc,
+            "algorithmic_bytes_per_launch": bytes_per_step,
+            "hgs_tiles": {"marched": f_march, "identity_copy": f_copy, "skipped": f_skip},
+            "kernel_ms_per_launch": kern_ms_per,
             "kernel_share_of_step": kern_ms_per / (ms / a.steps), "peak_source": peak_src}
     fp64 = None
     if tr and tr.get("fp64_inst_per_launch"):

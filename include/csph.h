@@ -65,7 +65,9 @@ typedef struct {
   int    precision;  /* 64 (fp64; the only mode of this build) */
   int    device;     /* CUDA ordinal for csph_create (single-process use) */
   int    path;       /* CSPH_PATH_FUSED (default) or CSPH_PATH_STAGED */
-  int    tile_rows;  /* fused path: rows marched per CTA (0 = auto) */
+  int    tile_rows;  /* fused path: rows marched per CTA (0 = auto = 128) */
+  int    hgs;        /* 1 (default): skip tiles whose neighbourhood is dry (the paper's
+                        HGS; exact); 0: march every tile */
 } csph_params;
 
 /* Fill *p with the defaults above. */
@@ -155,6 +157,13 @@ int         csph_profile(csph_t*, int enable);
 /* Accumulated main-kernel device time [ms] and number of steps timed since
  * profiling was enabled. */
 int         csph_get_profile(csph_t*, double* main_kernel_ms, long long* steps_timed);
+
+/* HGS tile counters of the fused path since csph_set_state (or the last reset):
+ * counts[0] tiles marched, counts[1] tiles updated by an identity copy (dry
+ * neighbourhood), counts[2] tiles skipped (dry and already identical in both
+ * state buffers).  A tile is the 120 x tile_rows chunk one CTA owns. */
+int         csph_get_tile_stats(csph_t*, long long counts[3]);
+int         csph_reset_tile_stats(csph_t*);
 
 /* Self-test: the kernels' branch-free correctly rounded reciprocal and square
  * root against IEEE division and sqrt on n hashed inputs

@@ -26,7 +26,7 @@ EXPORTS = [
     "csph_get_maxima", "csph_set_stream", "csph_strip_rows", "csph_destroy", "csph_strerror",
     "csph_last_error", "csph_nccl_id_bytes", "csph_make_nccl_id", "csph_create_dist",
     "csph_create_multi", "csph_last_launch_count", "csph_profile", "csph_get_profile",
-    "csph_selftest_math",
+    "csph_selftest_math", "csph_get_tile_stats", "csph_reset_tile_stats",
 ]
 
 
@@ -38,6 +38,7 @@ class csph_params(ctypes.Structure):
         ("C_J", ctypes.c_double), ("C_Sh", ctypes.c_double), ("d50", ctypes.c_double),
         ("q_plus", ctypes.c_double), ("q_minus", ctypes.c_double), ("precision", ctypes.c_int),
         ("device", ctypes.c_int), ("path", ctypes.c_int), ("tile_rows", ctypes.c_int),
+        ("hgs", ctypes.c_int),
     ]
 
 
@@ -92,6 +93,8 @@ def lib():
         L.csph_get_profile.argtypes = [_vp, _D, ctypes.POINTER(ctypes.c_longlong)]
         L.csph_selftest_math.argtypes = [ctypes.c_longlong, ctypes.c_ulonglong,
                                          ctypes.POINTER(ctypes.c_longlong)]
+        L.csph_get_tile_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_longlong)]
+        L.csph_reset_tile_stats.argtypes = [_vp]
         L.csph_last_launch_count.argtypes = [_vp]
         L.csph_last_launch_count.restype = ctypes.c_longlong
         _lib = L
@@ -227,6 +230,14 @@ class Csph:
         ms, n = ctypes.c_double(), ctypes.c_longlong()
         _check(lib().csph_get_profile(self.h, ctypes.byref(ms), ctypes.byref(n)), "csph_get_profile")
         return ms.value, n.value
+
+    def tile_stats(self):
+        c = (ctypes.c_longlong * 3)()
+        _check(lib().csph_get_tile_stats(self.h, c), "csph_get_tile_stats")
+        return tuple(c)
+
+    def reset_tile_stats(self):
+        return _check(lib().csph_reset_tile_stats(self.h), "csph_reset_tile_stats")
 
     def last_launch_count(self) -> int:
         return lib().csph_last_launch_count(self.h)

@@ -109,6 +109,10 @@ struct Strip {
   double* dtlog = nullptr;           // device [LOGCAP]
   int* limlog = nullptr;             // device [LOGCAP]
   int* dflags = nullptr;             // device validation flags
+  unsigned char* tflag = nullptr;    // HGS tile wet flags [2][ntiles]
+  unsigned char* tstate = nullptr;   // HGS identity-copy counters [ntiles]
+  unsigned long long* hstats = nullptr;  // HGS tile counters: marched, copied, skipped
+  int ntx = 0, nty = 0;
   double* Wbuf = nullptr;            // device psi -> W field (when psi varies)
   cudaStream_t st = nullptr;
   bool own_stream = true;
@@ -397,6 +401,18 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
   if ((st = dalloc(s, (void**)&s.dtlog, LOGCAP * sizeof(double)))) return st;
   if ((st = dalloc(s, (void**)&s.limlog, LOGCAP * sizeof(int)))) return st;
   if ((st = dalloc(s, (void**)&s.dflags, 4 * sizeof(int)))) return st;
+  {
+    const int TY = H->p.tile_rows > 0 ? H->p.tile_rows : 128;
+    s.ntx = (v.nx + FUSED_TX - 1) / FUSED_TX;
+    s.nty = (v.ny + TY - 1) / TY;
+    const size_t nt = (size_t)s.ntx * s.nty;
+    if ((st = dalloc(s, (void**)&s.tflag, 2 * nt))) return st;
+    if ((st = dalloc(s, (void**)&s.tstate, nt))) return st;
+    CK(cudaMemset(s.tflag, 1, 2 * nt));
+    CK(cudaMemset(s.tstate, 0, nt));
+    if ((st = dalloc(s, (void**)&s.hstats, 4 * sizeof(unsigned long long)))) return st;
+    CK(cudaMemset(s.hstats, 0, 4 * sizeof(unsigned long long)));
+  }
   CK(cudaMemset(s.gM, 0, 4 * sizeof(unsigned long long)));
   CK(cudaMemset(s.Mlast, 0, 4 * sizeof(double)));
   if (staged) {
@@ -466,6 +482,7 @@ void csph_default_params(csph_params* p) {
   p->device = 0;
   p->path = CSPH_PATH_FUSED;
   p->tile_rows = 0;
+  p->hgs = 1;
 }
 
 const char* csph_last_error(void) { return g_err.c_str(); }
@@ -654,6 +671,28 @@ int csph_selftest_math(long long n, unsigned long long seed, long long* mismatch
   CK(cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost));
   CK(cudaFree(d));
   *mismatches = (long long)h;
+  return CSPH_OK;
+}
+
+int csph_get_tile_stats(csph_t* H, long long counts[3]) {
+  if (!H || !counts) return fail(CSPH_EINVAL, "bad argument");
+  counts[0] = counts[1] = counts[2] = 0;
+  for (auto& s : H->s) {
+    unsigned long long c[4];
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.st));
+    CK(cudaMemcpy(c, s.hstats, sizeof c, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 3; ++k) counts[k] += (long long)c[k];
+  }
+  return CSPH_OK;
+}
+
+int csph_reset_tile_stats(csph_t* H) {
+  if (!H) return fail(CSPH_EINVAL, "bad argument");
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaMemsetAsync(s.hstats, 0, 4 * sizeof(unsigned long long), s.st));
+  }
   return CSPH_OK;
 }
 
@@ -864,6 +903,9 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
     if ((st = upload_rows(H, s, j_begin, j_end, h, hu, hv, b, psi))) return st;
     init_ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
     CK(cudaMemsetAsync(s.gM, 0, 4 * sizeof(unsigned long long), s.st));
+    CK(cudaMemsetAsync(s.tflag, 1, 2 * (size_t)s.ntx * s.nty, s.st));  // all tiles active
+    CK(cudaMemsetAsync(s.tstate, 0, (size_t)s.ntx * s.nty, s.st));
+    CK(cudaMemsetAsync(s.hstats, 0, 4 * sizeof(unsigned long long), s.st));
     // walls: ghosts of buffer 0 (W is read only on owned cells: no ghosts needed)
     launch_mirror(s.v, s.ctrl, 0, s.st, &H->launches);
     CK(cudaGetLastError());
@@ -901,6 +943,19 @@ int csph_set_state(csph_t* H, const double* h, const double* hu, const double* h
   return csph_set_state_rows(H, 0, H->ny, h, hu, hv, b, psi);
 }
 
+static Hgs hgs_of(const csph* H, const Strip& s) {
+  Hgs h;
+  const size_t nt = (size_t)s.ntx * s.nty;
+  h.fprev = s.tflag + nt * (size_t)H->host_parity;
+  h.fnext = s.tflag + nt * (size_t)(H->host_parity ^ 1);
+  h.tstate = s.tstate;
+  h.ntx = s.ntx;
+  h.nty = s.nty;
+  h.enable = H->p.hgs != 0 && H->p.path == CSPH_PATH_FUSED;
+  h.stats = s.hstats;
+  return h;
+}
+
 int csph_step(csph_t* H, int nsteps) {
   if (!H) return fail(CSPH_EINVAL, "handle is NULL");
   if (nsteps < 0) return fail(CSPH_EINVAL, "nsteps < 0");
@@ -915,23 +970,27 @@ int csph_step(csph_t* H, int nsteps) {
     }
   }
   const bool overlap = H->mode == DIST && H->nranks > 1 && H->p.path == CSPH_PATH_FUSED &&
-                       H->s[0].v.ny >= 2 * GY + 1;
+                       H->s[0].nty >= 2;
   for (int n = 0; n < nsteps; ++n) {
     const int q = H->host_parity ^ 1;
     if (overlap) {
       // boundary rows first; their halo exchange (NCCL stream) overlaps the interior
+      // boundary tile rows first (aligned to the HGS tiling), then the interior
       Strip& s = H->s[0];
-      const int ny = s.v.ny, ty = H->p.tile_rows;
+      const int ny = s.v.ny, ty = H->p.tile_rows > 0 ? H->p.tile_rows : 128;
+      const Hgs hg = hgs_of(H, s);
+      const int lo = ty < ny ? ty : ny, hi = (s.nty - 1) * ty;
       clear_flags_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
       H->launches += 1;
       if (H->profiling) CK(cudaEventRecord(H->evs[2 * n], s.st));
-      launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, GY, ty, s.st, &H->launches);
-      launch_fused_step(s.v, s.ctrl, H->P, s.gM, ny - GY, ny, ty, s.st, &H->launches);
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, lo, ty, hg, s.st, &H->launches);
+      if (hi > lo) launch_fused_step(s.v, s.ctrl, H->P, s.gM, hi, ny, ty, hg, s.st, &H->launches);
       CK(cudaEventRecord(s.ev_edge, s.st));
       CK(cudaStreamWaitEvent(s.cst, s.ev_edge, 0));
       int st = halo_nccl(H, q, s.cst);
       if (st) return st;
-      launch_fused_step(s.v, s.ctrl, H->P, s.gM, GY, ny - GY, ty, s.st, &H->launches);
+      if (hi > lo)
+        launch_fused_step(s.v, s.ctrl, H->P, s.gM, lo, hi, ty, hg, s.st, &H->launches);
       if (H->profiling) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
       CK(cudaGetLastError());
       CK(cudaEventRecord(s.ev_int, s.st));
@@ -954,8 +1013,8 @@ int csph_step(csph_t* H, int nsteps) {
       if (H->p.path == CSPH_PATH_STAGED)
         launch_staged_step(s.v, s.ctrl, s.scr, H->P, s.gM, s.st, &H->launches);
       else
-        launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, H->p.tile_rows, s.st,
-                          &H->launches);  // writes the wall ghosts in its epilogue
+        launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, H->p.tile_rows, hgs_of(H, s),
+                          s.st, &H->launches);  // writes the wall ghosts in its epilogue
       if (H->profiling && si == 0) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
       if (H->p.path == CSPH_PATH_STAGED) launch_mirror(s.v, s.ctrl, 1, s.st, &H->launches);
       CK(cudaGetLastError());

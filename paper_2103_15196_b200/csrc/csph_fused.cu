@@ -119,7 +119,7 @@ __device__ __forceinline__ double minmod_bf(double a, double b) {
 template <int NT, bool HASW, int D, int PF, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
     fused_step_kernel(StripView S, Ctrl* __restrict__ C, Phys P,
-                      unsigned long long* __restrict__ gM, int row0, int row1, int TY) {
+                      unsigned long long* __restrict__ gM, int row0, int row1, int TY, Hgs hg) {
   static_assert(D >= PF + 5, "ring too shallow");
   constexpr int TX = NT - 8;
   using SM = Smem<NT, HASW, D>;
@@ -146,6 +146,58 @@ __global__ void __launch_bounds__(NT, MINB)
   const int y0 = row0 + blockIdx.y * TY;
   const int y1 = min(y0 + TY, row1);
   if (y0 >= y1) return;
+  // ---- HGS: a tile whose 3x3 tile neighbourhood had
+  // no wet cell after the previous step updates to the identity ----
+  const int tr = y0 / TY;
+  const int ti = tr * hg.ntx + (int)blockIdx.x;
+  if (hg.enable && (S.wall_lo || tr > 0) && (S.wall_hi || tr < hg.nty - 1)) {
+    bool dry = true;
+    for (int a = -1; a <= 1; ++a)
+      for (int c2 = -1; c2 <= 1; ++c2) {
+        const int r = tr + a, q = (int)blockIdx.x + c2;
+        if (r >= 0 && r < hg.nty && q >= 0 && q < hg.ntx) dry = dry && hg.fprev[r * hg.ntx + q] == 0;
+      }
+    if (dry) {
+      const unsigned char stt = hg.tstate[ti];
+      if (stt < 2 || P.src != 0.0) {
+        // identity update: H' = H, Q' = +0, b' with R's K8 formula at zero fluxes
+        const bool outc = (t >= 4) && (t < 4 + TX) && (col < nx);
+        if (outc) {
+          for (int j = y0; j < y1; ++j) {
+            const size_t o = off(pitch, col, j);
+            const double H3 = gin[0][o], b3 = gin[3][o];
+            const double W3 = HASW ? S.W[o] : S.Wc;
+            const double z = 0.0 + (0.0 - 0.0);
+            const double Hn = H3 - lam * z;
+            double Qn = 0.0 - lam * z;
+            const double bn = (b3 - (lam * W3) * z) + (tau * W3) * P.src;
+            oH[o] = Hn; ob[o] = bn; oQx[o] = Qn; oQy[o] = Qn;
+            const bool gx = col < 3 || col >= nx - 3;
+            const bool gy = (S.wall_lo && j < 3) || (S.wall_hi && j >= ny - 3);
+            if (gx || gy) {
+              int gc[3] = {col, col < 3 ? -1 - col : INT_MIN, col >= nx - 3 ? 2 * nx - 1 - col : INT_MIN};
+              int gr[3] = {j, (S.wall_lo && j < 3) ? -1 - j : INT_MIN,
+                           (S.wall_hi && j >= ny - 3) ? 2 * ny - 1 - j : INT_MIN};
+              for (int a = 0; a < 3; ++a)
+                for (int c2 = 0; c2 < 3; ++c2) {
+                  if ((a | c2) == 0 || gc[a] == INT_MIN || gr[c2] == INT_MIN) continue;
+                  const size_t g = off(pitch, gc[a], gr[c2]);
+                  oH[g] = Hn; ob[g] = bn; oQx[g] = a ? -Qn : Qn; oQy[g] = c2 ? -Qn : Qn;
+                }
+            }
+          }
+        }
+        if (t == 0) {
+          hg.tstate[ti] = (unsigned char)(stt + 1);
+          atomicAdd(&hg.stats[1], 1ull);
+        }
+      } else if (t == 0) {
+        atomicAdd(&hg.stats[2], 1ull);
+      }
+      if (t == 0) hg.fnext[ti] = 0;
+      return;  // both buffers already hold the identity (tstate >= 2, no bed source)
+    }
+  }
   const int rfirst = y0 - GY;       // first input row
   const int niter = (y1 + 2) - rfirst + 1;  // input rows y0-3 .. y1+2
   // columns copied per row: [x0-4, min(x0-4+NT, nx+4)), even count
@@ -206,8 +258,10 @@ __global__ void __launch_bounds__(NT, MINB)
 
   // K8 epilogue for one cell: dry-momentum zeroing, negative-depth flag, stores,
   // wall ghosts and the next step's Eq.7 terms.
+  bool anywet = false;
   auto store_update = [&](double Hn, double Qxn, double Qyn, double bn, double W3, int j) {
     const bool wet = Hn > P.eps;
+    anywet |= wet;
     if (!wet) { Qxn = 0.0; Qyn = 0.0; }
     if (Hn < -P.neg_tol) neg = true;
     const size_t o = off(pitch, col, j);
@@ -464,7 +518,12 @@ __global__ void __launch_bounds__(NT, MINB)
   if ((t & 31) == 0) {
     sm.red[0][t >> 5] = m0; sm.red[1][t >> 5] = m1; sm.red[2][t >> 5] = m2;
   }
-  __syncthreads();
+  const bool tile_wet = __syncthreads_or(anywet);
+  if (t == 0 && hg.enable) {
+    hg.fnext[ti] = tile_wet ? 1 : 0;
+    hg.tstate[ti] = 0;
+  }
+  if (t == 0 && hg.stats) atomicAdd(&hg.stats[0], 1ull);
   if (t < 3) {
     unsigned long long m = 0;
 #pragma unroll
@@ -475,7 +534,7 @@ __global__ void __launch_bounds__(NT, MINB)
 
 template <int NT, bool HASW, int D, int PF, int MINB>
 void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM, int row0,
-              int row1, int TY, cudaStream_t st) {
+              int row1, int TY, const Hgs& hg, cudaStream_t st) {
   using SM = Smem<NT, HASW, D>;
   constexpr int TX = NT - 8;
   static bool configured = false;
@@ -486,16 +545,19 @@ void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
     configured = true;
   }
   dim3 grid((unsigned)((S.nx + TX - 1) / TX), (unsigned)((row1 - row0 + TY - 1) / TY));
-  fused_step_kernel<NT, HASW, D, PF, MINB><<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY);
+  fused_step_kernel<NT, HASW, D, PF, MINB><<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY,
+                                                                  hg);
 }
 
 template <int NT, int D, int PF, int MINB>
 void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM, int row0,
-              int row1, int TY, cudaStream_t st) {
+              int row1, int TY, const Hgs& hg, cudaStream_t st) {
+  Hgs h = hg;
+  if (NT - 8 != FUSED_TX) h.enable = 0;  // tiling of the flags is FUSED_TX wide
   if (S.W)
-    launch_t<NT, true, D, PF, MINB>(S, C, P, gM, row0, row1, TY, st);
+    launch_t<NT, true, D, PF, MINB>(S, C, P, gM, row0, row1, TY, h, st);
   else
-    launch_t<NT, false, D, PF, MINB>(S, C, P, gM, row0, row1, TY, st);
+    launch_t<NT, false, D, PF, MINB>(S, C, P, gM, row0, row1, TY, h, st);
 }
 
 int fused_variant() {
@@ -510,21 +572,22 @@ int fused_variant() {
 }  // namespace
 
 void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM,
-                       int row0, int row1, int tile_rows, cudaStream_t st, long long* nlaunch) {
+                       int row0, int row1, int tile_rows, const Hgs& hg, cudaStream_t st,
+                       long long* nlaunch) {
   if (row1 <= row0) return;
   int TY = tile_rows > 0 ? tile_rows : 128;
   switch (fused_variant()) {
-    case 0: launch_v<128, 8, 3, 1>(S, C, P, gM, row0, row1, TY, st); break;
-    case 2: launch_v<256, 6, 1, 2>(S, C, P, gM, row0, row1, TY, st); break;
-    case 3: launch_v<128, 7, 2, 4>(S, C, P, gM, row0, row1, TY, st); break;
-    case 4: launch_v<128, 6, 1, 3>(S, C, P, gM, row0, row1, TY, st); break;
-    case 5: launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, st); break;
-    case 6: launch_v<128, 10, 5, 3>(S, C, P, gM, row0, row1, TY, st); break;
-    case 7: launch_v<64, 8, 3, 6>(S, C, P, gM, row0, row1, TY, st); break;
-    case 8: launch_v<96, 8, 3, 4>(S, C, P, gM, row0, row1, TY, st); break;
-    case 9: launch_v<128, 12, 7, 2>(S, C, P, gM, row0, row1, TY, st); break;
-    case 10: launch_v<128, 9, 4, 3>(S, C, P, gM, row0, row1, TY, st); break;
-    default: launch_v<128, 6, 1, 4>(S, C, P, gM, row0, row1, TY, st); break;
+    case 0: launch_v<128, 8, 3, 1>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 2: launch_v<256, 6, 1, 2>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 3: launch_v<128, 7, 2, 4>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 4: launch_v<128, 6, 1, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 5: launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 6: launch_v<128, 10, 5, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 7: launch_v<64, 8, 3, 6>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 8: launch_v<96, 8, 3, 4>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 9: launch_v<128, 12, 7, 2>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 10: launch_v<128, 9, 4, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    default: launch_v<128, 6, 1, 4>(S, C, P, gM, row0, row1, TY, hg, st); break;
   }
   *nlaunch += 1;
 }

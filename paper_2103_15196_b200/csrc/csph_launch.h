@@ -16,9 +16,26 @@ struct Scratch {
 void launch_staged_step(const StripView& S, Ctrl* C, const Scratch& T, const Phys& P,
                         unsigned long long* gM, cudaStream_t st, long long* nlaunch);
 
-// Fused y-marching step (csph_fused.cu). Rows [row0, row1) of the strip.
+// HGS tile flags of the fused path: a tile is the TX x TY chunk
+// one CTA marches.  fprev/fnext: "some output cell of the tile was wet" for the
+// previous / this step; tstate: consecutive identity copies of the tile (2 = both
+// ping-pong buffers hold the same values, the tile may be skipped outright).
+struct Hgs {
+  const unsigned char* fprev;
+  unsigned char* fnext;
+  unsigned char* tstate;
+  int ntx, nty;
+  int enable;
+  unsigned long long* stats;  // [0] tiles marched, [1] copied (identity), [2] skipped
+};
+
+constexpr int FUSED_TX = 120;  // output columns per CTA of the fused kernel (NT - 8)
+
+// Fused y-marching step (csph_fused.cu). Rows [row0, row1) of the strip; row0 must be
+// a multiple of tile_rows when HGS is enabled.
 void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM,
-                       int row0, int row1, int tile_rows, cudaStream_t st, long long* nlaunch);
+                       int row0, int row1, int tile_rows, const Hgs& hgs, cudaStream_t st,
+                       long long* nlaunch);
 
 // Service kernels (csph_api.cu).
 void launch_mirror(const StripView& S, const Ctrl* C, int next_parity_from_ctrl,

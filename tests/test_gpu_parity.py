@@ -167,3 +167,32 @@ def test_branch_free_rcp_sqrt_match_ieee(cs):
     """the kernels' branch-free reciprocal and square root are
     bitwise IEEE-correct on 2^28 hashed inputs (exponents -300..300)."""
     assert cs.csph_selftest_math(1 << 28, 7) == 0
+
+
+@pytest.mark.parametrize("name,n,ny,steps", [("C5", 700, 650, 80), ("C3", 480, 500, 120),
+                                             ("C4", 600, 520, 80)])
+def test_hgs_tile_skipping_is_exact(cs, name, n, ny, steps):
+    """NEXT-1 HGS: skipping tiles whose neighbourhood
+    was dry changes nothing -- state and dt log bitwise equal with it off."""
+    c = synth.config(name, n, ny)
+    f = synth.fill(c)
+    res = []
+    for hgs in (1, 0):
+        g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, hgs=hgs))
+        g.set_state(*f)
+        g.step(steps)
+        res.append((g.get_dt_log(steps)[0], g.get_state()))
+        g.destroy()
+    assert np.array_equal(res[0][0], res[1][0])
+    for a, b in zip(res[0][1], res[1][1]):
+        assert np.array_equal(a, b)
+
+
+def test_hgs_with_bed_source_term(cs):
+    """q+ - q- != 0 changes b in dry cells too: HGS must keep copying (never skip)."""
+    c = synth.config("C5", 400, 380)
+    f = synth.fill(c)
+    p = dict(c.params, q_plus=1e-5, q_minus=0.0)
+    c2 = synth.Config("C5q", 5, c.nx, c.ny, params=p)
+    gpu, ref = run_both(cs, c2, 40, "fused", fields=f)
+    assert_parity(gpu, ref)
