@@ -93,6 +93,19 @@ int         csph_set_state_rows(csph_t*, int j_begin, int j_end, const double* h
                                 const double* hu, const double* hv, const double* b,
                                 const double* psi);
 
+/* NEXT-3 spatial inputs of the paper's model (Manning n_M(x,y) and
+ * absorption beta(x,y); Eq.6's sigma): per-cell Manning
+ * coefficient [s m^-1/3] (replaces params.n_manning), absorption rate beta [1/s]
+ * and water source s >= 0 [m/s] (rain, point inflow).  sigma = s - beta*H enters
+ * K8 as H' = ((H - lam dF) + tau s)/(1 + tau beta), momenta scaled by the same
+ * factor.  Global arrays [ny][nx]; any may be NULL (n_M from
+ * params; beta = s = 0).  Persist across csph_set_state. */
+int         csph_set_fields(csph_t*, const double* n_manning, const double* beta,
+                            const double* src);
+/* Row-window variant (global rows [j_begin, j_end), covering owned rows + halo). */
+int         csph_set_fields_rows(csph_t*, int j_begin, int j_end, const double* n_manning,
+                                 const double* beta, const double* src);
+
 /* Advance exactly nsteps CSPH-TVD steps, each with its own Eq.7 tau computed
  * on the device.  No host synchronisation inside the call except one status
  * readback at its end.  On CSPH_ENEGDEPTH/ENONFINITE/EDRY the steps up to the

@@ -86,6 +86,7 @@ def lib():
         L.orc_set_state.argtypes = [vp, _D, _D, _D, _D, _D]
         L.orc_set_state_padded.argtypes = [vp, _D, _D, _D, _D, _D]
         L.orc_get_state.argtypes = [vp, _D, _D, _D, _D]
+        L.orc_set_fields.argtypes = [vp, _D, _D, _D]
         L.orc_get_state_padded.argtypes = [vp, _D, _D, _D, _D]
         L.orc_reduce_M.argtypes = [vp, _D]
         L.orc_tau_from_M.argtypes = [vp, _D, _D, ctypes.POINTER(ctypes.c_int)]
@@ -152,6 +153,17 @@ class Oracle:
             psi = np.ascontiguousarray(np.broadcast_to(psi, (self.ny, self.nx)), dtype=np.float64)
             p = _ptr(psi)
         return lib().orc_set_state(self._h, *[_ptr(a) for a in arrs], p)
+
+    def set_fields(self, n_manning=None, beta=None, src=None) -> int:
+        arrs = []
+        for a in (n_manning, beta, src):
+            if a is None:
+                arrs.append(None)
+            else:
+                a = np.ascontiguousarray(np.broadcast_to(a, (self.ny, self.nx)), dtype=np.float64)
+                arrs.append(a)
+        self._fields = arrs  # keep alive during the call
+        return lib().orc_set_fields(self._h, *[None if a is None else _ptr(a) for a in arrs])
 
     def set_state_padded(self, H, Qx, Qy, b, W) -> int:
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (H, Qx, Qy, b, W)]

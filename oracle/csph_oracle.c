@@ -33,6 +33,10 @@ struct orc {
   double *QLx, *QLy, *J0x, *J0y, *J0a;
   double *FH, *FQx, *FQy, *FJ, *GH, *GQx, *GQy, *GJ;
   double *Hn, *Qxn, *Qyn, *bn;
+  /* NEXT-3 spatial inputs (P:129 n_M(x,y), beta(x,y); Eq.6 sigma):
+   * per-cell c_gam = g n_M^2, absorption beta and source s (rain + point inflow) */
+  double *cg, *beta, *srcf;
+  int has_fields, fields_fric, fields_src;
   unsigned char* w;
   double M[3];
   double t, last_dt;
@@ -195,7 +199,7 @@ orc_t* orc_create(int nx, int ny, double dx, const orc_params* p) {
                      &o->phix, &o->phiy, &o->gam, &o->Hh, &o->ut, &o->vt, &o->phix2,
                      &o->phiy2, &o->QLx, &o->QLy, &o->J0x, &o->J0y, &o->J0a, &o->FH,
                      &o->FQx, &o->FQy, &o->FJ, &o->GH, &o->GQx, &o->GQy, &o->GJ,
-                     &o->Hn, &o->Qxn, &o->Qyn, &o->bn};
+                     &o->Hn, &o->Qxn, &o->Qyn, &o->bn, &o->cg, &o->beta, &o->srcf};
   for (size_t k = 0; k < sizeof(arrs) / sizeof(arrs[0]); ++k) {
     *arrs[k] = (double*)calloc(n, sizeof(double));
     if (!*arrs[k]) { orc_destroy(o); return NULL; }
@@ -210,7 +214,8 @@ void orc_destroy(orc_t* o) {
   double* arrs[] = {o->H, o->Qx, o->Qy, o->b, o->W, o->eta, o->r, o->u, o->v, o->phix,
                     o->phiy, o->gam, o->Hh, o->ut, o->vt, o->phix2, o->phiy2, o->QLx,
                     o->QLy, o->J0x, o->J0y, o->J0a, o->FH, o->FQx, o->FQy, o->FJ,
-                    o->GH, o->GQx, o->GQy, o->GJ, o->Hn, o->Qxn, o->Qyn, o->bn};
+                    o->GH, o->GQx, o->GQy, o->GJ, o->Hn, o->Qxn, o->Qyn, o->bn,
+                    o->cg, o->beta, o->srcf};
   for (size_t k = 0; k < sizeof(arrs) / sizeof(arrs[0]); ++k) free(arrs[k]);
   free(o->w);
   free(o);
@@ -326,6 +331,48 @@ int orc_set_state_padded(orc_t* o, const double* H, const double* Qx, const doub
   return ORC_OK;
 }
 
+/* NEXT-3: per-cell Manning n_M, absorption beta and
+ * water source s >= 0 of Eq.6's sigma (rain, point inflow).  NULL
+ * arrays mean: scalar n_M of the params, beta = 0, s = 0.  Arrays are [ny][nx]. */
+int orc_set_fields(orc_t* o, const double* n_manning, const double* beta, const double* src) {
+  if (!o) return ORC_EINVAL;
+  size_t n = (size_t)o->nx * o->ny;
+  for (size_t k = 0; k < n; ++k) {
+    if (n_manning && !(n_manning[k] >= 0.0 && isfinite(n_manning[k]))) return ORC_EINVAL;
+    if (beta && !(beta[k] >= 0.0 && isfinite(beta[k]))) return ORC_EINVAL;
+    if (src && !(src[k] >= 0.0 && isfinite(src[k]))) return ORC_EINVAL;
+  }
+  for (int j = 0; j < o->ny; ++j)
+    for (int i = 0; i < o->nx; ++i) {
+      size_t s = (size_t)j * o->nx + i, d = IDX(o, i, j);
+      double nm = n_manning ? n_manning[s] : o->p.n_manning;
+      o->cg[d] = o->p.g * (nm * nm);
+      o->beta[d] = beta ? beta[s] : 0.0;
+      o->srcf[d] = src ? src[s] : 0.0;
+    }
+  /* the fields are mirrored into the wall ghosts like H and b (reading #14) */
+  {
+    double* fl[3] = {o->cg, o->beta, o->srcf};
+    for (int q = 0; q < 3; ++q) {
+      double* f = fl[q];
+      for (int j = 0; j < o->ny; ++j)
+        for (int k = 0; k < G; ++k) {
+          if (o->wall[0]) f[IDX(o, -1 - k, j)] = f[IDX(o, k, j)];
+          if (o->wall[1]) f[IDX(o, o->nx + k, j)] = f[IDX(o, o->nx - 1 - k, j)];
+        }
+      for (int i = -G; i < o->nx + G; ++i)
+        for (int k = 0; k < G; ++k) {
+          if (o->wall[2]) f[IDX(o, i, -1 - k)] = f[IDX(o, i, k)];
+          if (o->wall[3]) f[IDX(o, i, o->ny + k)] = f[IDX(o, i, o->ny - 1 - k)];
+        }
+    }
+  }
+  o->has_fields = (n_manning || beta || src) ? 1 : 0;
+  o->fields_fric = n_manning != NULL;
+  o->fields_src = (beta || src) ? 1 : 0;
+  return ORC_OK;
+}
+
 int orc_get_state(orc_t* o, double* h, double* hu, double* hv, double* b) {
   if (!o) return ORC_EINVAL;
   if (!o->have_state) return ORC_ENOSTATE;
@@ -387,7 +434,7 @@ int orc_step_tau(orc_t* o, double tau) {
   const double eps = p->eps_dry;
   const double theta = 0.5 * tau;
   const double lam = tau / o->h;
-  const int fric = p->n_manning > 0.0;
+  const int fric = p->n_manning > 0.0 || o->fields_fric;
   double *H = o->H, *Qx = o->Qx, *Qy = o->Qy, *b = o->b, *W = o->W;
   const size_t sx = 1, sy = (size_t)o->pw;
 
@@ -418,7 +465,11 @@ int orc_step_tau(orc_t* o, double tau) {
       double PS = face_force(o->cP, o->eta[s], b[s], o->eta[c], b[c]);
       o->phix[c] = -(PE + PW);
       o->phiy[c] = -(PN + PS);
-      if (fric) {
+      if (o->fields_fric) {
+        /* friction field: c_gam = g n_M(x,y)^2 per cell (gamma = 0 where n_M = 0) */
+        double sp = sqrt(o->u[c] * o->u[c] + o->v[c] * o->v[c]);
+        o->gam[c] = (o->cg[c] * sp) * (o->r[c] * orc_icbrt(H[c]));
+      } else if (fric) {
         double sp = sqrt(o->u[c] * o->u[c] + o->v[c] * o->v[c]);
         o->gam[c] = (o->cgam * sp) * (o->r[c] * orc_icbrt(H[c]));
       } else {
@@ -539,6 +590,14 @@ int orc_step_tau(orc_t* o, double tau) {
       double Hn = H[c] - lam * dH;
       double Qxn = o->QLx[c] - lam * dQx;
       double Qyn = o->QLy[c] - lam * dQy;
+      if (o->fields_src) {
+        /* sigma = s - beta H (reading #21): source explicit, absorption implicit,
+         * H' = ((H - lam dF) + tau s) / (1 + tau beta); momenta scaled alike */
+        double a = 1.0 / (1.0 + tau * o->beta[c]);
+        Hn = (Hn + tau * o->srcf[c]) * a;
+        Qxn = Qxn * a;
+        Qyn = Qyn * a;
+      }
       double bn = (b[c] - (lam * W[c]) * dJ) + (tau * W[c]) * src;
       if (!(Hn > eps)) { Qxn = 0.0; Qyn = 0.0; }
       if (Hn < -p->neg_tol) neg = 1;

@@ -65,6 +65,8 @@ int    orc_set_state(orc_t*, const double* h, const double* hu,
 int    orc_set_state_padded(orc_t*, const double* H, const double* Qx,
                             const double* Qy, const double* b, const double* W);
 int    orc_get_state(orc_t*, double* h, double* hu, double* hv, double* b);
+/* NEXT-3: Manning field, absorption field, source field (each may be NULL) */
+int    orc_set_fields(orc_t*, const double* n_manning, const double* beta, const double* src);
 int    orc_get_state_padded(orc_t*, double* H, double* Qx, double* Qy, double* b);
 /* maxima M1..M3 (step 9) of the current state over the owned cells */
 int    orc_reduce_M(orc_t*, double M[3]);

@@ -27,6 +27,7 @@ EXPORTS = [
     "csph_last_error", "csph_nccl_id_bytes", "csph_make_nccl_id", "csph_create_dist",
     "csph_create_multi", "csph_last_launch_count", "csph_profile", "csph_get_profile",
     "csph_selftest_math", "csph_get_tile_stats", "csph_reset_tile_stats",
+    "csph_set_fields", "csph_set_fields_rows",
 ]
 
 
@@ -75,6 +76,8 @@ def lib():
         L.csph_set_state.argtypes = [_vp, _D, _D, _D, _D, _D]
         L.csph_set_state_rows.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D, _D]
         L.csph_step.argtypes = [_vp, ctypes.c_int]
+        L.csph_set_fields.argtypes = [_vp, _D, _D, _D]
+        L.csph_set_fields_rows.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _D, _D, _D]
         L.csph_get_state.argtypes = [_vp, _D, _D, _D, _D]
         L.csph_get_state_rows.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D]
         L.csph_get_time.argtypes = [_vp, _D, ctypes.POINTER(ctypes.c_longlong), _D]
@@ -185,6 +188,17 @@ class Csph:
         ps = None if psi is None else _arr(np.broadcast_to(psi, shp), shp)
         return _check(lib().csph_set_state_rows(self.h, j_begin, j_end, *[_p(x) for x in a], _p(ps)),
                       "csph_set_state_rows")
+
+    def set_fields(self, n_manning=None, beta=None, src=None):
+        shp = (self.ny, self.nx)
+        a = [None if x is None else _arr(np.broadcast_to(x, shp), shp) for x in (n_manning, beta, src)]
+        return _check(lib().csph_set_fields(self.h, *[_p(x) for x in a]), "csph_set_fields")
+
+    def set_fields_rows(self, j_begin, j_end, n_manning=None, beta=None, src=None):
+        shp = (j_end - j_begin, self.nx)
+        a = [None if x is None else _arr(np.broadcast_to(x, shp), shp) for x in (n_manning, beta, src)]
+        return _check(lib().csph_set_fields_rows(self.h, j_begin, j_end, *[_p(x) for x in a]),
+                      "csph_set_fields_rows")
 
     def step(self, nsteps: int, check: bool = True) -> int:
         code = lib().csph_step(self.h, nsteps)

@@ -114,6 +114,7 @@ struct Strip {
   unsigned long long* hstats = nullptr;  // HGS tile counters: marched, copied, skipped
   int ntx = 0, nty = 0;
   double* Wbuf = nullptr;            // device psi -> W field (when psi varies)
+  double *cgbuf = nullptr, *betabuf = nullptr, *srcbuf = nullptr;  // NEXT-3 fields
   cudaStream_t st = nullptr;
   bool own_stream = true;
   cudaEvent_t ev = nullptr;
@@ -257,6 +258,60 @@ __global__ void maxima_kernel(StripView S, const Ctrl* C, Phys P, unsigned long 
     }
   }
   block_max3_atomic<8>(m0, m1, m2, gM);
+}
+
+// NEXT-3: validate the uploaded field rows and turn n_M into c_gam = g n_M^2 in place.
+__global__ void fields_kernel(StripView S, double* cg, double* beta, double* src, int jlo,
+                              int jhi, double g, double n_scalar, int has_n, int has_b,
+                              int has_s, int* flags) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int j = jlo + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+  int f = 0;
+  if (i < S.nx && j < jhi) {
+    size_t c = off(S.pitch, i, j);
+    if (cg) {
+      double n = has_n ? cg[c] : n_scalar;
+      if (!(n >= 0.0 && isfinite(n))) f |= 1;
+      cg[c] = g * (n * n);
+    }
+    if (beta) {
+      double b = has_b ? beta[c] : 0.0;
+      if (!(b >= 0.0 && isfinite(b))) f |= 2;
+      beta[c] = b;
+      double q = has_s ? src[c] : 0.0;
+      if (!(q >= 0.0 && isfinite(q))) f |= 4;
+      src[c] = q;
+    }
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+}
+
+// Mirror a static per-cell field into the wall ghosts (copy, no sign change).
+__global__ void mirror_field_kernel(StripView S, double* F) {
+  const int nx = S.nx, ny = S.ny;
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < (ny + 2 * GY) * 6) {
+    int j = t / 6 - GY, k = t % 6;
+    int gi = k < 3 ? -1 - k : nx + (k - 3);
+    int si = k < 3 ? k : nx - 1 - (k - 3);
+    F[off(S.pitch, gi, j)] = F[off(S.pitch, si, j)];
+  }
+}
+
+__global__ void mirror_field_y_kernel(StripView S, double* F) {
+  const int nx = S.nx, ny = S.ny;
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int w = nx + 6;
+  if (t >= w * 6) return;
+  int i = t % w - 3, k = t / w;
+  if (k < 3) {
+    if (!S.wall_lo) return;
+    F[off(S.pitch, i, -1 - k)] = F[off(S.pitch, i, k)];
+  } else {
+    if (!S.wall_hi) return;
+    F[off(S.pitch, i, ny + (k - 3))] = F[off(S.pitch, i, ny - 1 - (k - 3))];
+  }
 }
 
 __global__ void max_gather_kernel(unsigned long long* dst, const unsigned long long* src,
@@ -935,6 +990,80 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
   H->have_state = true;
   H->host_parity = 0;
   return CSPH_OK;
+}
+
+static int upload_field_rows(Strip& s, double* dst, const double* src_rows, int j_begin,
+                             int lo, int hi, int nx) {
+  const StripView& v = s.v;
+  CK(cudaMemcpy2DAsync(dst + off(v.pitch, 0, lo - s.gj0), (size_t)v.pitch * 8,
+                       src_rows + (size_t)(lo - j_begin) * nx, (size_t)nx * 8, (size_t)nx * 8,
+                       hi - lo, cudaMemcpyHostToDevice, s.st));
+  return CSPH_OK;
+}
+
+int csph_set_fields_rows(csph_t* H, int j_begin, int j_end, const double* n_manning,
+                         const double* beta, const double* src) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  if (j_begin < 0 || j_end > H->ny || j_end <= j_begin) return fail(CSPH_EINVAL, "bad row range");
+  const bool has_n = n_manning != nullptr, has_src = beta != nullptr || src != nullptr;
+  const int nx = H->nx;
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    StripView& v = s.v;
+    const int lo = s.gj0 - (v.wall_lo ? 0 : GY);
+    const int hi = s.gj0 + v.ny + (v.wall_hi ? 0 : GY);
+    if (lo < j_begin || hi > j_end)
+      return fail(CSPH_EINVAL, "rows [%d,%d) do not cover strip rows [%d,%d) + halo", j_begin,
+                  j_end, lo, hi);
+    const size_t n = (size_t)(v.ny + 2 * GY) * v.pitch;
+    int st;
+    double *cg = nullptr, *bt = nullptr, *sr = nullptr;
+    if (has_n) {
+      if (!s.cgbuf && (st = dalloc(s, (void**)&s.cgbuf, n * 8))) return st;
+      cg = s.cgbuf;
+      CK(cudaMemsetAsync(cg, 0, n * 8, s.st));
+      if ((st = upload_field_rows(s, cg, n_manning, j_begin, lo, hi, nx))) return st;
+    }
+    if (has_src) {
+      if (!s.betabuf && (st = dalloc(s, (void**)&s.betabuf, n * 8))) return st;
+      if (!s.srcbuf && (st = dalloc(s, (void**)&s.srcbuf, n * 8))) return st;
+      bt = s.betabuf;
+      sr = s.srcbuf;
+      CK(cudaMemsetAsync(bt, 0, n * 8, s.st));
+      CK(cudaMemsetAsync(sr, 0, n * 8, s.st));
+      if (beta && (st = upload_field_rows(s, bt, beta, j_begin, lo, hi, nx))) return st;
+      if (src && (st = upload_field_rows(s, sr, src, j_begin, lo, hi, nx))) return st;
+    }
+    CK(cudaMemsetAsync(s.dflags, 0, sizeof(int), s.st));
+    dim3 blk(32, 8), grd((nx + 31) / 32, (hi - lo + 7) / 8);
+    fields_kernel<<<grd, blk, 0, s.st>>>(v, cg, bt, sr, lo - s.gj0, hi - s.gj0, H->p.g,
+                                         H->p.n_manning, has_n, beta != nullptr,
+                                         src != nullptr, s.dflags);
+    CK(cudaGetLastError());
+    int flags = 0;
+    CK(cudaMemcpyAsync(&flags, s.dflags, sizeof(int), cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    if (flags & 1) return fail(CSPH_EINVAL, "n_manning field must be finite and >= 0");
+    if (flags & 2) return fail(CSPH_EINVAL, "beta field must be finite and >= 0");
+    if (flags & 4) return fail(CSPH_EINVAL, "source field must be finite and >= 0");
+    for (double* F : {cg, bt, sr}) {
+      if (!F) continue;
+      int n1 = (v.ny + 2 * GY) * 6, n2 = (v.nx + 6) * 6;
+      mirror_field_kernel<<<(n1 + 255) / 256, 256, 0, s.st>>>(v, F);
+      mirror_field_y_kernel<<<(n2 + 255) / 256, 256, 0, s.st>>>(v, F);
+    }
+    CK(cudaGetLastError());
+    v.cg = cg;
+    v.beta = bt;
+    v.src = sr;
+  }
+  H->P.fric = H->p.n_manning > 0.0 || has_n;
+  return CSPH_OK;
+}
+
+int csph_set_fields(csph_t* H, const double* n_manning, const double* beta, const double* src) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  return csph_set_fields_rows(H, 0, H->ny, n_manning, beta, src);
 }
 
 int csph_set_state(csph_t* H, const double* h, const double* hu, const double* hv,

@@ -159,18 +159,22 @@ __global__ void __launch_bounds__(NT, MINB)
       }
     if (dry) {
       const unsigned char stt = hg.tstate[ti];
-      if (stt < 2 || P.src != 0.0) {
-        // identity update: H' = H, Q' = +0, b' with R's K8 formula at zero fluxes
+      if (stt < 2 || P.src != 0.0 || S.beta) {
+        // identity update: H' = H, Q' = +0, b' with R's K8 formula at zero fluxes (with
+        // NEXT-3 sources H' = (H + tau s)/(1 + tau beta): a dry cell may become wet)
         const bool outc = (t >= 4) && (t < 4 + TX) && (col < nx);
+        bool cwet = false;
         if (outc) {
           for (int j = y0; j < y1; ++j) {
             const size_t o = off(pitch, col, j);
             const double H3 = gin[0][o], b3 = gin[3][o];
             const double W3 = HASW ? S.W[o] : S.Wc;
             const double z = 0.0 + (0.0 - 0.0);
-            const double Hn = H3 - lam * z;
-            double Qn = 0.0 - lam * z;
+            double Hn = H3 - lam * z;
+            double Qn = 0.0 - lam * z, Qm = Qn;
             const double bn = (b3 - (lam * W3) * z) + (tau * W3) * P.src;
+            apply_sources(S, tau, o, Hn, Qn, Qm);
+            if (Hn > P.eps) cwet = true;  // momenta stay +0 (they were +0 * a)
             oH[o] = Hn; ob[o] = bn; oQx[o] = Qn; oQy[o] = Qn;
             const bool gx = col < 3 || col >= nx - 3;
             const bool gy = (S.wall_lo && j < 3) || (S.wall_hi && j >= ny - 3);
@@ -187,15 +191,33 @@ __global__ void __launch_bounds__(NT, MINB)
             }
           }
         }
+        const bool any = __syncthreads_or(cwet);
         if (t == 0) {
-          hg.tstate[ti] = (unsigned char)(stt + 1);
+          hg.tstate[ti] = any ? 0 : (unsigned char)(stt + 1);
+          hg.fnext[ti] = any ? 1 : 0;
           atomicAdd(&hg.stats[1], 1ull);
         }
-      } else if (t == 0) {
-        atomicAdd(&hg.stats[2], 1ull);
+        // a cell made wet by a source has Q' = +0: its Eq.7 terms are those of a
+        // still wet cell
+        if (cwet) {
+          for (int j = y0; j < y1; ++j) {
+            const size_t o = off(pitch, col, j);
+            const double Hn = oH[o];
+            if (Hn > P.eps) {
+              double t1, t2, t3;
+              dt_terms(P, Hn, 0.0, 0.0, HASW ? S.W[o] : S.Wc, t1, t2, t3);
+              unsigned long long a2 = dbits(t1), b2 = dbits(t2), c2 = dbits(t3);
+              atomicMax(&gM[0], a2); atomicMax(&gM[1], b2); atomicMax(&gM[2], c2);
+            }
+          }
+        }
+        return;
       }
-      if (t == 0) hg.fnext[ti] = 0;
-      return;  // both buffers already hold the identity (tstate >= 2, no bed source)
+      if (t == 0) {
+        atomicAdd(&hg.stats[2], 1ull);
+        hg.fnext[ti] = 0;
+      }
+      return;  // both buffers already hold the identity (tstate >= 2, no source)
     }
   }
   const int rfirst = y0 - GY;       // first input row
@@ -334,10 +356,11 @@ __global__ void __launch_bounds__(NT, MINB)
         const double dQx = dF3[1] + (Gn[1] - Gs[1]);
         const double dQy = dF3[2] + (Gn[2] - Gs[2]);
         const double dJ = dF3[3] + (Gn[3] - Gs[3]);
-        const double Hn = H3 - lam * dH;
+        double Hn = H3 - lam * dH;
         double Qxn = QLx3 - lam * dQx;
         double Qyn = QLy3 - lam * dQy;
         const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
+        apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
         store_update(Hn, Qxn, Qyn, bn, W3, j);
       }
       QLx3 = 0.0; QLy3 = 0.0;
@@ -357,7 +380,10 @@ __global__ void __launch_bounds__(NT, MINB)
       const double rr = rcp_nb(Hs);
       const double uu = RG(F_QX, k, 0) * rr, vv = RG(F_QY, k, 0) * rr;
       double gg = 0.0;
-      if (P.fric) gg = (P.cgam * sqrt0nb(uu * uu + vv * vv)) * (rr * icbrt(Hs));
+      if (P.fric) {
+        const double cgc = S.cg ? S.cg[off(pitch, col, L)] : P.cgam;  // NEXT-3 field
+        gg = (cgc * sqrt0nb(uu * uu + vv * vv)) * (rr * icbrt(Hs));
+      }
       r0 = w0 ? rr : 0.0; u0 = w0 ? uu : 0.0; v0 = w0 ? vv : 0.0; gam0 = w0 ? gg : 0.0;
     }
     double PE0;
@@ -492,10 +518,11 @@ __global__ void __launch_bounds__(NT, MINB)
         const double dQx = dF3[1] + (Gn[1] - Gs[1]);
         const double dQy = dF3[2] + (Gn[2] - Gs[2]);
         const double dJ = dF3[3] + (Gn[3] - Gs[3]);
-        const double Hn = H3 - lam * dH;
+        double Hn = H3 - lam * dH;
         double Qxn = QLx3 - lam * dQx;
         double Qyn = QLy3 - lam * dQy;
         const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
+        apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
         store_update(Hn, Qxn, Qyn, bn, W3, j);
       }
       QLx3 = QLx2; QLy3 = QLy2;

@@ -56,7 +56,11 @@ __global__ void k2_forces(StripView S, const Ctrl* __restrict__ C, Scratch T, Ra
   double PS = face_force(P.cP, T.eta[s], b[s], T.eta[c], b[c]);
   T.phix[c] = -(PE + PW);
   T.phiy[c] = -(PN + PS);
-  if (P.fric) {
+  if (S.cg) {  // NEXT-3 Manning field
+    double u = T.u[c], v = T.v[c];
+    double sp = sqrt0(u * u + v * v);
+    T.gam[c] = (S.cg[c] * sp) * (T.r[c] * icbrt(S.H[p][c]));
+  } else if (P.fric) {
     double u = T.u[c], v = T.v[c];
     double sp = sqrt0(u * u + v * v);
     T.gam[c] = (P.cgam * sp) * (T.r[c] * icbrt(S.H[p][c]));
@@ -186,6 +190,7 @@ __global__ void k8_update(StripView S, Ctrl* C, Scratch T, Range R, Phys P,
     double Qxn = T.QLx[c] - lam * dQx;
     double Qyn = T.QLy[c] - lam * dQy;
     double bn = (S.b[p][c] - (lam * W) * dJ) + (tau * W) * P.src;
+    apply_sources(S, tau, c, Hn, Qxn, Qyn);
     bool wet = Hn > P.eps;
     if (!wet) { Qxn = 0.0; Qyn = 0.0; }
     if (Hn < -P.neg_tol) atomicOr(&C->flags, 1);
