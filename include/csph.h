@@ -56,7 +56,7 @@ typedef struct {
   double neg_tol;    /* h' < -neg_tol -> CSPH_ENEGDEPTH, default 1e-12 m */
   double n_manning;  /* Manning n_M [s m^-1/3]; 0 disables friction */
   double A_J;        /* Grass coefficient of Eq.3; 0 disables transport */
-  int    m_grass;    /* Grass exponent; this build implements 2 */
+  int    m_grass;    /* Grass exponent m of Eq.3, integer 0..8 (2 for fine sand) */
   double C_J;        /* Eq.2 slope coefficient (1.5..2.3, up to 5) */
   double C_Sh;       /* Eq.5 Shamov constant; 0 disables the gate */
   double d50;        /* Eq.5 median grain size [m] (> 0 when C_Sh > 0) */
@@ -68,6 +68,9 @@ typedef struct {
   int    tile_rows;  /* fused path: rows marched per CTA (0 = auto = 128) */
   int    hgs;        /* 1 (default): skip tiles whose neighbourhood is dry (the paper's
                         HGS; exact); 0: march every tile */
+  int    aj_mode;    /* 0 (default): constant A_J; 1: Eq.4
+                        A_J = 0.05 n_M^3 / ((s-1) sqrt(g H) d50), H the local depth */
+  double s_rel;      /* Eq.4 relative density rho_s/rho (> 1), default 2.65 */
 } csph_params;
 
 /* Fill *p with the defaults above. */

@@ -44,6 +44,7 @@ class _Params(ctypes.Structure):
         ("n_manning", ctypes.c_double), ("A_J", ctypes.c_double), ("m_grass", ctypes.c_int),
         ("C_J", ctypes.c_double), ("C_Sh", ctypes.c_double), ("d50", ctypes.c_double),
         ("q_plus", ctypes.c_double), ("q_minus", ctypes.c_double),
+        ("aj_mode", ctypes.c_int), ("s_rel", ctypes.c_double),
     ]
 
 
@@ -62,11 +63,13 @@ class Params:
     d50: float = 1e-3
     q_plus: float = 0.0
     q_minus: float = 0.0
+    aj_mode: int = 0
+    s_rel: float = 2.65
 
     def to_c(self) -> _Params:
         return _Params(self.g, self.K, self.eps_dry, self.dt_max, self.neg_tol,
                        self.n_manning, self.A_J, self.m_grass, self.C_J, self.C_Sh,
-                       self.d50, self.q_plus, self.q_minus)
+                       self.d50, self.q_plus, self.q_minus, self.aj_mode, self.s_rel)
 
 
 _lib = None
@@ -95,6 +98,9 @@ def lib():
         L.orc_get_time.argtypes = [vp, _D, ctypes.POINTER(ctypes.c_longlong), _D]
         L.orc_get_debug.argtypes = [vp, ctypes.c_char_p, _D]
         L.orc_grass.argtypes = [ctypes.c_double] * 3 + [_D] * 3
+        L.orc_grass_m.argtypes = [ctypes.c_double, ctypes.c_int] + [ctypes.c_double] * 2 + [_D] * 3
+        L.orc_aj_eq4.restype = ctypes.c_double
+        L.orc_aj_eq4.argtypes = [ctypes.c_double] * 5
         L.orc_slope_flux.restype = ctypes.c_double
         L.orc_slope_flux.argtypes = [ctypes.c_double] * 4
         L.orc_icbrt.restype = ctypes.c_double
@@ -233,6 +239,16 @@ def grass(A_J, vx, vy):
     jx, jy, ja = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     lib().orc_grass(A_J, vx, vy, ctypes.byref(jx), ctypes.byref(jy), ctypes.byref(ja))
     return jx.value, jy.value, ja.value
+
+
+def grass_m(A, m, vx, vy):
+    jx, jy, ja = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    lib().orc_grass_m(A, m, vx, vy, ctypes.byref(jx), ctypes.byref(jy), ctypes.byref(ja))
+    return jx.value, jy.value, ja.value
+
+
+def aj_eq4(g, n_manning, s_rel, H, d50):
+    return lib().orc_aj_eq4(g, n_manning, s_rel, H, d50)
 
 
 def slope_flux(J0n, J0abs, C_J, db_dn):

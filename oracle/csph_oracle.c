@@ -35,7 +35,7 @@ struct orc {
   double *Hn, *Qxn, *Qyn, *bn;
   /* NEXT-3 spatial inputs (P:129 n_M(x,y), beta(x,y); Eq.6 sigma):
    * per-cell c_gam = g n_M^2, absorption beta and source s (rain + point inflow) */
-  double *cg, *beta, *srcf;
+  double *cg, *beta, *srcf, *nfld;
   int has_fields, fields_fric, fields_src;
   unsigned char* w;
   double M[3];
@@ -82,6 +82,25 @@ void orc_grass(double A_J, double vx, double vy, double* jx, double* jy, double*
   *jx = a * vx;
   *jy = a * vy;
   *jabs = a * sqrt(s2);
+}
+
+/* Eq.3 with integer m (NEXT-4): p = |v|^m by repeated multiplication in s2 = |v|^2,
+ * then J0 = (A p) v and |J0| = (A p) |v|.  m = 2 reproduces orc_grass exactly. */
+void orc_grass_m(double A, int m, double vx, double vy, double* jx, double* jy, double* jabs) {
+  double s2 = vx * vx + vy * vy;
+  double a = sqrt(s2);
+  double pw = 1.0;
+  for (int k = 0; k < m / 2; ++k) pw = pw * s2;
+  if (m % 2) pw = pw * a;
+  double c = A * pw;
+  *jx = c * vx;
+  *jy = c * vy;
+  *jabs = c * a;
+}
+
+/* Eq.4, A_J from the local depth H (reading #5: H = local depth) */
+double orc_aj_eq4(double g, double n_manning, double s_rel, double H, double d50) {
+  return (0.05 * ((n_manning * n_manning) * n_manning)) / (((s_rel - 1.0) * sqrt(g * H)) * d50);
 }
 
 /* Eq.2, vector reading #4: J_n = J0_n - C_J |J0| db/dn */
@@ -171,7 +190,9 @@ static int valid_params(const orc_params* p) {
   if (!(p->neg_tol >= 0.0)) return 0;
   if (!(p->n_manning >= 0.0) || !isfinite(p->n_manning)) return 0;
   if (!(p->A_J >= 0.0) || !isfinite(p->A_J)) return 0;
-  if (p->m_grass != 2) return 0;
+  if (p->m_grass < 0 || p->m_grass > 8) return 0;
+  if (p->aj_mode != 0 && p->aj_mode != 1) return 0;
+  if (p->aj_mode == 1 && !(p->s_rel > 1.0 && isfinite(p->s_rel) && p->d50 > 0.0)) return 0;
   if (!isfinite(p->C_J)) return 0;
   if (!(p->C_Sh >= 0.0) || !isfinite(p->C_Sh)) return 0;
   if (p->C_Sh > 0.0 && !(p->d50 > 0.0)) return 0;
@@ -199,7 +220,7 @@ orc_t* orc_create(int nx, int ny, double dx, const orc_params* p) {
                      &o->phix, &o->phiy, &o->gam, &o->Hh, &o->ut, &o->vt, &o->phix2,
                      &o->phiy2, &o->QLx, &o->QLy, &o->J0x, &o->J0y, &o->J0a, &o->FH,
                      &o->FQx, &o->FQy, &o->FJ, &o->GH, &o->GQx, &o->GQy, &o->GJ,
-                     &o->Hn, &o->Qxn, &o->Qyn, &o->bn, &o->cg, &o->beta, &o->srcf};
+                     &o->Hn, &o->Qxn, &o->Qyn, &o->bn, &o->cg, &o->beta, &o->srcf, &o->nfld};
   for (size_t k = 0; k < sizeof(arrs) / sizeof(arrs[0]); ++k) {
     *arrs[k] = (double*)calloc(n, sizeof(double));
     if (!*arrs[k]) { orc_destroy(o); return NULL; }
@@ -215,7 +236,7 @@ void orc_destroy(orc_t* o) {
                     o->phiy, o->gam, o->Hh, o->ut, o->vt, o->phix2, o->phiy2, o->QLx,
                     o->QLy, o->J0x, o->J0y, o->J0a, o->FH, o->FQx, o->FQy, o->FJ,
                     o->GH, o->GQx, o->GQy, o->GJ, o->Hn, o->Qxn, o->Qyn, o->bn,
-                    o->cg, o->beta, o->srcf};
+                    o->cg, o->beta, o->srcf, o->nfld};
   for (size_t k = 0; k < sizeof(arrs) / sizeof(arrs[0]); ++k) free(arrs[k]);
   free(o->w);
   free(o);
@@ -263,6 +284,14 @@ static void mirror_fill(orc_t* o) {
   }
 }
 
+/* A_J of cell c at depth H: the constant, or Eq.4 with the cell's n_M (NEXT-4) */
+static double cell_aj(const orc_t* o, size_t c, double H) {
+  if (o->p.aj_mode == 0) return o->p.A_J;
+  if (!(H > o->p.eps_dry)) return 0.0;
+  double n = o->fields_fric ? o->nfld[c] : o->p.n_manning;
+  return orc_aj_eq4(o->p.g, n, o->p.s_rel, H, o->p.d50);
+}
+
 /* Step 9: maxima over the owned wet cells of the state. */
 static void reduce_M(orc_t* o, const double* H, const double* Qx, const double* Qy,
                      double M[3]) {
@@ -280,7 +309,12 @@ static void reduce_M(orc_t* o, const double* H, const double* Qx, const double* 
       double t1 = s2;
       double t2 = a + sqrt(p->g * Hc);
       double t3 = 0.0;
-      if (orc_shamov_gate(o->kappa, s2, Hc, p->C_Sh)) t3 = ((p->A_J * s2) * a) * o->W[c];
+      if (orc_shamov_gate(o->kappa, s2, Hc, p->C_Sh)) {
+        double pw = 1.0;  /* |v|^m as in orc_grass_m; m = 2: pw = s2 */
+        for (int k = 0; k < p->m_grass / 2; ++k) pw = pw * s2;
+        if (p->m_grass % 2) pw = pw * a;
+        t3 = ((cell_aj(o, c, Hc) * pw) * a) * o->W[c];
+      }
       /* max that lets NaN win */
       if (!(t1 <= M1)) M1 = t1;
       if (!(t2 <= M2)) M2 = t2;
@@ -347,13 +381,14 @@ int orc_set_fields(orc_t* o, const double* n_manning, const double* beta, const 
       size_t s = (size_t)j * o->nx + i, d = IDX(o, i, j);
       double nm = n_manning ? n_manning[s] : o->p.n_manning;
       o->cg[d] = o->p.g * (nm * nm);
+      o->nfld[d] = nm;
       o->beta[d] = beta ? beta[s] : 0.0;
       o->srcf[d] = src ? src[s] : 0.0;
     }
   /* the fields are mirrored into the wall ghosts like H and b (reading #14) */
   {
-    double* fl[3] = {o->cg, o->beta, o->srcf};
-    for (int q = 0; q < 3; ++q) {
+    double* fl[4] = {o->cg, o->beta, o->srcf, o->nfld};
+    for (int q = 0; q < 4; ++q) {
       double* f = fl[q];
       for (int j = 0; j < o->ny; ++j)
         for (int k = 0; k < G; ++k) {
@@ -520,7 +555,7 @@ int orc_step_tau(orc_t* o, double tau) {
     for (int i = -G + 1; i < nx + G - 1; ++i) {
       size_t c = IDX(o, i, j);
       double jx, jy, ja;
-      orc_grass(p->A_J, o->ut[c], o->vt[c], &jx, &jy, &ja);
+      orc_grass_m(cell_aj(o, c, H[c]), p->m_grass, o->ut[c], o->vt[c], &jx, &jy, &ja);
       double s2 = o->ut[c] * o->ut[c] + o->vt[c] * o->vt[c];
       if (orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh)) {
         o->J0x[c] = jx; o->J0y[c] = jy; o->J0a[c] = ja;

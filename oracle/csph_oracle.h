@@ -49,6 +49,8 @@ typedef struct {
   double C_Sh;     /* Eq.5 Shamov constant; 0 = no gate */
   double d50;      /* Eq.5 median grain size */
   double q_plus, q_minus; /* Eq.1 sources (scalars) */
+  int    aj_mode;  /* NEXT-4: 0 constant A_J; 1 Eq.4 A_J = 0.05 n_M^3/((s-1) sqrt(gH) d50) */
+  double s_rel;    /* Eq.4 relative density rho_s/rho (> 1 in mode 1) */
 } orc_params;
 
 typedef struct orc orc_t;
@@ -87,6 +89,10 @@ int    orc_get_debug(const orc_t*, const char* name, double* out);
 
 /* Closed-form pieces exposed for pins (same code the step uses). */
 void   orc_grass(double A_J, double vx, double vy, double* jx, double* jy, double* jabs);
+/* Eq.3 with an integer exponent m (0..8): |v|^m = s2^(m/2) [* sqrt(s2) if m odd] */
+void   orc_grass_m(double A, int m, double vx, double vy, double* jx, double* jy, double* jabs);
+/* Eq.4: A_J = (0.05 n^3) / (((s-1) sqrt(g H)) d50) */
+double orc_aj_eq4(double g, double n_manning, double s_rel, double H, double d50);
 double orc_slope_flux(double J0n, double J0abs, double C_J, double db_dn);
 double orc_icbrt(double x);                   /* pinned x^(-1/3) recipe */
 double orc_gamma(const orc_params* p, double H, double u, double v); /* Manning gamma */

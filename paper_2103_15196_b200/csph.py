@@ -39,7 +39,7 @@ class csph_params(ctypes.Structure):
         ("C_J", ctypes.c_double), ("C_Sh", ctypes.c_double), ("d50", ctypes.c_double),
         ("q_plus", ctypes.c_double), ("q_minus", ctypes.c_double), ("precision", ctypes.c_int),
         ("device", ctypes.c_int), ("path", ctypes.c_int), ("tile_rows", ctypes.c_int),
-        ("hgs", ctypes.c_int),
+        ("hgs", ctypes.c_int), ("aj_mode", ctypes.c_int), ("s_rel", ctypes.c_double),
     ]
 
 

@@ -115,6 +115,7 @@ struct Strip {
   int ntx = 0, nty = 0;
   double* Wbuf = nullptr;            // device psi -> W field (when psi varies)
   double *cgbuf = nullptr, *betabuf = nullptr, *srcbuf = nullptr;  // NEXT-3 fields
+  double* ajbuf = nullptr;  // NEXT-4: 0.05 n_M^3 field for Eq.4
   cudaStream_t st = nullptr;
   bool own_stream = true;
   cudaEvent_t ev = nullptr;
@@ -253,7 +254,8 @@ __global__ void maxima_kernel(StripView S, const Ctrl* C, Phys P, unsigned long 
     double H = S.H[p][c];
     if (H > P.eps) {
       double t1, t2, t3;
-      dt_terms(P, H, S.Qx[p][c], S.Qy[p][c], S.W ? S.W[c] : S.Wc, t1, t2, t3);
+      dt_terms(P, H, S.Qx[p][c], S.Qy[p][c], S.W ? S.W[c] : S.Wc, cell_aj(P, S, c, H), t1, t2,
+               t3);
       m0 = dbits(t1); m1 = dbits(t2); m2 = dbits(t3);
     }
   }
@@ -261,9 +263,9 @@ __global__ void maxima_kernel(StripView S, const Ctrl* C, Phys P, unsigned long 
 }
 
 // NEXT-3: validate the uploaded field rows and turn n_M into c_gam = g n_M^2 in place.
-__global__ void fields_kernel(StripView S, double* cg, double* beta, double* src, int jlo,
-                              int jhi, double g, double n_scalar, int has_n, int has_b,
-                              int has_s, int* flags) {
+__global__ void fields_kernel(StripView S, double* cg, double* beta, double* src,
+                              double* aj0, int jlo, int jhi, double g, double n_scalar,
+                              int has_n, int has_b, int has_s, int* flags) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   int j = jlo + (int)(blockIdx.y * blockDim.y + threadIdx.y);
   int f = 0;
@@ -273,6 +275,7 @@ __global__ void fields_kernel(StripView S, double* cg, double* beta, double* src
       double n = has_n ? cg[c] : n_scalar;
       if (!(n >= 0.0 && isfinite(n))) f |= 1;
       cg[c] = g * (n * n);
+      if (aj0) aj0[c] = 0.05 * ((n * n) * n);  // Eq.4 numerator
     }
     if (beta) {
       double b = has_b ? beta[c] : 0.0;
@@ -390,7 +393,12 @@ static Phys make_phys(double dx, const csph_params& p) {
   P.dt_max = p.dt_max;
   P.src = p.q_plus - p.q_minus;
   P.fric = p.n_manning > 0.0;
-  P.transport = p.A_J > 0.0;
+  P.transport = p.A_J > 0.0 || p.aj_mode == 1;
+  P.m_grass = p.m_grass;
+  P.aj_mode = p.aj_mode;
+  P.aj0 = 0.05 * ((p.n_manning * p.n_manning) * p.n_manning);
+  P.sm1 = p.s_rel - 1.0;
+  P.d50 = p.d50;
   return P;
 }
 
@@ -406,7 +414,10 @@ static int check_params(int nx, int ny, double dx, const csph_params* p) {
   if (!(p->neg_tol >= 0.0)) return fail(CSPH_EINVAL, "neg_tol must be >= 0");
   if (!(p->n_manning >= 0.0) || !std::isfinite(p->n_manning)) return fail(CSPH_EINVAL, "n_manning");
   if (!(p->A_J >= 0.0) || !std::isfinite(p->A_J)) return fail(CSPH_EINVAL, "A_J");
-  if (p->m_grass != 2) return fail(CSPH_EINVAL, "m_grass must be 2 in the fp64 hot path");
+  if (p->m_grass < 0 || p->m_grass > 8) return fail(CSPH_EINVAL, "m_grass must be an integer in 0..8");
+  if (p->aj_mode != 0 && p->aj_mode != 1) return fail(CSPH_EINVAL, "aj_mode must be 0 or 1");
+  if (p->aj_mode == 1 && !(p->s_rel > 1.0 && std::isfinite(p->s_rel) && p->d50 > 0.0))
+    return fail(CSPH_EINVAL, "Eq.4 mode needs s_rel > 1 and d50 > 0");
   if (!std::isfinite(p->C_J)) return fail(CSPH_EINVAL, "C_J");
   if (!(p->C_Sh >= 0.0) || !std::isfinite(p->C_Sh)) return fail(CSPH_EINVAL, "C_Sh");
   if (p->C_Sh > 0.0 && !(p->d50 > 0.0)) return fail(CSPH_EINVAL, "d50 must be > 0 when C_Sh > 0");
@@ -538,6 +549,8 @@ void csph_default_params(csph_params* p) {
   p->path = CSPH_PATH_FUSED;
   p->tile_rows = 0;
   p->hgs = 1;
+  p->aj_mode = 0;
+  p->s_rel = 2.65;
 }
 
 const char* csph_last_error(void) { return g_err.c_str(); }
@@ -1017,10 +1030,15 @@ int csph_set_fields_rows(csph_t* H, int j_begin, int j_end, const double* n_mann
                   j_end, lo, hi);
     const size_t n = (size_t)(v.ny + 2 * GY) * v.pitch;
     int st;
-    double *cg = nullptr, *bt = nullptr, *sr = nullptr;
+    double *cg = nullptr, *bt = nullptr, *sr = nullptr, *aj = nullptr;
     if (has_n) {
       if (!s.cgbuf && (st = dalloc(s, (void**)&s.cgbuf, n * 8))) return st;
       cg = s.cgbuf;
+      if (H->p.aj_mode == 1) {
+        if (!s.ajbuf && (st = dalloc(s, (void**)&s.ajbuf, n * 8))) return st;
+        aj = s.ajbuf;
+        CK(cudaMemsetAsync(aj, 0, n * 8, s.st));
+      }
       CK(cudaMemsetAsync(cg, 0, n * 8, s.st));
       if ((st = upload_field_rows(s, cg, n_manning, j_begin, lo, hi, nx))) return st;
     }
@@ -1036,7 +1054,7 @@ int csph_set_fields_rows(csph_t* H, int j_begin, int j_end, const double* n_mann
     }
     CK(cudaMemsetAsync(s.dflags, 0, sizeof(int), s.st));
     dim3 blk(32, 8), grd((nx + 31) / 32, (hi - lo + 7) / 8);
-    fields_kernel<<<grd, blk, 0, s.st>>>(v, cg, bt, sr, lo - s.gj0, hi - s.gj0, H->p.g,
+    fields_kernel<<<grd, blk, 0, s.st>>>(v, cg, bt, sr, aj, lo - s.gj0, hi - s.gj0, H->p.g,
                                          H->p.n_manning, has_n, beta != nullptr,
                                          src != nullptr, s.dflags);
     CK(cudaGetLastError());
@@ -1046,7 +1064,7 @@ int csph_set_fields_rows(csph_t* H, int j_begin, int j_end, const double* n_mann
     if (flags & 1) return fail(CSPH_EINVAL, "n_manning field must be finite and >= 0");
     if (flags & 2) return fail(CSPH_EINVAL, "beta field must be finite and >= 0");
     if (flags & 4) return fail(CSPH_EINVAL, "source field must be finite and >= 0");
-    for (double* F : {cg, bt, sr}) {
+    for (double* F : {cg, bt, sr, aj}) {
       if (!F) continue;
       int n1 = (v.ny + 2 * GY) * 6, n2 = (v.nx + 6) * 6;
       mirror_field_kernel<<<(n1 + 255) / 256, 256, 0, s.st>>>(v, F);
@@ -1056,6 +1074,7 @@ int csph_set_fields_rows(csph_t* H, int j_begin, int j_end, const double* n_mann
     v.cg = cg;
     v.beta = bt;
     v.src = sr;
+    v.aj0 = aj;
   }
   H->P.fric = H->p.n_manning > 0.0 || has_n;
   return CSPH_OK;

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(NT, MINB)
             const double Hn = oH[o];
             if (Hn > P.eps) {
               double t1, t2, t3;
-              dt_terms(P, Hn, 0.0, 0.0, HASW ? S.W[o] : S.Wc, t1, t2, t3);
+              dt_terms(P, Hn, 0.0, 0.0, HASW ? S.W[o] : S.Wc, cell_aj(P, S, o, Hn), t1, t2, t3);
               unsigned long long a2 = dbits(t1), b2 = dbits(t2), c2 = dbits(t3);
               atomicMax(&gM[0], a2); atomicMax(&gM[1], b2); atomicMax(&gM[2], c2);
             }
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     if (wet) {
       double t1, t2, t3;
-      dt_terms(P, Hn, Qxn, Qyn, W3, t1, t2, t3);
+      dt_terms(P, Hn, Qxn, Qyn, W3, cell_aj(P, S, off(pitch, col, j), Hn), t1, t2, t3);
       unsigned long long a = dbits(t1), b = dbits(t2), c = dbits(t3);
       m0 = a > m0 ? a : m0; m1 = b > m1 ? b : m1; m2 = c > m2 ? c : m2;
     }
@@ -417,7 +417,8 @@ __global__ void __launch_bounds__(NT, MINB)
       v2 = v1; v1 = v0;
       r1 = r0;
       double J0x1 = 0.0, J0y1 = 0.0, J0a1 = 0.0;
-      if (P.transport) grass_gated(P, ut1, vt1, H1, J0x1, J0y1, J0a1);
+      if (P.transport)
+        grass_gated(P, ut1, vt1, H1, cell_aj(P, S, off(pitch, col, L - 1), H1), J0x1, J0y1, J0a1);
       // Delta F_x of row L-2 from the own face (t|t+1) and the west face (t-1|t)
       double dF2[4];
 #pragma unroll

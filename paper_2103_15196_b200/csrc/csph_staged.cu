@@ -118,7 +118,8 @@ __global__ void k6_corrector(StripView S, const Ctrl* __restrict__ C, Scratch T,
   if (in_range(RJ, i, j)) {
     size_t c = off(S.pitch, i, j);
     double jx, jy, ja;
-    grass_gated(P, T.ut[c], T.vt[c], S.H[p][c], jx, jy, ja);
+    const double Hc = S.H[p][c];
+    grass_gated(P, T.ut[c], T.vt[c], Hc, cell_aj(P, S, c, Hc), jx, jy, ja);
     T.J0x[c] = jx; T.J0y[c] = jy; T.J0a[c] = ja;
   }
   if (i < R.i0 || i >= R.i1 || j < R.j0 || j >= R.j1) return;
@@ -197,7 +198,7 @@ __global__ void k8_update(StripView S, Ctrl* C, Scratch T, Range R, Phys P,
     S.H[q][c] = Hn; S.Qx[q][c] = Qxn; S.Qy[q][c] = Qyn; S.b[q][c] = bn;
     if (wet) {
       double t1, t2, t3;
-      dt_terms(P, Hn, Qxn, Qyn, W, t1, t2, t3);
+      dt_terms(P, Hn, Qxn, Qyn, W, cell_aj(P, S, c, Hn), t1, t2, t3);
       m0 = dbits(t1); m1 = dbits(t2); m2 = dbits(t3);
     }
   }
