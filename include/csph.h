@@ -20,7 +20,7 @@
  *    hu, hv = momenta [m^2/s], b = bed elevation [m]; psi = bed porosity of
  *    Eq.1 (0 <= psi < 1), may be NULL (psi = 0).
  *  - Boundaries: solid reflective walls on the four global edges (DESIGN.md
- *    reading #14).
+ *    reading #14), or open zero-gradient edges (params.open_bc).
  *  - Every function returns 0 (CSPH_OK) or a negative CSPH_E* code; the
  *    thread-local csph_last_error() describes the last failure.
  *  - There is no CPU fallback: with no CUDA device every call that needs one
@@ -71,6 +71,8 @@ typedef struct {
   int    aj_mode;    /* 0 (default): constant A_J; 1: Eq.4
                         A_J = 0.05 n_M^3 / ((s-1) sqrt(g H) d50), H the local depth */
   double s_rel;      /* Eq.4 relative density rho_s/rho (> 1), default 2.65 */
+  int    open_bc;    /* NEXT-4 boundaries: bit mask of open (zero-gradient) edges,
+                        1 x-low, 2 x-high, 4 y-low, 8 y-high; default 0 = solid walls */
 } csph_params;
 
 /* Fill *p with the defaults above. */

@@ -148,7 +148,10 @@ class Oracle:
         return (self.ny + 2 * GHOST, self.nx + 2 * GHOST)
 
     def set_walls(self, xlo=True, xhi=True, ylo=True, yhi=True):
-        lib().orc_set_walls(self._h, int(xlo), int(xhi), int(ylo), int(yhi))
+        """Per side: True/1 wall, 2 open (zero-gradient), False/0 caller-supplied ghosts."""
+        st = lib().orc_set_walls(self._h, int(xlo), int(xhi), int(ylo), int(yhi))
+        if st != OK:
+            raise OracleError(st, "orc_set_walls")
 
     def set_state(self, h, hu, hv, b, psi=None) -> int:
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (h, hu, hv, b)]

@@ -244,42 +244,41 @@ void orc_destroy(orc_t* o) {
 
 int orc_set_walls(orc_t* o, int xlo, int xhi, int ylo, int yhi) {
   if (!o) return ORC_EINVAL;
-  o->wall[0] = xlo != 0; o->wall[1] = xhi != 0; o->wall[2] = ylo != 0; o->wall[3] = yhi != 0;
+  int v[4] = {xlo, xhi, ylo, yhi};
+  for (int k = 0; k < 4; ++k) {
+    if (v[k] < 0 || v[k] > 2) return ORC_EINVAL;
+    o->wall[k] = v[k];
+  }
   return ORC_OK;
 }
 
-/* Solid walls (reading #14): 3-layer mirror ghosts.  H, b, W copied, the
- * normal momentum negated, the tangential copied.  x-ghosts first on every
- * padded row (owned rows and any caller-supplied halo rows), then y-ghosts
- * over the full padded width on wall sides (corners = double mirror). */
+/* Boundary ghosts, 3 layers (reading #14): on a solid wall ghost -1-k mirrors cell k
+ * (H, b, W copied, the normal momentum negated, the tangential copied); on an open
+ * (zero-gradient, NEXT-4) side every ghost layer copies the boundary cell unchanged.
+ * x-ghosts first on every padded row (owned rows and caller-supplied halo rows),
+ * then y-ghosts over the full padded width (corners compose both rules). */
+static void ghost_copy(orc_t* o, size_t d, size_t s, int negx, int negy) {
+  o->H[d] = o->H[s]; o->b[d] = o->b[s]; o->W[d] = o->W[s];
+  o->Qx[d] = negx ? -o->Qx[s] : o->Qx[s];
+  o->Qy[d] = negy ? -o->Qy[s] : o->Qy[s];
+}
+
 static void mirror_fill(orc_t* o) {
   int nx = o->nx, ny = o->ny;
   for (int j = -G; j < ny + G; ++j) {
     for (int k = 0; k < G; ++k) {
-      if (o->wall[0]) {
-        size_t d = IDX(o, -1 - k, j), s = IDX(o, k, j);
-        o->H[d] = o->H[s]; o->b[d] = o->b[s]; o->W[d] = o->W[s];
-        o->Qx[d] = -o->Qx[s]; o->Qy[d] = o->Qy[s];
-      }
-      if (o->wall[1]) {
-        size_t d = IDX(o, nx + k, j), s = IDX(o, nx - 1 - k, j);
-        o->H[d] = o->H[s]; o->b[d] = o->b[s]; o->W[d] = o->W[s];
-        o->Qx[d] = -o->Qx[s]; o->Qy[d] = o->Qy[s];
-      }
+      if (o->wall[0] == 1) ghost_copy(o, IDX(o, -1 - k, j), IDX(o, k, j), 1, 0);
+      if (o->wall[0] == 2) ghost_copy(o, IDX(o, -1 - k, j), IDX(o, 0, j), 0, 0);
+      if (o->wall[1] == 1) ghost_copy(o, IDX(o, nx + k, j), IDX(o, nx - 1 - k, j), 1, 0);
+      if (o->wall[1] == 2) ghost_copy(o, IDX(o, nx + k, j), IDX(o, nx - 1, j), 0, 0);
     }
   }
   for (int i = -G; i < nx + G; ++i) {
     for (int k = 0; k < G; ++k) {
-      if (o->wall[2]) {
-        size_t d = IDX(o, i, -1 - k), s = IDX(o, i, k);
-        o->H[d] = o->H[s]; o->b[d] = o->b[s]; o->W[d] = o->W[s];
-        o->Qx[d] = o->Qx[s]; o->Qy[d] = -o->Qy[s];
-      }
-      if (o->wall[3]) {
-        size_t d = IDX(o, i, ny + k), s = IDX(o, i, ny - 1 - k);
-        o->H[d] = o->H[s]; o->b[d] = o->b[s]; o->W[d] = o->W[s];
-        o->Qx[d] = o->Qx[s]; o->Qy[d] = -o->Qy[s];
-      }
+      if (o->wall[2] == 1) ghost_copy(o, IDX(o, i, -1 - k), IDX(o, i, k), 0, 1);
+      if (o->wall[2] == 2) ghost_copy(o, IDX(o, i, -1 - k), IDX(o, i, 0), 0, 0);
+      if (o->wall[3] == 1) ghost_copy(o, IDX(o, i, ny + k), IDX(o, i, ny - 1 - k), 0, 1);
+      if (o->wall[3] == 2) ghost_copy(o, IDX(o, i, ny + k), IDX(o, i, ny - 1), 0, 0);
     }
   }
 }
@@ -392,13 +391,15 @@ int orc_set_fields(orc_t* o, const double* n_manning, const double* beta, const 
       double* f = fl[q];
       for (int j = 0; j < o->ny; ++j)
         for (int k = 0; k < G; ++k) {
-          if (o->wall[0]) f[IDX(o, -1 - k, j)] = f[IDX(o, k, j)];
-          if (o->wall[1]) f[IDX(o, o->nx + k, j)] = f[IDX(o, o->nx - 1 - k, j)];
+          if (o->wall[0]) f[IDX(o, -1 - k, j)] = f[IDX(o, o->wall[0] == 2 ? 0 : k, j)];
+          if (o->wall[1])
+            f[IDX(o, o->nx + k, j)] = f[IDX(o, o->wall[1] == 2 ? o->nx - 1 : o->nx - 1 - k, j)];
         }
       for (int i = -G; i < o->nx + G; ++i)
         for (int k = 0; k < G; ++k) {
-          if (o->wall[2]) f[IDX(o, i, -1 - k)] = f[IDX(o, i, k)];
-          if (o->wall[3]) f[IDX(o, i, o->ny + k)] = f[IDX(o, i, o->ny - 1 - k)];
+          if (o->wall[2]) f[IDX(o, i, -1 - k)] = f[IDX(o, i, o->wall[2] == 2 ? 0 : k)];
+          if (o->wall[3])
+            f[IDX(o, i, o->ny + k)] = f[IDX(o, i, o->wall[3] == 2 ? o->ny - 1 : o->ny - 1 - k)];
         }
     }
   }

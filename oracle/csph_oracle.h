@@ -58,7 +58,8 @@ typedef struct orc orc_t;
 /* side index: 0 = x-low (i=-1..-3), 1 = x-high, 2 = y-low, 3 = y-high */
 orc_t* orc_create(int nx, int ny, double dx, const orc_params* p);
 void   orc_destroy(orc_t*);
-/* 1 = solid wall (3-layer mirror ghosts), 0 = ghosts supplied by caller */
+/* per side: 1 = solid wall (3-layer mirror ghosts), 2 = open (zero-gradient ghosts,
+ * NEXT-4), 0 = ghosts supplied by the caller */
 int    orc_set_walls(orc_t*, int xlo, int xhi, int ylo, int yhi);
 /* interior arrays [ny][nx]; psi may be NULL (psi = 0) */
 int    orc_set_state(orc_t*, const double* h, const double* hu,

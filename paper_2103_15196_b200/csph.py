@@ -40,6 +40,7 @@ class csph_params(ctypes.Structure):
         ("q_plus", ctypes.c_double), ("q_minus", ctypes.c_double), ("precision", ctypes.c_int),
         ("device", ctypes.c_int), ("path", ctypes.c_int), ("tile_rows", ctypes.c_int),
         ("hgs", ctypes.c_int), ("aj_mode", ctypes.c_int), ("s_rel", ctypes.c_double),
+        ("open_bc", ctypes.c_int),
     ]
 
 

@@ -199,21 +199,30 @@ __global__ void ctrl_kernel(Ctrl* C, unsigned long long* gM, double* Mlast, doub
 
 // Wall ghosts of buffer (parity ^ flip): x-ghosts on owned rows, y-ghosts on
 // wall sides (full padded width, so corners are double mirrors).
+// Boundary ghosts of buffer (parity ^ flip), DESIGN.md 3.1/3.13: x-ghosts of every padded
+// row (wall: mirror, normal momentum negated; open: copy of the boundary cell), then
+// y-ghosts over the full padded width on global y edges (corners compose both rules).
 __global__ void mirror_kernel(StripView S, const Ctrl* C, int flip) {
   const int q = C->parity ^ flip;
   if (flip && C->status) return;  // a skipped step leaves the next buffer alone
   double *H = S.H[q], *Qx = S.Qx[q], *Qy = S.Qy[q], *b = S.b[q];
   const int nx = S.nx, ny = S.ny;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
-  // x-ghosts (3 per side) of every padded row: owned rows and the halo/ghost rows
-  // (wall ghost rows are rewritten by mirror_y_kernel; halo rows by the exchange)
   if (t < (ny + 2 * GY) * 6) {
     int j = t / 6 - GY, k = t % 6;
     int gi, si;
-    if (k < 3) { gi = -1 - k; si = k; }
-    else { gi = nx + (k - 3); si = nx - 1 - (k - 3); }
+    bool neg;
+    if (k < 3) {
+      gi = -1 - k;
+      si = S.bc_xlo == 2 ? 0 : k;
+      neg = S.bc_xlo == 1;
+    } else {
+      gi = nx + (k - 3);
+      si = S.bc_xhi == 2 ? nx - 1 : nx - 1 - (k - 3);
+      neg = S.bc_xhi == 1;
+    }
     size_t d = off(S.pitch, gi, j), s = off(S.pitch, si, j);
-    H[d] = H[s]; b[d] = b[s]; Qx[d] = -Qx[s]; Qy[d] = Qy[s];
+    H[d] = H[s]; b[d] = b[s]; Qx[d] = neg ? -Qx[s] : Qx[s]; Qy[d] = Qy[s];
   }
 }
 
@@ -226,16 +235,17 @@ __global__ void mirror_y_kernel(StripView S, const Ctrl* C, int flip) {
   int w = nx + 6;
   if (t >= w * 6) return;
   int i = t % w - 3, k = t / w;  // k 0..2: low side, 3..5: high side
-  int gj, sj;
+  int gj, sj, mode;
   if (k < 3) {
-    if (!S.wall_lo) return;
-    gj = -1 - k; sj = k;
+    mode = S.wall_lo;
+    gj = -1 - k; sj = mode == 2 ? 0 : k;
   } else {
-    if (!S.wall_hi) return;
-    gj = ny + (k - 3); sj = ny - 1 - (k - 3);
+    mode = S.wall_hi;
+    gj = ny + (k - 3); sj = mode == 2 ? ny - 1 : ny - 1 - (k - 3);
   }
+  if (!mode) return;
   size_t d = off(S.pitch, i, gj), s = off(S.pitch, i, sj);
-  H[d] = H[s]; b[d] = b[s]; Qx[d] = Qx[s]; Qy[d] = -Qy[s];
+  H[d] = H[s]; b[d] = b[s]; Qx[d] = Qx[s]; Qy[d] = mode == 1 ? -Qy[s] : Qy[s];
 }
 
 __global__ void w_from_psi_kernel(double* W, const double* psi, size_t n) {  // in place ok
@@ -290,14 +300,15 @@ __global__ void fields_kernel(StripView S, double* cg, double* beta, double* src
   if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
 }
 
-// Mirror a static per-cell field into the wall ghosts (copy, no sign change).
+// Boundary ghosts of a static per-cell field (copy: mirror on walls, boundary cell on
+// open sides).
 __global__ void mirror_field_kernel(StripView S, double* F) {
   const int nx = S.nx, ny = S.ny;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < (ny + 2 * GY) * 6) {
     int j = t / 6 - GY, k = t % 6;
     int gi = k < 3 ? -1 - k : nx + (k - 3);
-    int si = k < 3 ? k : nx - 1 - (k - 3);
+    int si = k < 3 ? (S.bc_xlo == 2 ? 0 : k) : (S.bc_xhi == 2 ? nx - 1 : nx - 1 - (k - 3));
     F[off(S.pitch, gi, j)] = F[off(S.pitch, si, j)];
   }
 }
@@ -310,10 +321,11 @@ __global__ void mirror_field_y_kernel(StripView S, double* F) {
   int i = t % w - 3, k = t / w;
   if (k < 3) {
     if (!S.wall_lo) return;
-    F[off(S.pitch, i, -1 - k)] = F[off(S.pitch, i, k)];
+    F[off(S.pitch, i, -1 - k)] = F[off(S.pitch, i, S.wall_lo == 2 ? 0 : k)];
   } else {
     if (!S.wall_hi) return;
-    F[off(S.pitch, i, ny + (k - 3))] = F[off(S.pitch, i, ny - 1 - (k - 3))];
+    F[off(S.pitch, i, ny + (k - 3))] =
+        F[off(S.pitch, i, S.wall_hi == 2 ? ny - 1 : ny - 1 - (k - 3))];
   }
 }
 
@@ -424,6 +436,7 @@ static int check_params(int nx, int ny, double dx, const csph_params* p) {
   if (!std::isfinite(p->q_plus) || !std::isfinite(p->q_minus)) return fail(CSPH_EINVAL, "q_plus/q_minus");
   if (p->precision != 64) return fail(CSPH_EINVAL, "precision must be 64");
   if (p->path != CSPH_PATH_FUSED && p->path != CSPH_PATH_STAGED) return fail(CSPH_EINVAL, "path");
+  if (p->open_bc < 0 || p->open_bc > 15) return fail(CSPH_EINVAL, "open_bc is a 4-bit mask");
   return CSPH_OK;
 }
 
@@ -445,8 +458,12 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
   v.nx = H->nx;
   v.ny = rows;
   v.pitch = ((H->nx + GX + 3) + 31) / 32 * 32;
-  v.wall_lo = gj0 == 0;
-  v.wall_hi = gj0 + rows == H->ny;
+  // y edges: 0 halo (interior strip edge), 1 wall, 2 open; x edges: 1 wall, 2 open
+  const int ob = H->p.open_bc;
+  v.wall_lo = gj0 == 0 ? ((ob & 4) ? 2 : 1) : 0;
+  v.wall_hi = gj0 + rows == H->ny ? ((ob & 8) ? 2 : 1) : 0;
+  v.bc_xlo = (ob & 1) ? 2 : 1;
+  v.bc_xhi = (ob & 2) ? 2 : 1;
   v.W = nullptr;
   v.Wc = 1.0;
   size_t n = (size_t)(rows + 2 * GY) * v.pitch;
@@ -551,6 +568,7 @@ void csph_default_params(csph_params* p) {
   p->hgs = 1;
   p->aj_mode = 0;
   p->s_rel = 2.65;
+  p->open_bc = 0;
 }
 
 const char* csph_last_error(void) { return g_err.c_str(); }

@@ -116,7 +116,7 @@ __device__ __forceinline__ double minmod_bf(double a, double b) {
   return same ? m : 0.0;
 }
 
-template <int NT, bool HASW, int D, int PF, int MINB>
+template <int NT, bool HASW, int D, int PF, int MINB, bool GEN>
 __global__ void __launch_bounds__(NT, MINB)
     fused_step_kernel(StripView S, Ctrl* __restrict__ C, Phys P,
                       unsigned long long* __restrict__ gM, int row0, int row1, int TY, Hgs hg) {
@@ -173,22 +173,10 @@ __global__ void __launch_bounds__(NT, MINB)
             double Hn = H3 - lam * z;
             double Qn = 0.0 - lam * z, Qm = Qn;
             const double bn = (b3 - (lam * W3) * z) + (tau * W3) * P.src;
-            apply_sources(S, tau, o, Hn, Qn, Qm);
+            if (GEN) apply_sources(S, tau, o, Hn, Qn, Qm);
             if (Hn > P.eps) cwet = true;  // momenta stay +0 (they were +0 * a)
-            oH[o] = Hn; ob[o] = bn; oQx[o] = Qn; oQy[o] = Qn;
-            const bool gx = col < 3 || col >= nx - 3;
-            const bool gy = (S.wall_lo && j < 3) || (S.wall_hi && j >= ny - 3);
-            if (gx || gy) {
-              int gc[3] = {col, col < 3 ? -1 - col : INT_MIN, col >= nx - 3 ? 2 * nx - 1 - col : INT_MIN};
-              int gr[3] = {j, (S.wall_lo && j < 3) ? -1 - j : INT_MIN,
-                           (S.wall_hi && j >= ny - 3) ? 2 * ny - 1 - j : INT_MIN};
-              for (int a = 0; a < 3; ++a)
-                for (int c2 = 0; c2 < 3; ++c2) {
-                  if ((a | c2) == 0 || gc[a] == INT_MIN || gr[c2] == INT_MIN) continue;
-                  const size_t g = off(pitch, gc[a], gr[c2]);
-                  oH[g] = Hn; ob[g] = bn; oQx[g] = a ? -Qn : Qn; oQy[g] = c2 ? -Qn : Qn;
-                }
-            }
+            if (GEN) write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
+            else write_with_wall_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
           }
         }
         const bool any = __syncthreads_or(cwet);
@@ -205,7 +193,8 @@ __global__ void __launch_bounds__(NT, MINB)
             const double Hn = oH[o];
             if (Hn > P.eps) {
               double t1, t2, t3;
-              dt_terms(P, Hn, 0.0, 0.0, HASW ? S.W[o] : S.Wc, cell_aj(P, S, o, Hn), t1, t2, t3);
+              dt_terms<GEN>(P, Hn, 0.0, 0.0, HASW ? S.W[o] : S.Wc,
+                            GEN ? cell_aj(P, S, o, Hn) : P.A_J, t1, t2, t3);
               unsigned long long a2 = dbits(t1), b2 = dbits(t2), c2 = dbits(t3);
               atomicMax(&gM[0], a2); atomicMax(&gM[1], b2); atomicMax(&gM[2], c2);
             }
@@ -277,6 +266,7 @@ __global__ void __launch_bounds__(NT, MINB)
   unsigned hist = 0;  // wet flags of rows L..L-4 of this column (bit 0 = row L)
 
   const bool col_out = (t >= 4) && (t < 4 + TX) && (col < nx);
+  const bool colg = feeds_xghost(S, col);
 
   // K8 epilogue for one cell: dry-momentum zeroing, negative-depth flag, stores,
   // wall ghosts and the next step's Eq.7 terms.
@@ -286,27 +276,12 @@ __global__ void __launch_bounds__(NT, MINB)
     anywet |= wet;
     if (!wet) { Qxn = 0.0; Qyn = 0.0; }
     if (Hn < -P.neg_tol) neg = true;
-    const size_t o = off(pitch, col, j);
-    oH[o] = Hn; oQx[o] = Qxn; oQy[o] = Qyn; ob[o] = bn;
-    // a cell within 3 of both walls of a small grid mirrors into both sides
-    const bool gx = col < 3 || col >= nx - 3;
-    const bool gy = (S.wall_lo && j < 3) || (S.wall_hi && j >= ny - 3);
-    if (gx || gy) {
-      int gc[3] = {col, col < 3 ? -1 - col : INT_MIN, col >= nx - 3 ? 2 * nx - 1 - col : INT_MIN};
-      int gr[3] = {j, (S.wall_lo && j < 3) ? -1 - j : INT_MIN,
-                   (S.wall_hi && j >= ny - 3) ? 2 * ny - 1 - j : INT_MIN};
-      for (int a = 0; a < 3; ++a)
-        for (int c2 = 0; c2 < 3; ++c2) {
-          if ((a | c2) == 0 || gc[a] == INT_MIN || gr[c2] == INT_MIN) continue;
-          const size_t g = off(pitch, gc[a], gr[c2]);
-          oH[g] = Hn; ob[g] = bn;
-          oQx[g] = a ? -Qxn : Qxn;
-          oQy[g] = c2 ? -Qyn : Qyn;
-        }
-    }
+    if (GEN) write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
+    else write_with_wall_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
     if (wet) {
       double t1, t2, t3;
-      dt_terms(P, Hn, Qxn, Qyn, W3, cell_aj(P, S, off(pitch, col, j), Hn), t1, t2, t3);
+      dt_terms<GEN>(P, Hn, Qxn, Qyn, W3, GEN ? cell_aj(P, S, off(pitch, col, j), Hn) : P.A_J,
+                    t1, t2, t3);
       unsigned long long a = dbits(t1), b = dbits(t2), c = dbits(t3);
       m0 = a > m0 ? a : m0; m1 = b > m1 ? b : m1; m2 = c > m2 ? c : m2;
     }
@@ -360,7 +335,7 @@ __global__ void __launch_bounds__(NT, MINB)
         double Qxn = QLx3 - lam * dQx;
         double Qyn = QLy3 - lam * dQy;
         const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
-        apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
+        if (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
         store_update(Hn, Qxn, Qyn, bn, W3, j);
       }
       QLx3 = 0.0; QLy3 = 0.0;
@@ -381,7 +356,7 @@ __global__ void __launch_bounds__(NT, MINB)
       const double uu = RG(F_QX, k, 0) * rr, vv = RG(F_QY, k, 0) * rr;
       double gg = 0.0;
       if (P.fric) {
-        const double cgc = S.cg ? S.cg[off(pitch, col, L)] : P.cgam;  // NEXT-3 field
+        const double cgc = (GEN && S.cg) ? S.cg[off(pitch, col, L)] : P.cgam;  // NEXT-3 field
         gg = (cgc * sqrt0nb(uu * uu + vv * vv)) * (rr * icbrt(Hs));
       }
       r0 = w0 ? rr : 0.0; u0 = w0 ? uu : 0.0; v0 = w0 ? vv : 0.0; gam0 = w0 ? gg : 0.0;
@@ -418,7 +393,8 @@ __global__ void __launch_bounds__(NT, MINB)
       r1 = r0;
       double J0x1 = 0.0, J0y1 = 0.0, J0a1 = 0.0;
       if (P.transport)
-        grass_gated(P, ut1, vt1, H1, cell_aj(P, S, off(pitch, col, L - 1), H1), J0x1, J0y1, J0a1);
+        grass_gated<GEN>(P, ut1, vt1, H1, GEN ? cell_aj(P, S, off(pitch, col, L - 1), H1) : P.A_J,
+                         J0x1, J0y1, J0a1);
       // Delta F_x of row L-2 from the own face (t|t+1) and the west face (t-1|t)
       double dF2[4];
 #pragma unroll
@@ -523,7 +499,7 @@ __global__ void __launch_bounds__(NT, MINB)
         double Qxn = QLx3 - lam * dQx;
         double Qyn = QLy3 - lam * dQy;
         const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
-        apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
+        if (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
         store_update(Hn, Qxn, Qyn, bn, W3, j);
       }
       QLx3 = QLx2; QLy3 = QLy2;
@@ -560,7 +536,7 @@ __global__ void __launch_bounds__(NT, MINB)
   }
 }
 
-template <int NT, bool HASW, int D, int PF, int MINB>
+template <int NT, bool HASW, int D, int PF, int MINB, bool GEN>
 void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM, int row0,
               int row1, int TY, const Hgs& hg, cudaStream_t st) {
   using SM = Smem<NT, HASW, D>;
@@ -568,12 +544,12 @@ void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
   static bool configured = false;
   const size_t smem = sizeof(SM);
   if (!configured) {
-    cudaFuncSetAttribute(fused_step_kernel<NT, HASW, D, PF, MINB>,
+    cudaFuncSetAttribute(fused_step_kernel<NT, HASW, D, PF, MINB, GEN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   dim3 grid((unsigned)((S.nx + TX - 1) / TX), (unsigned)((row1 - row0 + TY - 1) / TY));
-  fused_step_kernel<NT, HASW, D, PF, MINB><<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY,
+  fused_step_kernel<NT, HASW, D, PF, MINB, GEN><<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY,
                                                                   hg);
 }
 
@@ -582,10 +558,16 @@ void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
               int row1, int TY, const Hgs& hg, cudaStream_t st) {
   Hgs h = hg;
   if (NT - 8 != FUSED_TX) h.enable = 0;  // tiling of the flags is FUSED_TX wide
-  if (S.W)
-    launch_t<NT, true, D, PF, MINB>(S, C, P, gM, row0, row1, TY, h, st);
-  else
-    launch_t<NT, false, D, PF, MINB>(S, C, P, gM, row0, row1, TY, h, st);
+  // GEN: NEXT-3/4 features present; otherwise the hot-path specialisation
+  const bool gen = P.m_grass != 2 || P.aj_mode || S.cg || S.beta || S.aj0 || S.bc_xlo != 1 ||
+                   S.bc_xhi != 1 || S.wall_lo == 2 || S.wall_hi == 2;
+  if (S.W) {
+    if (gen) launch_t<NT, true, D, PF, MINB, true>(S, C, P, gM, row0, row1, TY, h, st);
+    else launch_t<NT, true, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
+  } else {
+    if (gen) launch_t<NT, false, D, PF, MINB, true>(S, C, P, gM, row0, row1, TY, h, st);
+    else launch_t<NT, false, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
+  }
 }
 
 int fused_variant() {
@@ -605,17 +587,8 @@ void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long
   if (row1 <= row0) return;
   int TY = tile_rows > 0 ? tile_rows : 128;
   switch (fused_variant()) {
-    case 0: launch_v<128, 8, 3, 1>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 2: launch_v<256, 6, 1, 2>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 3: launch_v<128, 7, 2, 4>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 4: launch_v<128, 6, 1, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 5: launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
     case 6: launch_v<128, 10, 5, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 7: launch_v<64, 8, 3, 6>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 8: launch_v<96, 8, 3, 4>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 9: launch_v<128, 12, 7, 2>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 10: launch_v<128, 9, 4, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    default: launch_v<128, 6, 1, 4>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    default: launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
   }
   *nlaunch += 1;
 }

@@ -113,3 +113,98 @@ def test_gpu_closure_parity(path, case):
     assert np.array_equal(dt, dt_r)
     for x, y in zip(g.get_state(), ref.get_state()):
         assert np.array_equal(x, y)
+
+
+# ---------------------------------------------------------------- open boundaries
+
+def test_open_boundaries_keep_a_uniform_current():
+    """Zero-gradient (open) ghosts (NEXT-4): a uniform current in a
+    frictionless channel open at both ends is an exact steady state -- every face
+    sees the same two states -- while walls would reflect it."""
+    nx, ny = 30, 5
+    H0, u0 = 1.2, 0.7
+    h = np.full((ny, nx), H0); hu = np.full((ny, nx), H0 * u0); z = np.zeros((ny, nx))
+    o = oracle.Oracle(nx, ny, 1.0, oracle.Params())
+    o.set_walls(2, 2, 1, 1)
+    o.set_state(h, hu, z, z)
+    o.step(25)
+    H, Qx, Qy, b = o.get_state()
+    assert np.all(H == H0) and np.all(Qx == H0 * u0) and np.all(Qy == 0.0)
+    w = oracle.Oracle(nx, ny, 1.0, oracle.Params())
+    w.set_state(h, hu, z, z)
+    w.step(25)
+    assert not np.all(w.get_state()[0] == H0)
+
+
+def test_open_boundary_drains_a_dam_break():
+    """A dam break with an open x-high edge: identical to the walled run until the
+    front reaches the edge, then water leaves -- the volume never increases and
+    ends well below its start."""
+    nx, ny = 40, 4
+    h = np.zeros((ny, nx)); h[:, :20] = 1.0
+    z = np.zeros((ny, nx))
+    o = oracle.Oracle(nx, ny, 1.0, oracle.Params())
+    o.set_walls(1, 2, 1, 1)
+    o.set_state(h, z, z, z)
+    w = oracle.Oracle(nx, ny, 1.0, oracle.Params())
+    w.set_state(h, z, z, z)
+    o.step(5); w.step(5)
+    for a, b in zip(o.get_state(), w.get_state()):
+        assert np.array_equal(a, b)  # the front is still far from the edge
+    V = [math.fsum(o.get_state()[0].ravel())]
+    for _ in range(60):
+        st, _, _ = o.step(10)
+        assert st == 0
+        V.append(math.fsum(o.get_state()[0].ravel()))
+    assert V[-1] < 0.7 * V[0]
+    assert all(b <= a * (1 + 1e-14) for a, b in zip(V, V[1:]))
+
+
+def test_open_boundaries_keep_lake_at_rest():
+    """Well-balance with open edges: a dyadic lake at rest stays bitwise at rest."""
+    c = synth.config("C2", 64, 48)
+    h, hu, hv, b, psi = synth.fill(c)
+    o = oracle.Oracle(c.nx, c.ny, 1.0, oracle.Params(**c.params))
+    o.set_walls(2, 2, 2, 2)
+    o.set_state(h, hu, hv, b, psi)
+    o.step(200)
+    H, Qx, Qy, bn = o.get_state()
+    assert np.array_equal(H, h) and np.all(Qx == 0.0) and np.array_equal(bn, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("mask", [2, 5, 15])
+def test_gpu_open_boundary_parity(path, mask):
+    from paper_2103_15196_b200 import build, csph
+    build.build()
+    c = synth.config("C4", 190, 210)
+    h, hu, hv, b, psi = synth.fill(c)
+    sides = [2 if mask & (1 << k) else 1 for k in range(4)]
+    ref = oracle.Oracle(c.nx, c.ny, 1.0, oracle.Params(**c.params))
+    ref.set_walls(*sides)
+    ref.set_state(h, hu, hv, b, psi)
+    st_r, dt_r, _ = ref.step(80)
+    g = csph.csph_create(c.nx, c.ny, 1.0, csph.params_from(c.params, path=path, open_bc=mask))
+    g.set_state(h, hu, hv, b, psi)
+    assert g.step(80, check=False) == st_r
+    dt, _ = g.get_dt_log(80)
+    assert np.array_equal(dt, dt_r)
+    for x, y in zip(g.get_state(), ref.get_state()):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.gpu
+def test_gpu_open_boundary_strips():
+    """Open y edges with the strip decomposition (3 strips on one GPU)."""
+    from paper_2103_15196_b200 import build, csph
+    build.build()
+    c = synth.config("C5", 160, 150)
+    f = synth.fill(c)
+    p = csph.params_from(c.params, open_bc=12)
+    a = csph.csph_create(c.nx, c.ny, 1.0, p)
+    a.set_state(*f); a.step(40)
+    m = csph.csph_create_multi(c.nx, c.ny, 1.0, p, [0, 0, 0])
+    m.set_state(*f); m.step(40)
+    for x, y in zip(a.get_state(), m.get_state()):
+        assert np.array_equal(x, y)
