@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override the grid size (n x n)")
     ap.add_argument("--path", choices=["fused", "staged"], default="fused")
     ap.add_argument("--tile-rows", type=int, default=0)
+    ap.add_argument("--precision", type=int, choices=[64, 32], default=64,
+                    help="32 = the NEXT-2 fp32 mode (not the headline metric)")
     ap.add_argument("--e2e-steps", type=int, default=100,
                     help="steps between host saves in the end-to-end run (P:131: 100-1000)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -194,7 +196,8 @@ def run_ours(a, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = synth.config(a.config, a.n)
     path = csph.CSPH_PATH_FUSED if a.path == "fused" else csph.CSPH_PATH_STAGED
-    p = csph.params_from(c.params, path=path, device=local, tile_rows=a.tile_rows)
+    p = csph.params_from(c.params, path=path, device=local, tile_rows=a.tile_rows,
+                         precision=a.precision)
     j0, j1 = csph.csph_strip_rows(c.ny, world, rank)
     wa, wb = max(0, j0 - 3), min(c.ny, j1 + 3)
     fields = synth.fill(c, wa, wb)
@@ -259,14 +262,15 @@ def run_ours(a, rank, world, local):
 
     # ---- roofline of the dominant kernel (the fused step kernel) ----
     peak, peak_src = peaks()
-    bpc = 72 if psi_field else 64  # algorithmic bytes per cell-update
+    es = 8 if a.precision == 64 else 4
+    bpc = (9 if psi_field else 8) * es  # algorithmic bytes per cell-update
     own_cells = c.nx * (j1 - j0)
     kern_ms_per = kern_ms / max(kern_steps, 1)
     # HGS: marched tiles move bpc B/cell, identity-copied tiles read H, b (+W) and write
     # 4 fields, skipped tiles move nothing
     ntile = max(sum(tiles), 1)
     f_march, f_copy, f_skip = (x / ntile for x in tiles)
-    bpc_copy = (24 if psi_field else 16) + 32
+    bpc_copy = ((3 if psi_field else 2) + 4) * es
     bytes_per_step = own_cells * (bpc * f_march + bpc_copy * f_copy)
     achieved = bytes_per_step / (kern_ms_per / 1e3) / 1e9
     tr = ncu_traffic("fused_step_kernel" if path == csph.CSPH_PATH_FUSED else "k7_fluxes")
@@ -326,7 +330,8 @@ def run_ours(a, rank, world, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if a.precision == 64 else "f32", "data": "synthetic",
             "config": {
                 "workload": f"{a.config} river-floodplain flood + sediment transport"
                             if a.config == "C5" else a.config,

@@ -14,6 +14,7 @@
 
 #include "../../include/csph.h"
 #include "csph_launch.h"
+#include "csph_real.cuh"
 
 using namespace ck;
 
@@ -114,6 +115,8 @@ struct Strip {
   unsigned long long* hstats = nullptr;  // HGS tile counters: marched, copied, skipped
   int ntx = 0, nty = 0;
   double* Wbuf = nullptr;            // device psi -> W field (when psi varies)
+  float* Wbuf32 = nullptr;           // fp32 mode W field
+  double* tmpd = nullptr;            // fp32 mode: fp64 staging for get_state
   double *cgbuf = nullptr, *betabuf = nullptr, *srcbuf = nullptr;  // NEXT-3 fields
   double* ajbuf = nullptr;  // NEXT-4: 0.05 n_M^3 field for Eq.4
   cudaStream_t st = nullptr;
@@ -202,10 +205,11 @@ __global__ void ctrl_kernel(Ctrl* C, unsigned long long* gM, double* Mlast, doub
 // Boundary ghosts of buffer (parity ^ flip), DESIGN.md 3.1/3.13: x-ghosts of every padded
 // row (wall: mirror, normal momentum negated; open: copy of the boundary cell), then
 // y-ghosts over the full padded width on global y edges (corners compose both rules).
+template <typename T>
 __global__ void mirror_kernel(StripView S, const Ctrl* C, int flip) {
   const int q = C->parity ^ flip;
   if (flip && C->status) return;  // a skipped step leaves the next buffer alone
-  double *H = S.H[q], *Qx = S.Qx[q], *Qy = S.Qy[q], *b = S.b[q];
+  T *H = (T*)S.H[q], *Qx = (T*)S.Qx[q], *Qy = (T*)S.Qy[q], *b = (T*)S.b[q];
   const int nx = S.nx, ny = S.ny;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < (ny + 2 * GY) * 6) {
@@ -226,10 +230,11 @@ __global__ void mirror_kernel(StripView S, const Ctrl* C, int flip) {
   }
 }
 
+template <typename T>
 __global__ void mirror_y_kernel(StripView S, const Ctrl* C, int flip) {
   const int q = C->parity ^ flip;
   if (flip && C->status) return;
-  double *H = S.H[q], *Qx = S.Qx[q], *Qy = S.Qy[q], *b = S.b[q];
+  T *H = (T*)S.H[q], *Qx = (T*)S.Qx[q], *Qy = (T*)S.Qy[q], *b = (T*)S.b[q];
   const int nx = S.nx, ny = S.ny;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   int w = nx + 6;
@@ -329,6 +334,37 @@ __global__ void mirror_field_y_kernel(StripView S, double* F) {
   }
 }
 
+// fp32 state: the same Eq.7 terms computed in fp32 (NEXT-2), maxima kept as fp64 bits.
+__global__ void maxima32_kernel(StripView S, const Ctrl* C, Phys P, unsigned long long* gM) {
+  const int p = C->parity;
+  const PT<float> Q = make_pt<float>(P);
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int j = blockIdx.y * blockDim.y + threadIdx.y;
+  unsigned long long m0 = 0, m1 = 0, m2 = 0;
+  if (i < S.nx && j < S.ny) {
+    size_t c = off(S.pitch, i, j);
+    const float H = ((const float*)S.H[p])[c];
+    if (H > Q.eps) {
+      float t1, t2, t3;
+      const float W = S.W ? ((const float*)S.W)[c] : (float)S.Wc;
+      dt_terms_t<false>(Q, H, ((const float*)S.Qx[p])[c], ((const float*)S.Qy[p])[c], W, Q.A_J,
+                        t1, t2, t3);
+      m0 = dbits_t(t1); m1 = dbits_t(t2); m2 = dbits_t(t3);
+    }
+  }
+  block_max3_atomic<8>(m0, m1, m2, gM);
+}
+
+// fp64 <-> fp32 conversion of one padded field (NEXT-2 set/get state)
+__global__ void to_f32_kernel(float* dst, const double* src, size_t n) {
+  size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) dst[k] = (float)src[k];
+}
+__global__ void to_f64_kernel(double* dst, const float* src, size_t n) {
+  size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) dst[k] = (double)src[k];
+}
+
 __global__ void max_gather_kernel(unsigned long long* dst, const unsigned long long* src,
                                   int n) {
   if (threadIdx.x < 3) {
@@ -376,9 +412,14 @@ namespace ck {
 void launch_mirror(const StripView& S, const Ctrl* C, int flip, cudaStream_t st,
                    long long* nlaunch) {
   int n1 = (S.ny + 2 * GY) * 6;
-  mirror_kernel<<<(n1 + 255) / 256, 256, 0, st>>>(S, C, flip);
   int n2 = (S.nx + 6) * 6;
-  mirror_y_kernel<<<(n2 + 255) / 256, 256, 0, st>>>(S, C, flip);
+  if (S.prec == 4) {
+    mirror_kernel<float><<<(n1 + 255) / 256, 256, 0, st>>>(S, C, flip);
+    mirror_y_kernel<float><<<(n2 + 255) / 256, 256, 0, st>>>(S, C, flip);
+  } else {
+    mirror_kernel<double><<<(n1 + 255) / 256, 256, 0, st>>>(S, C, flip);
+    mirror_y_kernel<double><<<(n2 + 255) / 256, 256, 0, st>>>(S, C, flip);
+  }
   *nlaunch += 2;
 }
 }  // namespace ck
@@ -434,7 +475,11 @@ static int check_params(int nx, int ny, double dx, const csph_params* p) {
   if (!(p->C_Sh >= 0.0) || !std::isfinite(p->C_Sh)) return fail(CSPH_EINVAL, "C_Sh");
   if (p->C_Sh > 0.0 && !(p->d50 > 0.0)) return fail(CSPH_EINVAL, "d50 must be > 0 when C_Sh > 0");
   if (!std::isfinite(p->q_plus) || !std::isfinite(p->q_minus)) return fail(CSPH_EINVAL, "q_plus/q_minus");
-  if (p->precision != 64) return fail(CSPH_EINVAL, "precision must be 64");
+  if (p->precision != 64 && p->precision != 32) return fail(CSPH_EINVAL, "precision must be 64 or 32");
+  if (p->precision == 32 && (p->path != CSPH_PATH_FUSED || p->m_grass != 2 || p->aj_mode != 0 ||
+                             p->open_bc != 0))
+    return fail(CSPH_EINVAL,
+                "precision 32 (NEXT-2) runs the fused path with walls, m_grass = 2, constant A_J");
   if (p->path != CSPH_PATH_FUSED && p->path != CSPH_PATH_STAGED) return fail(CSPH_EINVAL, "path");
   if (p->open_bc < 0 || p->open_bc > 15) return fail(CSPH_EINVAL, "open_bc is a 4-bit mask");
   return CSPH_OK;
@@ -464,6 +509,7 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
   v.wall_hi = gj0 + rows == H->ny ? ((ob & 8) ? 2 : 1) : 0;
   v.bc_xlo = (ob & 1) ? 2 : 1;
   v.bc_xhi = (ob & 2) ? 2 : 1;
+  v.prec = H->p.precision == 32 ? 4 : 8;
   v.W = nullptr;
   v.Wc = 1.0;
   size_t n = (size_t)(rows + 2 * GY) * v.pitch;
@@ -806,19 +852,20 @@ static int halo_nccl(csph* H, int q, cudaStream_t stream) {
   Strip& s = H->s[0];
   const StripView& v = s.v;
   const size_t cnt = (size_t)GY * v.pitch;
-  double* f[4] = {v.H[q], v.Qx[q], v.Qy[q], v.b[q]};
+  const size_t es = (size_t)v.prec;  // element size: fp64 or fp32 state
+  const ncclDataType_t dt = v.prec == 4 ? ncclFloat32 : ncclFloat64;
+  char* f[4] = {(char*)v.H[q], (char*)v.Qx[q], (char*)v.Qy[q], (char*)v.b[q]};
   if (H->nranks == 1) return CSPH_OK;
   NK(g_nccl.GroupStart());
   for (int k = 0; k < 4; ++k) {
     if (H->rank > 0) {
-      NK(g_nccl.Send(f[k] + off(v.pitch, -GX, 0), cnt, ncclFloat64, H->rank - 1, H->comm, stream));
-      NK(g_nccl.Recv(f[k] + off(v.pitch, -GX, -GY), cnt, ncclFloat64, H->rank - 1, H->comm, stream));
+      NK(g_nccl.Send(f[k] + es * off(v.pitch, -GX, 0), cnt, dt, H->rank - 1, H->comm, stream));
+      NK(g_nccl.Recv(f[k] + es * off(v.pitch, -GX, -GY), cnt, dt, H->rank - 1, H->comm, stream));
     }
     if (H->rank < H->nranks - 1) {
-      NK(g_nccl.Send(f[k] + off(v.pitch, -GX, v.ny - GY), cnt, ncclFloat64, H->rank + 1, H->comm,
+      NK(g_nccl.Send(f[k] + es * off(v.pitch, -GX, v.ny - GY), cnt, dt, H->rank + 1, H->comm,
                      stream));
-      NK(g_nccl.Recv(f[k] + off(v.pitch, -GX, v.ny), cnt, ncclFloat64, H->rank + 1, H->comm,
-                     stream));
+      NK(g_nccl.Recv(f[k] + es * off(v.pitch, -GX, v.ny), cnt, dt, H->rank + 1, H->comm, stream));
     }
   }
   NK(g_nccl.GroupEnd());
@@ -865,21 +912,24 @@ static int exchange(csph* H, int q) {
       if (r > 0)
         CK(cudaMemcpyPeerAsync(s.gM, s.dev, s0.gM, s0.dev, 3 * sizeof(unsigned long long), s.st));
       const StripView& v = s.v;
-      const size_t bytes = (size_t)GY * v.pitch * 8;
-      double* f[4] = {v.H[q], v.Qx[q], v.Qy[q], v.b[q]};
+      const size_t es = (size_t)v.prec;
+      const size_t bytes = (size_t)GY * v.pitch * es;
+      char* f[4] = {(char*)v.H[q], (char*)v.Qx[q], (char*)v.Qy[q], (char*)v.b[q]};
       if (r > 0) {
         const Strip& o = H->s[r - 1];
-        const double* g[4] = {o.v.H[q], o.v.Qx[q], o.v.Qy[q], o.v.b[q]};
+        const char* g[4] = {(const char*)o.v.H[q], (const char*)o.v.Qx[q], (const char*)o.v.Qy[q],
+                            (const char*)o.v.b[q]};
         for (int k = 0; k < 4; ++k)
-          CK(cudaMemcpyPeerAsync(f[k] + off(v.pitch, -GX, -GY), s.dev,
-                                 g[k] + off(o.v.pitch, -GX, o.v.ny - GY), o.dev, bytes, s.st));
+          CK(cudaMemcpyPeerAsync(f[k] + es * off(v.pitch, -GX, -GY), s.dev,
+                                 g[k] + es * off(o.v.pitch, -GX, o.v.ny - GY), o.dev, bytes, s.st));
       }
       if (r < n - 1) {
         const Strip& o = H->s[r + 1];
-        const double* g[4] = {o.v.H[q], o.v.Qx[q], o.v.Qy[q], o.v.b[q]};
+        const char* g[4] = {(const char*)o.v.H[q], (const char*)o.v.Qx[q], (const char*)o.v.Qy[q],
+                            (const char*)o.v.b[q]};
         for (int k = 0; k < 4; ++k)
-          CK(cudaMemcpyPeerAsync(f[k] + off(v.pitch, -GX, v.ny), s.dev,
-                                 g[k] + off(o.v.pitch, -GX, 0), o.dev, bytes, s.st));
+          CK(cudaMemcpyPeerAsync(f[k] + es * off(v.pitch, -GX, v.ny), s.dev,
+                                 g[k] + es * off(o.v.pitch, -GX, 0), o.dev, bytes, s.st));
       }
     }
     // every strip must finish reading its neighbours before they run ahead
@@ -901,13 +951,13 @@ static int exchange(csph* H, int q) {
 // Input validation on the device (CSPH_EINVAL on NaN/Inf, h < 0, psi
 // outside [0,1)); bit 3 = psi is not uniform over this strip's rows.
 __global__ void validate_kernel(StripView S, int jlo, int jhi, const double* psi, double psi0,
-                                int* flags) {
+                                int* flags, int buf) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   int j = jlo + (int)(blockIdx.y * blockDim.y + threadIdx.y);
   int f = 0;
   if (i < S.nx && j < jhi) {
     size_t c = off(S.pitch, i, j);
-    double H = S.H[0][c], qx = S.Qx[0][c], qy = S.Qy[0][c], b = S.b[0][c];
+    double H = S.H[buf][c], qx = S.Qx[buf][c], qy = S.Qy[buf][c], b = S.b[buf][c];
     if (!isfinite(H) || !isfinite(qx) || !isfinite(qy) || !isfinite(b)) f |= 1;
     if (H < 0.0) f |= 2;
     if (psi) {
@@ -920,6 +970,10 @@ __global__ void validate_kernel(StripView S, int jlo, int jhi, const double* psi
   if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
 }
 
+static double* src_dst0(const StripView& v, int k) {
+  return k == 0 ? v.H[0] : k == 1 ? v.Qx[0] : k == 2 ? v.Qy[0] : v.b[0];
+}
+
 static int upload_rows(csph* H, Strip& s, int j_begin, int j_end, const double* h,
                        const double* hu, const double* hv, const double* b, const double* psi) {
   // rows of this strip incl. halo rows where a neighbour exists
@@ -930,8 +984,9 @@ static int upload_rows(csph* H, Strip& s, int j_begin, int j_end, const double* 
     return fail(CSPH_EINVAL, "rows [%d,%d) do not cover strip rows [%d,%d) + halo", j_begin,
                 j_end, lo, hi);
   const int nx = H->nx;
+  const int ub = v.prec == 4 ? 1 : 0;  // fp32 mode: fp64 upload into buffer 1, then convert
   const double* src[4] = {h, hu, hv, b};
-  double* dst[4] = {v.H[0], v.Qx[0], v.Qy[0], v.b[0]};
+  double* dst[4] = {v.H[ub], v.Qx[ub], v.Qy[ub], v.b[ub]};
   for (int k = 0; k < 4; ++k) {
     const double* a = src[k] + (size_t)(lo - j_begin) * nx;
     double* d = dst[k] + off(v.pitch, 0, lo - s.gj0);
@@ -956,7 +1011,7 @@ static int upload_rows(csph* H, Strip& s, int j_begin, int j_end, const double* 
   CK(cudaMemsetAsync(s.dflags, 0, sizeof(int), s.st));
   {
     dim3 blk(32, 8), grd((nx + 31) / 32, (hi - lo + 7) / 8);
-    validate_kernel<<<grd, blk, 0, s.st>>>(v, lo - s.gj0, hi - s.gj0, psid, psi0, s.dflags);
+    validate_kernel<<<grd, blk, 0, s.st>>>(v, lo - s.gj0, hi - s.gj0, psid, psi0, s.dflags, ub);
     CK(cudaGetLastError());
   }
   int flags = 0;
@@ -965,15 +1020,30 @@ static int upload_rows(csph* H, Strip& s, int j_begin, int j_end, const double* 
   if (flags & 1) return fail(CSPH_EINVAL, "non-finite input value");
   if (flags & 2) return fail(CSPH_EINVAL, "negative depth in input");
   if (flags & 4) return fail(CSPH_EINVAL, "psi outside [0,1)");
+  const size_t ntot = (size_t)(v.ny + 2 * GY) * v.pitch;
+  if (v.prec == 4) {
+    for (int k = 0; k < 4; ++k)
+      to_f32_kernel<<<(unsigned)((ntot + 255) / 256), 256, 0, s.st>>>((float*)src_dst0(v, k),
+                                                                      dst[k], ntot);
+    CK(cudaGetLastError());
+  }
   if (!psi || !(flags & 8)) {
     // uniform porosity: W is a scalar (64 B/cell instead of 72 B/cell)
     v.W = nullptr;
     v.Wc = 1.0 / (1.0 - psi0);
   } else {
-    size_t n = (size_t)(v.ny + 2 * GY) * v.pitch;
-    w_from_psi_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s.st>>>(s.Wbuf, s.Wbuf, n);
+    w_from_psi_kernel<<<(unsigned)((ntot + 255) / 256), 256, 0, s.st>>>(s.Wbuf, s.Wbuf, ntot);
     CK(cudaGetLastError());
     v.W = s.Wbuf;
+    if (v.prec == 4) {
+      if (!s.Wbuf32) {
+        int st = dalloc(s, (void**)&s.Wbuf32, ntot * 4);
+        if (st) return st;
+      }
+      to_f32_kernel<<<(unsigned)((ntot + 255) / 256), 256, 0, s.st>>>(s.Wbuf32, s.Wbuf, ntot);
+      CK(cudaGetLastError());
+      v.W = (const double*)s.Wbuf32;  // holds fp32 values
+    }
   }
   return CSPH_OK;
 }
@@ -1000,7 +1070,10 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
   for (auto& s : H->s) {
     CK(cudaSetDevice(s.dev));
     dim3 blk(32, 8), grd((s.v.nx + 31) / 32, (s.v.ny + 7) / 8);
-    maxima_kernel<<<grd, blk, 0, s.st>>>(s.v, s.ctrl, H->P, s.gM);
+    if (s.v.prec == 4)
+      maxima32_kernel<<<grd, blk, 0, s.st>>>(s.v, s.ctrl, H->P, s.gM);
+    else
+      maxima_kernel<<<grd, blk, 0, s.st>>>(s.v, s.ctrl, H->P, s.gM);
     CK(cudaGetLastError());
   }
   if (H->mode == DIST) {
@@ -1036,6 +1109,8 @@ int csph_set_fields_rows(csph_t* H, int j_begin, int j_end, const double* n_mann
                          const double* beta, const double* src) {
   if (!H) return fail(CSPH_EINVAL, "handle is NULL");
   if (j_begin < 0 || j_end > H->ny || j_end <= j_begin) return fail(CSPH_EINVAL, "bad row range");
+  if (H->p.precision == 32)
+    return fail(CSPH_EINVAL, "csph_set_fields: the fp32 mode runs the hot-path features only");
   const bool has_n = n_manning != nullptr, has_src = beta != nullptr || src != nullptr;
   const int nx = H->nx;
   for (auto& s : H->s) {
@@ -1241,10 +1316,22 @@ int csph_get_state_rows(csph_t* H, int j_begin, int j_end, double* h, double* hu
     const int p = c.parity;
     double* dst[4] = {h, hu, hv, b};
     const double* src[4] = {v.H[p], v.Qx[p], v.Qy[p], v.b[p]};
+    const size_t ntot = (size_t)(v.ny + 2 * GY) * v.pitch;
+    if (v.prec == 4 && !s.tmpd) {
+      int st = dalloc(s, (void**)&s.tmpd, ntot * 8);
+      if (st) return st;
+    }
     for (int k = 0; k < 4; ++k) {
       if (!dst[k]) continue;
+      const double* sk = src[k];
+      if (v.prec == 4) {  // widen the fp32 field first
+        to_f64_kernel<<<(unsigned)((ntot + 255) / 256), 256, 0, s.st>>>(s.tmpd, (const float*)sk,
+                                                                         ntot);
+        CK(cudaGetLastError());
+        sk = s.tmpd;
+      }
       CK(cudaMemcpy2DAsync(dst[k] + (size_t)(lo - j_begin) * H->nx, (size_t)H->nx * 8,
-                           src[k] + off(v.pitch, 0, lo - s.gj0), (size_t)v.pitch * 8,
+                           sk + off(v.pitch, 0, lo - s.gj0), (size_t)v.pitch * 8,
                            (size_t)H->nx * 8, hi - lo, cudaMemcpyDeviceToHost, s.st));
     }
     CK(cudaStreamSynchronize(s.st));

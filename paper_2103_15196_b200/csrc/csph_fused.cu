@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "csph_launch.h"
+#include "csph_real.cuh"
 
 namespace ck {
 
@@ -60,17 +61,18 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-template <int NT, bool HASW, int D>
+template <typename T, int NT, bool HASW, int D>
 struct Smem {
   static constexpr int NF = HASW ? 5 : 4;
-  static constexpr int RW = NT + 4;  // ring row: data at [2, 2+NT), 16 B aligned
-  static constexpr int XW = NT + 2;  // exchange row: element t at [t+1]
-  alignas(128) double ring[D][NF][RW];
-  double U[2][XW];      // u of the last two rows (div)
-  double PE[XW];        // K2 x-face force (t|t+1), row L
-  double X2[5][XW];     // row L-1: H_half, u~, v~, J0x, |J0|
-  double X3[5][XW];     // row L-1: K5 x-face force, sigma_x (eta, H, u~, v~)
-  double X4[4][XW];     // row L-1: x-face fluxes (t|t+1): F^H, F^Qx, F^Qy, F^J
+  static constexpr int OFR = 16 / (int)sizeof(T);  // ring data offset: 16 B aligned
+  static constexpr int RW = NT + 2 * OFR;          // ring row: data at [OFR, OFR+NT)
+  static constexpr int XW = NT + 2;                // exchange row: element t at [t+1]
+  alignas(128) T ring[D][NF][RW];
+  T U[2][XW];      // u of the last two rows (div)
+  T PE[XW];        // K2 x-face force (t|t+1), row L
+  T X2[5][XW];     // row L-1: H_half, u~, v~, J0x, |J0|
+  T X3[5][XW];     // row L-1: K5 x-face force, sigma_x (eta, H, u~, v~)
+  T X4[4][XW];     // row L-1: x-face fluxes (t|t+1): F^H, F^Qx, F^Qy, F^J
   alignas(8) unsigned long long bar[D];
   unsigned long long red[3][NT / 32];
 };
@@ -80,31 +82,31 @@ enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
 // K7 hydrostatic step + HLL without branches: every case of
 // hll_face() is evaluated with the same operations and the result selected, so
 // the value is bitwise identical.  Callers have already excluded both-dry cells.
-__device__ __forceinline__ void hll_bf(double g, double eta_m, double H_m, double un_m,
-                                       double ut_m, double eta_p, double H_p, double un_p,
-                                       double ut_p, double& F0, double& F1, double& F2) {
-  const double bs = smax(eta_m - H_m, eta_p - H_p);
-  const double Hm = smax(0.0, eta_m - bs);
-  const double Hp = smax(0.0, eta_p - bs);
-  const bool dm = !(Hm > 0.0), dp = !(Hp > 0.0);
-  const double mm = Hm * un_m, mp = Hp * un_p;
-  const double cm = sqrt0nb(g * Hm), cp = sqrt0nb(g * Hp);
-  double SL, SR;
-  if (!dm && !dp) { SL = smin(un_m - cm, un_p - cp); SR = smax(un_m + cm, un_p + cp); }
-  else if (dp) { SL = un_m - cm; SR = fma(2.0, cm, un_m); }
-  else { SL = fma(-2.0, cp, un_p); SR = un_p + cp; }
+template <typename T>
+__device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T eta_p, T H_p,
+                                       T un_p, T ut_p, T& F0, T& F1, T& F2) {
+  const T bs = smax_t(eta_m - H_m, eta_p - H_p);
+  const T Hm = smax_t(T(0), eta_m - bs);
+  const T Hp = smax_t(T(0), eta_p - bs);
+  const bool dm = !(Hm > T(0)), dp = !(Hp > T(0));
+  const T mm = Hm * un_m, mp = Hp * un_p;
+  const T cm = sqrt0_t(g * Hm), cp = sqrt0_t(g * Hp);
+  T SL, SR;
+  if (!dm && !dp) { SL = smin_t(un_m - cm, un_p - cp); SR = smax_t(un_m + cm, un_p + cp); }
+  else if (dp) { SL = un_m - cm; SR = fma(T(2), cm, un_m); }
+  else { SL = fma(T(-2), cp, un_p); SR = un_p + cp; }
   const bool none = dm && dp;
-  const double den = none ? 1.0 : (SR - SL);
-  const double inv = rcp_nb(den);
-  const double SLSR = SL * SR;
-  const double fl1 = mm * un_m, fl2 = mm * ut_m, fr1 = mp * un_p, fr2 = mp * ut_p;
-  const double h0 = ((SR * mm - SL * mp) + SLSR * (Hp - Hm)) * inv;
-  const double h1 = ((SR * fl1 - SL * fr1) + SLSR * (mp - mm)) * inv;
-  const double h2 = ((SR * fl2 - SL * fr2) + SLSR * (Hp * ut_p - Hm * ut_m)) * inv;
-  const bool up = SL >= 0.0, dn = SR <= 0.0;
-  F0 = none ? 0.0 : (up ? mm : (dn ? mp : h0));
-  F1 = none ? 0.0 : (up ? fl1 : (dn ? fr1 : h1));
-  F2 = none ? 0.0 : (up ? fl2 : (dn ? fr2 : h2));
+  const T den = none ? T(1) : (SR - SL);
+  const T inv = rcp_t(den);
+  const T SLSR = SL * SR;
+  const T fl1 = mm * un_m, fl2 = mm * ut_m, fr1 = mp * un_p, fr2 = mp * ut_p;
+  const T h0 = ((SR * mm - SL * mp) + SLSR * (Hp - Hm)) * inv;
+  const T h1 = ((SR * fl1 - SL * fr1) + SLSR * (mp - mm)) * inv;
+  const T h2 = ((SR * fl2 - SL * fr2) + SLSR * (Hp * ut_p - Hm * ut_m)) * inv;
+  const bool up = SL >= T(0), dn = SR <= T(0);
+  F0 = none ? T(0) : (up ? mm : (dn ? mp : h0));
+  F1 = none ? T(0) : (up ? fl1 : (dn ? fr1 : h1));
+  F2 = none ? T(0) : (up ? fl2 : (dn ? fr2 : h2));
 }
 
 // minmod without branches, bitwise equal to R's select form: when a and b are
@@ -116,28 +118,39 @@ __device__ __forceinline__ double minmod_bf(double a, double b) {
   return same ? m : 0.0;
 }
 
-template <int NT, bool HASW, int D, int PF, int MINB, bool GEN>
+template <typename T, int NT, bool HASW, int D, int PF, int MINB, bool GEN>
 __global__ void __launch_bounds__(NT, MINB)
     fused_step_kernel(StripView S, Ctrl* __restrict__ C, Phys P,
                       unsigned long long* __restrict__ gM, int row0, int row1, int TY, Hgs hg) {
   static_assert(D >= PF + 5, "ring too shallow");
   constexpr int TX = NT - 8;
-  using SM = Smem<NT, HASW, D>;
+  using SM = Smem<T, NT, HASW, D>;
+  static_assert(!GEN || sizeof(T) == 8, "NEXT-3/4 features are fp64 only");
   extern __shared__ __align__(128) unsigned char smraw[];
   SM& sm = *reinterpret_cast<SM*>(smraw);
 
   const int status = C->status;
   if (status) return;
   const int par = C->parity;
-  const double tau = C->tau;
-  const double theta = 0.5 * tau;
-  const double lam = tau / P.h;
-  const double* __restrict__ gin[5] = {par ? S.H[1] : S.H[0], par ? S.Qx[1] : S.Qx[0],
-                                       par ? S.Qy[1] : S.Qy[0], par ? S.b[1] : S.b[0], S.W};
-  double* __restrict__ oH = par ? S.H[0] : S.H[1];
-  double* __restrict__ oQx = par ? S.Qx[0] : S.Qx[1];
-  double* __restrict__ oQy = par ? S.Qy[0] : S.Qy[1];
-  double* __restrict__ ob = par ? S.b[0] : S.b[1];
+  const PT<T> Q = make_pt<T>(P);
+  const double taud = C->tau;
+  const T tau = T(taud);
+  const T theta = T(0.5) * tau;
+  const T lam = T(taud / P.h);  // lambda in fp64 (identical for T = double)
+  // state buffers hold T values (fp32 mode reuses the fp64 allocations)
+  auto tp = [](double* x) { return reinterpret_cast<T*>(x); };
+  // A_J of a cell: constant, or Eq.4 per cell (NEXT-4, fp64 GEN instance only)
+  auto aj_at = [&](size_t c, T Hc) -> T {
+    if constexpr (GEN) return cell_aj(P, S, c, Hc);
+    else return Q.A_J;
+  };
+  const T* __restrict__ gin[5] = {tp(par ? S.H[1] : S.H[0]), tp(par ? S.Qx[1] : S.Qx[0]),
+                                       tp(par ? S.Qy[1] : S.Qy[0]), tp(par ? S.b[1] : S.b[0]),
+                                  reinterpret_cast<const T*>(S.W)};
+  T* __restrict__ oH = tp(par ? S.H[0] : S.H[1]);
+  T* __restrict__ oQx = tp(par ? S.Qx[0] : S.Qx[1]);
+  T* __restrict__ oQy = tp(par ? S.Qy[0] : S.Qy[1]);
+  T* __restrict__ ob = tp(par ? S.b[0] : S.b[1]);
 
   const int t = threadIdx.x;
   const int nx = S.nx, ny = S.ny, pitch = S.pitch;
@@ -159,7 +172,7 @@ __global__ void __launch_bounds__(NT, MINB)
       }
     if (dry) {
       const unsigned char stt = hg.tstate[ti];
-      if (stt < 2 || P.src != 0.0 || S.beta) {
+      if (stt < 2 || Q.src != T(0) || S.beta) {
         // identity update: H' = H, Q' = +0, b' with R's K8 formula at zero fluxes (with
         // NEXT-3 sources H' = (H + tau s)/(1 + tau beta): a dry cell may become wet)
         const bool outc = (t >= 4) && (t < 4 + TX) && (col < nx);
@@ -167,16 +180,18 @@ __global__ void __launch_bounds__(NT, MINB)
         if (outc) {
           for (int j = y0; j < y1; ++j) {
             const size_t o = off(pitch, col, j);
-            const double H3 = gin[0][o], b3 = gin[3][o];
-            const double W3 = HASW ? S.W[o] : S.Wc;
-            const double z = 0.0 + (0.0 - 0.0);
-            double Hn = H3 - lam * z;
-            double Qn = 0.0 - lam * z, Qm = Qn;
-            const double bn = (b3 - (lam * W3) * z) + (tau * W3) * P.src;
-            if (GEN) apply_sources(S, tau, o, Hn, Qn, Qm);
-            if (Hn > P.eps) cwet = true;  // momenta stay +0 (they were +0 * a)
-            if (GEN) write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
-            else write_with_wall_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
+            const T H3 = gin[0][o], b3 = gin[3][o];
+            const T W3 = HASW ? gin[4][o] : T(S.Wc);
+            const T z = T(0) + (T(0) - T(0));
+            T Hn = H3 - lam * z;
+            T Qn = T(0) - lam * z, Qm = Qn;
+            const T bn = (b3 - (lam * W3) * z) + (tau * W3) * Q.src;
+            if constexpr (GEN) apply_sources(S, tau, o, Hn, Qn, Qm);
+            if (Hn > Q.eps) cwet = true;  // momenta stay +0 (they were +0 * a)
+            if constexpr (GEN)
+              write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
+            else
+              write_wall_ghosts_t(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
           }
         }
         const bool any = __syncthreads_or(cwet);
@@ -190,12 +205,12 @@ __global__ void __launch_bounds__(NT, MINB)
         if (cwet) {
           for (int j = y0; j < y1; ++j) {
             const size_t o = off(pitch, col, j);
-            const double Hn = oH[o];
-            if (Hn > P.eps) {
-              double t1, t2, t3;
-              dt_terms<GEN>(P, Hn, 0.0, 0.0, HASW ? S.W[o] : S.Wc,
-                            GEN ? cell_aj(P, S, o, Hn) : P.A_J, t1, t2, t3);
-              unsigned long long a2 = dbits(t1), b2 = dbits(t2), c2 = dbits(t3);
+            const T Hn = oH[o];
+            if (Hn > Q.eps) {
+              T t1, t2, t3;
+              dt_terms_t<GEN>(Q, Hn, T(0), T(0), HASW ? gin[4][o] : T(S.Wc),
+                            aj_at(o, Hn), t1, t2, t3);
+              unsigned long long a2 = dbits_t(t1), b2 = dbits_t(t2), c2 = dbits_t(t3);
               atomicMax(&gM[0], a2); atomicMax(&gM[1], b2); atomicMax(&gM[2], c2);
             }
           }
@@ -213,15 +228,15 @@ __global__ void __launch_bounds__(NT, MINB)
   const int niter = (y1 + 2) - rfirst + 1;  // input rows y0-3 .. y1+2
   // columns copied per row: [x0-4, min(x0-4+NT, nx+4)), even count
   int ncopy = min(NT, nx + 8 - x0);
-  ncopy = (ncopy + 1) & ~1;
-  const unsigned row_bytes = (unsigned)ncopy * 8u;
+  ncopy = (ncopy + SM::OFR - 1) & ~(SM::OFR - 1);  // 16 B multiple
+  const unsigned row_bytes = (unsigned)ncopy * (unsigned)sizeof(T);
   const unsigned tx_bytes = row_bytes * SM::NF;
 
   // zero the exchange and ring memory once (edge threads read never-written slots)
   {
-    double* z = reinterpret_cast<double*>(smraw);
-    const int nd = (int)(offsetof(SM, bar) / sizeof(double));
-    for (int k = t; k < nd; k += NT) z[k] = 0.0;
+    T* z = reinterpret_cast<T*>(smraw);
+    const int nd = (int)(offsetof(SM, bar) / sizeof(T));
+    for (int k = t; k < nd; k += NT) z[k] = T(0);
   }
   if (t == 0) {
     for (int s = 0; s < D; ++s) mbar_init(&sm.bar[s], 1);
@@ -233,7 +248,8 @@ __global__ void __launch_bounds__(NT, MINB)
     const size_t go = off(pitch, x0 - 4, rfirst + k);
     mbar_expect_tx(&sm.bar[s], tx_bytes);
 #pragma unroll
-    for (int f = 0; f < SM::NF; ++f) tma_row(&sm.ring[s][f][2], gin[f] + go, row_bytes, &sm.bar[s]);
+    for (int f = 0; f < SM::NF; ++f)
+      tma_row(&sm.ring[s][f][SM::OFR], gin[f] + go, row_bytes, &sm.bar[s]);
   };
   if (t == 0) {
     fence_proxy_async();
@@ -241,26 +257,26 @@ __global__ void __launch_bounds__(NT, MINB)
   }
 
   // ring access: value of field f at iteration-row k, thread column t + dt
-#define RG(f, k, dt) sm.ring[(k) % D][f][(t) + 2 + (dt)]
+#define RG(f, k, dt) sm.ring[(k) % D][f][(t) + SM::OFR + (dt)]
 #define XG(a, dt) a[(t) + 1 + (dt)]
 
   // ---- carried registers (row offsets relative to the newest row L) ----
   // Depth-1 carries are overwritten in place right after their last use, so the
   // register allocator needs no moves for them.
-  double v1 = 0, v2 = 0;          // v(L-1), v(L-2)
-  double r1 = 0;                  // r(L-1)
-  double gam1 = 0, gam2 = 0;      // gamma(L-1), gamma(L-2)
-  double PS = 0;                  // K2 y-face force (L-2|L-1)
-  double phix1 = 0;               // Phi_x(L-1)
-  double Hh2 = 0;                 // H_half(L-2)
-  double PhS = 0;                 // K5 y-face force (L-3|L-2)
-  double phx2h = 0;               // Phi_half_x(L-2)
-  double QLx3 = 0, QLy3 = 0;      // Q^L(L-3)
-  double ut2 = 0, vt2 = 0, ut3 = 0, vt3 = 0;  // u~, v~ of rows L-2, L-3
-  double J0y2 = 0, J0a2 = 0, J0y3 = 0, J0a3 = 0;
-  double sy3[4] = {0, 0, 0, 0};   // sigma_y of row L-3 (eta, H, v~, u~)
-  double dF3[4] = {0, 0, 0, 0};   // Delta F_x of row L-3
-  double Gs[4] = {0, 0, 0, 0};    // y-face flux (L-4|L-3)
+  T v1 = 0, v2 = 0;          // v(L-1), v(L-2)
+  T r1 = 0;                  // r(L-1)
+  T gam1 = 0, gam2 = 0;      // gamma(L-1), gamma(L-2)
+  T PS = 0;                  // K2 y-face force (L-2|L-1)
+  T phix1 = 0;               // Phi_x(L-1)
+  T Hh2 = 0;                 // H_half(L-2)
+  T PhS = 0;                 // K5 y-face force (L-3|L-2)
+  T phx2h = 0;               // Phi_half_x(L-2)
+  T QLx3 = 0, QLy3 = 0;      // Q^L(L-3)
+  T ut2 = 0, vt2 = 0, ut3 = 0, vt3 = 0;  // u~, v~ of rows L-2, L-3
+  T J0y2 = 0, J0a2 = 0, J0y3 = 0, J0a3 = 0;
+  T sy3[4] = {0, 0, 0, 0};   // sigma_y of row L-3 (eta, H, v~, u~)
+  T dF3[4] = {0, 0, 0, 0};   // Delta F_x of row L-3
+  T Gs[4] = {0, 0, 0, 0};    // y-face flux (L-4|L-3)
   unsigned long long m0 = 0, m1 = 0, m2 = 0;
   bool neg = false;
   unsigned hist = 0;  // wet flags of rows L..L-4 of this column (bit 0 = row L)
@@ -271,18 +287,20 @@ __global__ void __launch_bounds__(NT, MINB)
   // K8 epilogue for one cell: dry-momentum zeroing, negative-depth flag, stores,
   // wall ghosts and the next step's Eq.7 terms.
   bool anywet = false;
-  auto store_update = [&](double Hn, double Qxn, double Qyn, double bn, double W3, int j) {
-    const bool wet = Hn > P.eps;
+  auto store_update = [&](T Hn, T Qxn, T Qyn, T bn, T W3, int j) {
+    const bool wet = Hn > Q.eps;
     anywet |= wet;
-    if (!wet) { Qxn = 0.0; Qyn = 0.0; }
-    if (Hn < -P.neg_tol) neg = true;
-    if (GEN) write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
-    else write_with_wall_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
+    if (!wet) { Qxn = T(0); Qyn = T(0); }
+    if (Hn < -Q.neg_tol) neg = true;
+    if constexpr (GEN)
+      write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
+    else
+      write_wall_ghosts_t(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
     if (wet) {
-      double t1, t2, t3;
-      dt_terms<GEN>(P, Hn, Qxn, Qyn, W3, GEN ? cell_aj(P, S, off(pitch, col, j), Hn) : P.A_J,
+      T t1, t2, t3;
+      dt_terms_t<GEN>(Q, Hn, Qxn, Qyn, W3, aj_at(off(pitch, col, j), Hn),
                     t1, t2, t3);
-      unsigned long long a = dbits(t1), b = dbits(t2), c = dbits(t3);
+      unsigned long long a = dbits_t(t1), b = dbits_t(t2), c = dbits_t(t3);
       m0 = a > m0 ? a : m0; m1 = b > m1 ? b : m1; m2 = c > m2 ? c : m2;
     }
   };
@@ -290,7 +308,7 @@ __global__ void __launch_bounds__(NT, MINB)
   // The dry decision for iteration k is made at the last barrier of iteration k-1
   // (a __syncthreads_and over "rows L-4..L of my column are dry").
   mbar_wait(&sm.bar[0], 0u);
-  hist = RG(F_H, 0, 0) > P.eps ? 1u : 0u;
+  hist = RG(F_H, 0, 0) > Q.eps ? 1u : 0u;
   bool cta_dry = __syncthreads_and(hist == 0u);
 
   for (int k = 0; k < niter; ++k) {
@@ -305,98 +323,101 @@ __global__ void __launch_bounds__(NT, MINB)
     auto next_hist = [&]() {
       if (k + 1 < niter) {
         mbar_wait(&sm.bar[(k + 1) % D], (unsigned)(((k + 1) / D) & 1));
-        hist = ((hist << 1) | (RG(F_H, k + 1, 0) > P.eps ? 1u : 0u)) & 31u;
+        hist = ((hist << 1) | (RG(F_H, k + 1, 0) > Q.eps ? 1u : 0u)) & 31u;
       }
     };
     const int j = L - 3;  // row updated in this iteration
-    double Gn[4] = {0.0, 0.0, 0.0, 0.0};  // (G^H, G^Qx, G^Qy, G^J) at (L-3|L-2)
+    T Gn[4] = {T(0), T(0), T(0), T(0)};  // (G^H, G^Qx, G^Qy, G^J) at (L-3|L-2)
     if (cta_dry) {
       // Dry fast path (exact): every quantity of R on rows L-4..L is either 0 or the
       // identity, so only the carried window and the row L-3 update run.
-      const double H1 = RG(F_H, km1, 0);
-      phix1 = 0.0;
-      v2 = v1; v1 = 0.0;
-      r1 = 0.0;
-      gam2 = gam1; gam1 = 0.0;
+      const T H1 = RG(F_H, km1, 0);
+      phix1 = T(0);
+      v2 = v1; v1 = T(0);
+      r1 = T(0);
+      gam2 = gam1; gam1 = T(0);
       Hh2 = H1;
-      phx2h = 0.0;
-      ut3 = ut2; vt3 = vt2; ut2 = 0.0; vt2 = 0.0;
-      J0y3 = J0y2; J0a3 = J0a2; J0y2 = 0.0; J0a2 = 0.0;
+      phx2h = T(0);
+      ut3 = ut2; vt3 = vt2; ut2 = T(0); vt2 = T(0);
+      J0y3 = J0y2; J0a3 = J0a2; J0y2 = T(0); J0a2 = T(0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = 0.0;
+      for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = T(0);
       if (col_out && j >= y0 && j < y1) {
-        const double H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
-        const double W3 = HASW ? RG(F_W, km3, 0) : S.Wc;
-        const double dH = dF3[0] + (Gn[0] - Gs[0]);
-        const double dQx = dF3[1] + (Gn[1] - Gs[1]);
-        const double dQy = dF3[2] + (Gn[2] - Gs[2]);
-        const double dJ = dF3[3] + (Gn[3] - Gs[3]);
-        double Hn = H3 - lam * dH;
-        double Qxn = QLx3 - lam * dQx;
-        double Qyn = QLy3 - lam * dQy;
-        const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
-        if (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
+        const T H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
+        const T W3 = HASW ? RG(F_W, km3, 0) : T(S.Wc);
+        const T dH = dF3[0] + (Gn[0] - Gs[0]);
+        const T dQx = dF3[1] + (Gn[1] - Gs[1]);
+        const T dQy = dF3[2] + (Gn[2] - Gs[2]);
+        const T dJ = dF3[3] + (Gn[3] - Gs[3]);
+        T Hn = H3 - lam * dH;
+        T Qxn = QLx3 - lam * dQx;
+        T Qyn = QLy3 - lam * dQy;
+        const T bn = (b3 - (lam * W3) * dJ) + (tau * W3) * Q.src;
+        if constexpr (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
         store_update(Hn, Qxn, Qyn, bn, W3, j);
       }
-      QLx3 = 0.0; QLy3 = 0.0;
+      QLx3 = T(0); QLy3 = T(0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) { dF3[q] = 0.0; Gs[q] = 0.0; sy3[q] = 0.0; }
+      for (int q = 0; q < 4; ++q) { dF3[q] = T(0); Gs[q] = T(0); sy3[q] = T(0); }
       next_hist();
       cta_dry = __syncthreads_and(hist == 0u);
       continue;
     }
     // ================= phase A: K1 + K2 x-face + K2 y-face (row L) =================
-    const double H0 = RG(F_H, k, 0), b0 = RG(F_B, k, 0);
-    const bool w0 = H0 > P.eps;
-    const double eta0 = H0 + b0;
-    double r0 = 0.0, u0 = 0.0, v0 = 0.0, gam0 = 0.0;
+    const T H0 = RG(F_H, k, 0), b0 = RG(F_B, k, 0);
+    const bool w0 = H0 > Q.eps;
+    const T eta0 = H0 + b0;
+    T r0 = T(0), u0 = T(0), v0 = T(0), gam0 = T(0);
     if (__any_sync(0xffffffffu, w0)) {  // warp-uniform; dry lanes compute on H = 1
-      const double Hs = w0 ? H0 : 1.0;
-      const double rr = rcp_nb(Hs);
-      const double uu = RG(F_QX, k, 0) * rr, vv = RG(F_QY, k, 0) * rr;
-      double gg = 0.0;
+      const T Hs = w0 ? H0 : T(1);
+      const T rr = rcp_t(Hs);
+      const T uu = RG(F_QX, k, 0) * rr, vv = RG(F_QY, k, 0) * rr;
+      T gg = T(0);
       if (P.fric) {
-        const double cgc = (GEN && S.cg) ? S.cg[off(pitch, col, L)] : P.cgam;  // NEXT-3 field
-        gg = (cgc * sqrt0nb(uu * uu + vv * vv)) * (rr * icbrt(Hs));
+        T cgc = Q.cgam;
+        if constexpr (GEN) {
+          if (S.cg) cgc = S.cg[off(pitch, col, L)];  // NEXT-3 field
+        }
+        gg = (cgc * sqrt0_t(uu * uu + vv * vv)) * (rr * icbrt_t(Hs));
       }
-      r0 = w0 ? rr : 0.0; u0 = w0 ? uu : 0.0; v0 = w0 ? vv : 0.0; gam0 = w0 ? gg : 0.0;
+      r0 = w0 ? rr : T(0); u0 = w0 ? uu : T(0); v0 = w0 ? vv : T(0); gam0 = w0 ? gg : T(0);
     }
-    double PE0;
+    T PE0;
     {
-      const double bR = RG(F_B, k, 1);
-      PE0 = face_force_h(P.cPh, eta0, b0, RG(F_H, k, 1) + bR, bR);
+      const T bR = RG(F_B, k, 1);
+      PE0 = face_force_t(Q.cPh, eta0, b0, RG(F_H, k, 1) + bR, bR);
     }
-    const double H1 = RG(F_H, km1, 0), b1 = RG(F_B, km1, 0);
-    const bool w1 = H1 > P.eps;
-    const double eta1 = H1 + b1;
-    const double PN1 = face_force_h(P.cPh, eta1, b1, eta0, b0);  // face (L-1|L)
-    const double phiy1 = w1 ? -(PN1 + PS) : 0.0;
+    const T H1 = RG(F_H, km1, 0), b1 = RG(F_B, km1, 0);
+    const bool w1 = H1 > Q.eps;
+    const T eta1 = H1 + b1;
+    const T PN1 = face_force_t(Q.cPh, eta1, b1, eta0, b0);  // face (L-1|L)
+    const T phiy1 = w1 ? -(PN1 + PS) : T(0);
     PS = PN1;
     XG(sm.U[k & 1], 0) = u0;
     XG(sm.PE, 0) = PE0;
     __syncthreads();  // ---------------------------------------------------- barrier 1
     {
       // ================= phase B: K4 predictor + J0 (row L-1) =================
-      const double phix0 = w0 ? -(PE0 + XG(sm.PE, -1)) : 0.0;
-      double Hh1 = H1, ut1 = 0.0, vt1 = 0.0;
+      const T phix0 = w0 ? -(PE0 + XG(sm.PE, -1)) : T(0);
+      T Hh1 = H1, ut1 = T(0), vt1 = T(0);
       if (__any_sync(0xffffffffu, w1)) {
-        const double* Up = sm.U[(k - 1) & 1];
-        double div = ((XG(Up, 1) - XG(Up, -1)) + (v0 - v2)) * P.inv_2h;
-        const double hh = H1 * (1.0 - theta * div);
-        const double f = P.fric ? rcp_nb(1.0 + theta * gam1) : 1.0;  // gam1 = 0 when dry
-        const double uu = ((RG(F_QX, km1, 0) + theta * phix1) * f) * r1;
-        const double vv = ((RG(F_QY, km1, 0) + theta * phiy1) * f) * r1;
-        Hh1 = w1 ? hh : H1; ut1 = w1 ? uu : 0.0; vt1 = w1 ? vv : 0.0;
+        const T* Up = sm.U[(k - 1) & 1];
+        T div = ((XG(Up, 1) - XG(Up, -1)) + (v0 - v2)) * Q.inv_2h;
+        const T hh = H1 * (T(1) - theta * div);
+        const T f = P.fric ? rcp_t(T(1) + theta * gam1) : T(1);  // gam1 = 0 when dry
+        const T uu = ((RG(F_QX, km1, 0) + theta * phix1) * f) * r1;
+        const T vv = ((RG(F_QY, km1, 0) + theta * phiy1) * f) * r1;
+        Hh1 = w1 ? hh : H1; ut1 = w1 ? uu : T(0); vt1 = w1 ? vv : T(0);
       }
       phix1 = phix0;
       v2 = v1; v1 = v0;
       r1 = r0;
-      double J0x1 = 0.0, J0y1 = 0.0, J0a1 = 0.0;
+      T J0x1 = T(0), J0y1 = T(0), J0a1 = T(0);
       if (P.transport)
-        grass_gated<GEN>(P, ut1, vt1, H1, GEN ? cell_aj(P, S, off(pitch, col, L - 1), H1) : P.A_J,
+        grass_t<GEN>(Q, ut1, vt1, H1, aj_at(off(pitch, col, L - 1), H1),
                          J0x1, J0y1, J0a1);
       // Delta F_x of row L-2 from the own face (t|t+1) and the west face (t-1|t)
-      double dF2[4];
+      T dF2[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) dF2[q] = XG(sm.X4[q], 0) - XG(sm.X4[q], -1);
       XG(sm.X2[0], 0) = Hh1;
@@ -406,54 +427,54 @@ __global__ void __launch_bounds__(NT, MINB)
       XG(sm.X2[4], 0) = J0a1;
       __syncthreads();  // -------------------------------------------------- barrier 2
       // ============ phase C: K5, sigma_x (row L-1), K6 (row L-2), y-face (L-3|L-2) ====
-      double PhE1;
+      T PhE1;
       {
-        const double bR = RG(F_B, km1, 1);
-        PhE1 = face_force_h(P.cPh, Hh1 + b1, b1, XG(sm.X2[0], 1) + bR, bR);
+        const T bR = RG(F_B, km1, 1);
+        PhE1 = face_force_t(Q.cPh, Hh1 + b1, b1, XG(sm.X2[0], 1) + bR, bR);
       }
-      double sx1[4];
+      T sx1[4];
       {
-        const double HLm = RG(F_H, km1, -1), HRp = RG(F_H, km1, 1);
-        const double eL = HLm + RG(F_B, km1, -1), eR = HRp + RG(F_B, km1, 1);
-        sx1[0] = minmod(eta1 - eL, eR - eta1);
-        sx1[1] = minmod(H1 - HLm, HRp - H1);
-        sx1[2] = minmod(ut1 - XG(sm.X2[1], -1), XG(sm.X2[1], 1) - ut1);
-        sx1[3] = minmod(vt1 - XG(sm.X2[2], -1), XG(sm.X2[2], 1) - vt1);
+        const T HLm = RG(F_H, km1, -1), HRp = RG(F_H, km1, 1);
+        const T eL = HLm + RG(F_B, km1, -1), eR = HRp + RG(F_B, km1, 1);
+        sx1[0] = minmod_t(eta1 - eL, eR - eta1);
+        sx1[1] = minmod_t(H1 - HLm, HRp - H1);
+        sx1[2] = minmod_t(ut1 - XG(sm.X2[1], -1), XG(sm.X2[1], 1) - ut1);
+        sx1[3] = minmod_t(vt1 - XG(sm.X2[2], -1), XG(sm.X2[2], 1) - vt1);
       }
-      const double H2 = RG(F_H, km2, 0), b2 = RG(F_B, km2, 0);
-      const bool w2 = H2 > P.eps;
-      const double PhN2 = face_force_h(P.cPh, Hh2 + b2, b2, Hh1 + b1, b1);  // face (L-2|L-1)
-      double QLx2 = 0.0, QLy2 = 0.0;
+      const T H2 = RG(F_H, km2, 0), b2 = RG(F_B, km2, 0);
+      const bool w2 = H2 > Q.eps;
+      const T PhN2 = face_force_t(Q.cPh, Hh2 + b2, b2, Hh1 + b1, b1);  // face (L-2|L-1)
+      T QLx2 = T(0), QLy2 = T(0);
       if (__any_sync(0xffffffffu, w2)) {
-        const double phy2h = -(PhN2 + PhS);
-        const double f1 = P.fric ? rcp_nb(1.0 + tau * gam2) : 1.0;
-        const double qx = (RG(F_QX, km2, 0) + tau * phx2h) * f1;
-        const double qy = (RG(F_QY, km2, 0) + tau * phy2h) * f1;
-        QLx2 = w2 ? qx : 0.0; QLy2 = w2 ? qy : 0.0;
+        const T phy2h = -(PhN2 + PhS);
+        const T f1 = P.fric ? rcp_t(T(1) + tau * gam2) : T(1);
+        const T qx = (RG(F_QX, km2, 0) + tau * phx2h) * f1;
+        const T qy = (RG(F_QY, km2, 0) + tau * phy2h) * f1;
+        QLx2 = w2 ? qx : T(0); QLy2 = w2 ? qy : T(0);
       }
       PhS = PhN2;
       Hh2 = Hh1;
       gam2 = gam1; gam1 = gam0;
       // y-face (L-3|L-2): sigma_y of row L-2 (always: it is carried), HLL, sediment
-      const double H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
-      const bool w3 = H3 > P.eps;
-      const double eta2 = H2 + b2, eta3 = H3 + b3;
-      double sy2[4];
-      sy2[0] = minmod(eta2 - eta3, eta1 - eta2);
-      sy2[1] = minmod(H2 - H3, H1 - H2);
-      sy2[2] = minmod(vt2 - vt3, vt1 - vt2);
-      sy2[3] = minmod(ut2 - ut3, ut1 - ut2);
+      const T H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
+      const bool w3 = H3 > Q.eps;
+      const T eta2 = H2 + b2, eta3 = H3 + b3;
+      T sy2[4];
+      sy2[0] = minmod_t(eta2 - eta3, eta1 - eta2);
+      sy2[1] = minmod_t(H2 - H3, H1 - H2);
+      sy2[2] = minmod_t(vt2 - vt3, vt1 - vt2);
+      sy2[3] = minmod_t(ut2 - ut3, ut1 - ut2);
       if (__any_sync(0xffffffffu, w3 || w2)) {
-        double F0, F1, F2;
-        hll_bf(P.g, fma(0.5, sy3[0], eta3), fma(0.5, sy3[1], H3), fma(0.5, sy3[2], vt3),
-                 fma(0.5, sy3[3], ut3), fma(-0.5, sy2[0], eta2), fma(-0.5, sy2[1], H2),
-                 fma(-0.5, sy2[2], vt2), fma(-0.5, sy2[3], ut2), F0, F1, F2);
+        T F0, F1, F2;
+        hll_bf(Q.g, fma(T(0.5), sy3[0], eta3), fma(T(0.5), sy3[1], H3), fma(T(0.5), sy3[2], vt3),
+                 fma(T(0.5), sy3[3], ut3), fma(T(-0.5), sy2[0], eta2), fma(T(-0.5), sy2[1], H2),
+                 fma(T(-0.5), sy2[2], vt2), fma(T(-0.5), sy2[3], ut2), F0, F1, F2);
         const bool any = w3 || w2;
-        Gn[0] = any ? F0 : 0.0;
-        Gn[2] = any ? F1 : 0.0;  // normal momentum of a y-face -> Qy
-        Gn[1] = any ? F2 : 0.0;  // tangential -> Qx
-        Gn[3] = (any && P.transport) ? sed_face(P, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2)
-                                     : 0.0;
+        Gn[0] = any ? F0 : T(0);
+        Gn[2] = any ? F1 : T(0);  // normal momentum of a y-face -> Qy
+        Gn[1] = any ? F2 : T(0);  // tangential -> Qx
+        Gn[3] = (any && P.transport) ? sed_face_t(Q, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2)
+                                     : T(0);
       }
       ut3 = ut2; vt3 = vt2; ut2 = ut1; vt2 = vt1;
       J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = J0a1;
@@ -465,41 +486,41 @@ __global__ void __launch_bounds__(NT, MINB)
       next_hist();
       const bool dry_next = __syncthreads_and(hist == 0u);  // ---------------- barrier 3
       // ====== phase D: Phi_half_x (row L-1), x-face flux (row L-1) ======
-      phx2h = w1 ? -(PhE1 + XG(sm.X3[0], -1)) : 0.0;
-      double Fn[4] = {0.0, 0.0, 0.0, 0.0};
+      phx2h = w1 ? -(PhE1 + XG(sm.X3[0], -1)) : T(0);
+      T Fn[4] = {T(0), T(0), T(0), T(0)};
       {
-        const double HR = RG(F_H, km1, 1);
-        const bool any = w1 || HR > P.eps;
+        const T HR = RG(F_H, km1, 1);
+        const bool any = w1 || HR > Q.eps;
         if (__any_sync(0xffffffffu, any)) {
-          const double bR = RG(F_B, km1, 1);
-          const double eR = HR + bR;
-          const double uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
-          double F0, F1, F2;
-          hll_bf(P.g, fma(0.5, sx1[0], eta1), fma(0.5, sx1[1], H1), fma(0.5, sx1[2], ut1),
-                   fma(0.5, sx1[3], vt1), fma(-0.5, XG(sm.X3[1], 1), eR), fma(-0.5, XG(sm.X3[2], 1), HR),
-                   fma(-0.5, XG(sm.X3[3], 1), uR), fma(-0.5, XG(sm.X3[4], 1), vR), F0, F1, F2);
-          Fn[0] = any ? F0 : 0.0;
-          Fn[1] = any ? F1 : 0.0;  // normal momentum of an x-face -> Qx
-          Fn[2] = any ? F2 : 0.0;  // tangential -> Qy
-          Fn[3] = (any && P.transport) ? sed_face(P, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
+          const T bR = RG(F_B, km1, 1);
+          const T eR = HR + bR;
+          const T uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
+          T F0, F1, F2;
+          hll_bf(Q.g, fma(T(0.5), sx1[0], eta1), fma(T(0.5), sx1[1], H1), fma(T(0.5), sx1[2], ut1),
+                   fma(T(0.5), sx1[3], vt1), fma(T(-0.5), XG(sm.X3[1], 1), eR), fma(T(-0.5), XG(sm.X3[2], 1), HR),
+                   fma(T(-0.5), XG(sm.X3[3], 1), uR), fma(T(-0.5), XG(sm.X3[4], 1), vR), F0, F1, F2);
+          Fn[0] = any ? F0 : T(0);
+          Fn[1] = any ? F1 : T(0);  // normal momentum of an x-face -> Qx
+          Fn[2] = any ? F2 : T(0);  // tangential -> Qy
+          Fn[3] = (any && P.transport) ? sed_face_t(Q, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
                                                   XG(sm.X2[4], 1), b1, bR)
-                                       : 0.0;
+                                       : T(0);
         }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = Fn[q];
       // ---- K8 update of row L-3 ----
       if (col_out && j >= y0 && j < y1) {
-        const double W3 = HASW ? RG(F_W, km3, 0) : S.Wc;
-        const double dH = dF3[0] + (Gn[0] - Gs[0]);
-        const double dQx = dF3[1] + (Gn[1] - Gs[1]);
-        const double dQy = dF3[2] + (Gn[2] - Gs[2]);
-        const double dJ = dF3[3] + (Gn[3] - Gs[3]);
-        double Hn = H3 - lam * dH;
-        double Qxn = QLx3 - lam * dQx;
-        double Qyn = QLy3 - lam * dQy;
-        const double bn = (b3 - (lam * W3) * dJ) + (tau * W3) * P.src;
-        if (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
+        const T W3 = HASW ? RG(F_W, km3, 0) : T(S.Wc);
+        const T dH = dF3[0] + (Gn[0] - Gs[0]);
+        const T dQx = dF3[1] + (Gn[1] - Gs[1]);
+        const T dQy = dF3[2] + (Gn[2] - Gs[2]);
+        const T dJ = dF3[3] + (Gn[3] - Gs[3]);
+        T Hn = H3 - lam * dH;
+        T Qxn = QLx3 - lam * dQx;
+        T Qyn = QLy3 - lam * dQy;
+        const T bn = (b3 - (lam * W3) * dJ) + (tau * W3) * Q.src;
+        if constexpr (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
         store_update(Hn, Qxn, Qyn, bn, W3, j);
       }
       QLx3 = QLx2; QLy3 = QLy2;
@@ -536,21 +557,21 @@ __global__ void __launch_bounds__(NT, MINB)
   }
 }
 
-template <int NT, bool HASW, int D, int PF, int MINB, bool GEN>
+template <typename T, int NT, bool HASW, int D, int PF, int MINB, bool GEN>
 void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM, int row0,
               int row1, int TY, const Hgs& hg, cudaStream_t st) {
-  using SM = Smem<NT, HASW, D>;
+  using SM = Smem<T, NT, HASW, D>;
   constexpr int TX = NT - 8;
   static bool configured = false;
   const size_t smem = sizeof(SM);
   if (!configured) {
-    cudaFuncSetAttribute(fused_step_kernel<NT, HASW, D, PF, MINB, GEN>,
+    cudaFuncSetAttribute(fused_step_kernel<T, NT, HASW, D, PF, MINB, GEN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   dim3 grid((unsigned)((S.nx + TX - 1) / TX), (unsigned)((row1 - row0 + TY - 1) / TY));
-  fused_step_kernel<NT, HASW, D, PF, MINB, GEN><<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY,
-                                                                  hg);
+  fused_step_kernel<T, NT, HASW, D, PF, MINB, GEN>
+      <<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY, hg);
 }
 
 template <int NT, int D, int PF, int MINB>
@@ -558,15 +579,20 @@ void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
               int row1, int TY, const Hgs& hg, cudaStream_t st) {
   Hgs h = hg;
   if (NT - 8 != FUSED_TX) h.enable = 0;  // tiling of the flags is FUSED_TX wide
+  if (S.prec == 4) {  // NEXT-2 fp32 mode: hot-path features only (checked at create)
+    if (S.W) launch_t<float, NT, true, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
+    else launch_t<float, NT, false, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
+    return;
+  }
   // GEN: NEXT-3/4 features present; otherwise the hot-path specialisation
   const bool gen = P.m_grass != 2 || P.aj_mode || S.cg || S.beta || S.aj0 || S.bc_xlo != 1 ||
                    S.bc_xhi != 1 || S.wall_lo == 2 || S.wall_hi == 2;
   if (S.W) {
-    if (gen) launch_t<NT, true, D, PF, MINB, true>(S, C, P, gM, row0, row1, TY, h, st);
-    else launch_t<NT, true, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
+    if (gen) launch_t<double, NT, true, D, PF, MINB, true>(S, C, P, gM, row0, row1, TY, h, st);
+    else launch_t<double, NT, true, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
   } else {
-    if (gen) launch_t<NT, false, D, PF, MINB, true>(S, C, P, gM, row0, row1, TY, h, st);
-    else launch_t<NT, false, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
+    if (gen) launch_t<double, NT, false, D, PF, MINB, true>(S, C, P, gM, row0, row1, TY, h, st);
+    else launch_t<double, NT, false, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
   }
 }
 

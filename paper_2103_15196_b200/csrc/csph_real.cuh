@@ -1,0 +1,138 @@
+// csph_real.cuh -- the fused kernel's arithmetic helpers, generic in the real type T.
+// T = double: the same operations, in the same order, as csph_internal.cuh (reading R,
+// bitwise parity with the oracle).  T = float: the NEXT-2 fp32 mode,
+// which uses the hardware's correctly rounded fp32 reciprocal and square root.
+#pragma once
+
+#include "csph_internal.cuh"
+
+namespace ck {
+
+// Scalar constants of R converted once to T at kernel start.
+template <typename T>
+struct PT {
+  T g, eps, neg_tol, A_J, C_J, C_Sh, kappa, cPh, cgam, inv_h, inv_2h, src;
+  int m_grass, fric, transport;
+};
+
+template <typename T>
+__device__ __forceinline__ PT<T> make_pt(const Phys& P) {
+  PT<T> q;
+  q.g = T(P.g); q.eps = T(P.eps); q.neg_tol = T(P.neg_tol); q.A_J = T(P.A_J);
+  q.C_J = T(P.C_J); q.C_Sh = T(P.C_Sh); q.kappa = T(P.kappa); q.cPh = T(P.cPh);
+  q.cgam = T(P.cgam); q.inv_h = T(P.inv_h); q.inv_2h = T(P.inv_2h); q.src = T(P.src);
+  q.m_grass = P.m_grass; q.fric = P.fric; q.transport = P.transport;
+  return q;
+}
+
+template <typename T> __device__ __forceinline__ T smin_t(T a, T b) { return (a < b) ? a : b; }
+template <typename T> __device__ __forceinline__ T smax_t(T a, T b) { return (a > b) ? a : b; }
+
+template <typename T>
+__device__ __forceinline__ T minmod_t(T a, T b) {
+  if (a > T(0) && b > T(0)) return smin_t(a, b);
+  if (a < T(0) && b < T(0)) return smax_t(a, b);
+  return T(0);
+}
+
+__device__ __forceinline__ double rcp_t(double x) { return rcp_nb(x); }
+__device__ __forceinline__ float rcp_t(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double sqrt0_t(double x) { return sqrt0nb(x); }
+__device__ __forceinline__ float sqrt0_t(float x) { return x > 0.0f ? __fsqrt_rn(x) : x; }
+__device__ __forceinline__ double icbrt_t(double x) { return icbrt(x); }
+// fp32 x^(-1/3): bit-trick seed and 3 Newton steps (fp32 mode only)
+__device__ __forceinline__ float icbrt_t(float x) {
+  float y = __int_as_float(0x54A2FA8C - __float_as_int(x) / 3);
+  const float third = 1.0f / 3.0f;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) y = y + y * ((1.0f - x * ((y * y) * y)) * third);
+  return y;
+}
+__device__ __forceinline__ unsigned long long dbits_t(double x) { return dbits(x); }
+__device__ __forceinline__ unsigned long long dbits_t(float x) { return dbits((double)x); }
+
+// K2/K5 face force (hydrostatic form), c_P/2 folded in (see face_force_h)
+template <typename T>
+__device__ __forceinline__ T face_force_t(T cPh, T etaL, T bL, T etaR, T bR) {
+  T bs = smax_t(bL, bR);
+  T hL = smax_t(T(0), etaL - bs);
+  T hR = smax_t(T(0), etaR - bs);
+  return (cPh * (hL + hR)) * (hR - hL);
+}
+
+template <bool GEN, typename T>
+__device__ __forceinline__ T pow_m_t(int m, T s2, T a) {
+  if (!GEN || m == 2) return s2;
+  T pw = T(1);
+  for (int k = 0; k < m / 2; ++k) pw = pw * s2;
+  if (m & 1) pw = pw * a;
+  return pw;
+}
+
+template <bool GEN, typename T>
+__device__ __forceinline__ void grass_t(const PT<T>& P, T ut, T vt, T H, T A, T& jx, T& jy,
+                                        T& ja) {
+  T s2 = ut * ut + vt * vt;
+  T sa = sqrt0_t(s2);
+  T a = A * pow_m_t<GEN>(P.m_grass, s2, sa);
+  bool gate = (P.C_Sh == T(0)) || ((s2 * s2) * s2 > P.kappa * H);
+  if (gate) {
+    jx = a * ut; jy = a * vt; ja = a * sa;
+  } else {
+    jx = T(0); jy = T(0); ja = T(0);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T sed_face_t(const PT<T>& P, T unL, T unR, T JnL, T JnR, T JaL, T JaR,
+                                        T bL, T bR) {
+  T us = unL + unR;
+  T Jn, Ja;
+  if (us > T(0)) { Jn = JnL; Ja = JaL; }
+  else if (us < T(0)) { Jn = JnR; Ja = JaR; }
+  else { Jn = T(0.5) * (JnL + JnR); Ja = T(0.5) * (JaL + JaR); }
+  return Jn - (P.C_J * Ja) * ((bR - bL) * P.inv_h);
+}
+
+template <bool GEN, typename T>
+__device__ __forceinline__ void dt_terms_t(const PT<T>& P, T H, T Qx, T Qy, T W, T A, T& t1,
+                                           T& t2, T& t3) {
+  T r = rcp_t(H);
+  T u = Qx * r, v = Qy * r;
+  T s2 = u * u + v * v;
+  T a = sqrt0_t(s2);
+  t1 = s2;
+  t2 = a + sqrt0_t(P.g * H);
+  bool gate = (P.C_Sh == T(0)) || ((s2 * s2) * s2 > P.kappa * H);
+  t3 = gate ? ((A * pow_m_t<GEN>(P.m_grass, s2, a)) * a) * W : T(0);
+}
+
+// Wall-only ghost writer (the hot-path specialisation), generic in T.
+template <typename T>
+__device__ __forceinline__ void write_wall_ghosts_t(const StripView& S, T* oH, T* oQx, T* oQy,
+                                                    T* ob, int col, int j, T Hn, T Qxn, T Qyn,
+                                                    T bn, bool gx) {
+  const size_t o = off(S.pitch, col, j);
+  oH[o] = Hn; oQx[o] = Qxn; oQy[o] = Qyn; ob[o] = bn;
+  const bool gyl = S.wall_lo && j < 3, gyh = S.wall_hi && j >= S.ny - 3;
+  if (!(gx || gyl || gyh)) return;
+  const int gcs[2] = {col < 3 ? -1 - col : INT_MIN, col >= S.nx - 3 ? 2 * S.nx - 1 - col : INT_MIN};
+  const int grs[2] = {gyl ? -1 - j : INT_MIN, gyh ? 2 * S.ny - 1 - j : INT_MIN};
+  for (int a = 0; a < 2; ++a) {
+    if (gcs[a] == INT_MIN) continue;
+    const size_t g = off(S.pitch, gcs[a], j);
+    oH[g] = Hn; oQx[g] = -Qxn; oQy[g] = Qyn; ob[g] = bn;
+  }
+  for (int c = 0; c < 2; ++c) {
+    if (grs[c] == INT_MIN) continue;
+    size_t g = off(S.pitch, col, grs[c]);
+    oH[g] = Hn; oQx[g] = Qxn; oQy[g] = -Qyn; ob[g] = bn;
+    for (int a = 0; a < 2; ++a) {
+      if (gcs[a] == INT_MIN) continue;
+      g = off(S.pitch, gcs[a], grs[c]);
+      oH[g] = Hn; oQx[g] = -Qxn; oQy[g] = -Qyn; ob[g] = bn;
+    }
+  }
+}
+
+}  // namespace ck
