@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcsph.so")
 SOURCES = ["csph_api.cu", "csph_staged.cu", "csph_fused.cu"]
-HEADERS = ["csph_internal.cuh", "csph_launch.h", "../../include/csph.h"]
+HEADERS = ["csph_internal.cuh", "csph_real.cuh", "csph_launch.h", "../../include/csph.h"]
 
 
 def _nccl_include() -> str:

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libcsph.so")
+SO_PATH = os.environ.get("CSPH_LIB_DEV") or os.path.join(_HERE, "libcsph.so")  # dev A/B knob
 
 CSPH_OK, CSPH_EINVAL, CSPH_ENOSTATE, CSPH_ENOMEM, CSPH_ECUDA, CSPH_ENCCL = 0, -1, -2, -3, -4, -5
 CSPH_ENEGDEPTH, CSPH_ENONFINITE, CSPH_EDRY = -6, -7, -8

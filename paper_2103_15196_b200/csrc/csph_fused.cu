@@ -17,9 +17,25 @@
 #include "csph_launch.h"
 #include "csph_real.cuh"
 
+#ifndef CSPH_UNROLL
+#define CSPH_UNROLL 1
+#endif
+
 namespace ck {
 
 namespace {
+
+constexpr int kUnroll = CSPH_UNROLL;  // y-march unroll (register renaming of the carries)
+
+#ifndef CSPH_GUARD
+#define CSPH_GUARD 0
+#endif
+// warp-uniform guard: skip a stage when no lane of the warp needs it
+#define ANYW(x) (CSPH_GUARD ? __any_sync(0xffffffffu, (x)) : true)
+// friction / transport switches: runtime in the general (and fp32) instances, compile-time
+// on in the fp64 hot-path specialisation (launch_v sends other cases to the general one)
+#define FRIC (RTF ? P.fric != 0 : true)
+#define TRANSP (RTF ? P.transport != 0 : true)
 
 // Ring of D slots with rows prefetched PF ahead; rows L-4..L are live, so D >= PF + 5.
 
@@ -91,10 +107,11 @@ __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T et
   const bool dm = !(Hm > T(0)), dp = !(Hp > T(0));
   const T mm = Hm * un_m, mp = Hp * un_p;
   const T cm = sqrt0_t(g * Hm), cp = sqrt0_t(g * Hp);
-  T SL, SR;
-  if (!dm && !dp) { SL = smin_t(un_m - cm, un_p - cp); SR = smax_t(un_m + cm, un_p + cp); }
-  else if (dp) { SL = un_m - cm; SR = fma(T(2), cm, un_m); }
-  else { SL = fma(T(-2), cp, un_p); SR = un_p + cp; }
+  // the three wave-speed cases of R, all evaluated, then selected
+  const T aL = un_m - cm, aR = un_p - cp, bL2 = un_m + cm, bR2 = un_p + cp;
+  const bool both = !dm & !dp;
+  const T SL = both ? smin_t(aL, aR) : (dp ? aL : fma(T(-2), cp, un_p));
+  const T SR = both ? smax_t(bL2, bR2) : (dp ? fma(T(2), cm, un_m) : bR2);
   const bool none = dm && dp;
   const T den = none ? T(1) : (SR - SL);
   const T inv = rcp_t(den);
@@ -109,15 +126,6 @@ __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T et
   F2 = none ? T(0) : (up ? fl2 : (dn ? fr2 : h2));
 }
 
-// minmod without branches, bitwise equal to R's select form: when a and b are
-// both > 0 (or both < 0) the result is the one of smaller magnitude, exactly
-// copysign(min(|a|,|b|), a); otherwise +0.
-__device__ __forceinline__ double minmod_bf(double a, double b) {
-  const bool same = (a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0);
-  const double m = copysign(fmin(fabs(a), fabs(b)), a);
-  return same ? m : 0.0;
-}
-
 template <typename T, int NT, bool HASW, int D, int PF, int MINB, bool GEN>
 __global__ void __launch_bounds__(NT, MINB)
     fused_step_kernel(StripView S, Ctrl* __restrict__ C, Phys P,
@@ -126,6 +134,7 @@ __global__ void __launch_bounds__(NT, MINB)
   constexpr int TX = NT - 8;
   using SM = Smem<T, NT, HASW, D>;
   static_assert(!GEN || sizeof(T) == 8, "NEXT-3/4 features are fp64 only");
+  constexpr bool RTF = GEN || sizeof(T) == 4;
   extern __shared__ __align__(128) unsigned char smraw[];
   SM& sm = *reinterpret_cast<SM*>(smraw);
 
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(NT, MINB)
   T* __restrict__ ob = tp(par ? S.b[0] : S.b[1]);
 
   const int t = threadIdx.x;
-  const int nx = S.nx, ny = S.ny, pitch = S.pitch;
+  const int nx = S.nx, pitch = S.pitch;
   const int x0 = blockIdx.x * TX;
   const int col = x0 - 4 + t;
   const int y0 = row0 + blockIdx.y * TY;
@@ -277,6 +286,9 @@ __global__ void __launch_bounds__(NT, MINB)
   T sy3[4] = {0, 0, 0, 0};   // sigma_y of row L-3 (eta, H, v~, u~)
   T dF3[4] = {0, 0, 0, 0};   // Delta F_x of row L-3
   T Gs[4] = {0, 0, 0, 0};    // y-face flux (L-4|L-3)
+  // phase-A results of the newest row, produced at the end of the previous iteration
+  T aPE0 = 0, av0 = 0, ar0 = 0, agam0 = 0, aphiy1 = 0;
+  bool aw0 = false;
   unsigned long long m0 = 0, m1 = 0, m2 = 0;
   bool neg = false;
   unsigned hist = 0;  // wet flags of rows L..L-4 of this column (bit 0 = row L)
@@ -305,11 +317,52 @@ __global__ void __launch_bounds__(NT, MINB)
     }
   };
 
+  // ================= phase A: K1 + K2 x-face + K2 y-face (row L = rfirst + k) =================
+  // Run at the end of the previous iteration, in the same barrier interval as its phase D,
+  // so that the long dependency chains of both (K1's 1/H, |v|, H^(-1/3); the x-face HLL)
+  // are scheduled together.  Row k's ring slot has been waited for by next_hist().
+  auto phaseA = [&](int k) {
+    const int L = rfirst + k;
+    const int km1 = k - 1 + D;
+    const T H0 = RG(F_H, k, 0), b0 = RG(F_B, k, 0);
+    const bool w0 = H0 > Q.eps;
+    const T eta0 = H0 + b0;
+    T r0 = T(0), u0 = T(0), v0 = T(0), gam0 = T(0);
+    if (ANYW(w0)) {  // warp-uniform; dry lanes compute on H = 1
+      const T Hs = w0 ? H0 : T(1);
+      const T rr = rcp_t(Hs);
+      const T uu = RG(F_QX, k, 0) * rr, vv = RG(F_QY, k, 0) * rr;
+      T gg = T(0);
+      if (FRIC) {
+        T cgc = Q.cgam;
+        if constexpr (GEN) {
+          if (S.cg) cgc = S.cg[off(pitch, col, L)];  // NEXT-3 field
+        }
+        gg = (cgc * sqrt0_t(uu * uu + vv * vv)) * (rr * icbrt_t(Hs));
+      }
+      r0 = w0 ? rr : T(0); u0 = w0 ? uu : T(0); v0 = w0 ? vv : T(0); gam0 = w0 ? gg : T(0);
+    }
+    T PE0;
+    {
+      const T bR = RG(F_B, k, 1);
+      PE0 = face_force_t(Q.cPh, eta0, b0, RG(F_H, k, 1) + bR, bR);
+    }
+    const T H1 = RG(F_H, km1, 0), b1 = RG(F_B, km1, 0);
+    const bool w1 = H1 > Q.eps;
+    const T PN1 = face_force_t(Q.cPh, H1 + b1, b1, eta0, b0);  // face (L-1|L)
+    aphiy1 = w1 ? -(PN1 + PS) : T(0);
+    PS = PN1;
+    XG(sm.U[k & 1], 0) = u0;
+    XG(sm.PE, 0) = PE0;
+    aw0 = w0; aPE0 = PE0; av0 = v0; ar0 = r0; agam0 = gam0;
+  };
+
   // The dry decision for iteration k is made at the last barrier of iteration k-1
   // (a __syncthreads_and over "rows L-4..L of my column are dry").
   mbar_wait(&sm.bar[0], 0u);
   hist = RG(F_H, 0, 0) > Q.eps ? 1u : 0u;
   bool cta_dry = __syncthreads_and(hist == 0u);
+  if (!cta_dry) phaseA(0);
 
   for (int k = 0; k < niter; ++k) {
     const int L = rfirst + k;  // newest row (strip-local index)
@@ -361,50 +414,24 @@ __global__ void __launch_bounds__(NT, MINB)
       for (int q = 0; q < 4; ++q) { dF3[q] = T(0); Gs[q] = T(0); sy3[q] = T(0); }
       next_hist();
       cta_dry = __syncthreads_and(hist == 0u);
+      if (!cta_dry && k + 1 < niter) phaseA(k + 1);
       continue;
-    }
-    // ================= phase A: K1 + K2 x-face + K2 y-face (row L) =================
-    const T H0 = RG(F_H, k, 0), b0 = RG(F_B, k, 0);
-    const bool w0 = H0 > Q.eps;
-    const T eta0 = H0 + b0;
-    T r0 = T(0), u0 = T(0), v0 = T(0), gam0 = T(0);
-    if (__any_sync(0xffffffffu, w0)) {  // warp-uniform; dry lanes compute on H = 1
-      const T Hs = w0 ? H0 : T(1);
-      const T rr = rcp_t(Hs);
-      const T uu = RG(F_QX, k, 0) * rr, vv = RG(F_QY, k, 0) * rr;
-      T gg = T(0);
-      if (P.fric) {
-        T cgc = Q.cgam;
-        if constexpr (GEN) {
-          if (S.cg) cgc = S.cg[off(pitch, col, L)];  // NEXT-3 field
-        }
-        gg = (cgc * sqrt0_t(uu * uu + vv * vv)) * (rr * icbrt_t(Hs));
-      }
-      r0 = w0 ? rr : T(0); u0 = w0 ? uu : T(0); v0 = w0 ? vv : T(0); gam0 = w0 ? gg : T(0);
-    }
-    T PE0;
-    {
-      const T bR = RG(F_B, k, 1);
-      PE0 = face_force_t(Q.cPh, eta0, b0, RG(F_H, k, 1) + bR, bR);
     }
     const T H1 = RG(F_H, km1, 0), b1 = RG(F_B, km1, 0);
     const bool w1 = H1 > Q.eps;
     const T eta1 = H1 + b1;
-    const T PN1 = face_force_t(Q.cPh, eta1, b1, eta0, b0);  // face (L-1|L)
-    const T phiy1 = w1 ? -(PN1 + PS) : T(0);
-    PS = PN1;
-    XG(sm.U[k & 1], 0) = u0;
-    XG(sm.PE, 0) = PE0;
+    const bool w0 = aw0;
+    const T PE0 = aPE0, v0 = av0, r0 = ar0, gam0 = agam0, phiy1 = aphiy1;
     __syncthreads();  // ---------------------------------------------------- barrier 1
     {
       // ================= phase B: K4 predictor + J0 (row L-1) =================
       const T phix0 = w0 ? -(PE0 + XG(sm.PE, -1)) : T(0);
       T Hh1 = H1, ut1 = T(0), vt1 = T(0);
-      if (__any_sync(0xffffffffu, w1)) {
+      if (ANYW(w1)) {
         const T* Up = sm.U[(k - 1) & 1];
         T div = ((XG(Up, 1) - XG(Up, -1)) + (v0 - v2)) * Q.inv_2h;
         const T hh = H1 * (T(1) - theta * div);
-        const T f = P.fric ? rcp_t(T(1) + theta * gam1) : T(1);  // gam1 = 0 when dry
+        const T f = FRIC ? rcp_t(T(1) + theta * gam1) : T(1);  // gam1 = 0 when dry
         const T uu = ((RG(F_QX, km1, 0) + theta * phix1) * f) * r1;
         const T vv = ((RG(F_QY, km1, 0) + theta * phiy1) * f) * r1;
         Hh1 = w1 ? hh : H1; ut1 = w1 ? uu : T(0); vt1 = w1 ? vv : T(0);
@@ -413,7 +440,7 @@ __global__ void __launch_bounds__(NT, MINB)
       v2 = v1; v1 = v0;
       r1 = r0;
       T J0x1 = T(0), J0y1 = T(0), J0a1 = T(0);
-      if (P.transport)
+      if (TRANSP)
         grass_t<GEN>(Q, ut1, vt1, H1, aj_at(off(pitch, col, L - 1), H1),
                          J0x1, J0y1, J0a1);
       // Delta F_x of row L-2 from the own face (t|t+1) and the west face (t-1|t)
@@ -445,9 +472,9 @@ __global__ void __launch_bounds__(NT, MINB)
       const bool w2 = H2 > Q.eps;
       const T PhN2 = face_force_t(Q.cPh, Hh2 + b2, b2, Hh1 + b1, b1);  // face (L-2|L-1)
       T QLx2 = T(0), QLy2 = T(0);
-      if (__any_sync(0xffffffffu, w2)) {
+      if (ANYW(w2)) {
         const T phy2h = -(PhN2 + PhS);
-        const T f1 = P.fric ? rcp_t(T(1) + tau * gam2) : T(1);
+        const T f1 = FRIC ? rcp_t(T(1) + tau * gam2) : T(1);
         const T qx = (RG(F_QX, km2, 0) + tau * phx2h) * f1;
         const T qy = (RG(F_QY, km2, 0) + tau * phy2h) * f1;
         QLx2 = w2 ? qx : T(0); QLy2 = w2 ? qy : T(0);
@@ -464,7 +491,7 @@ __global__ void __launch_bounds__(NT, MINB)
       sy2[1] = minmod_t(H2 - H3, H1 - H2);
       sy2[2] = minmod_t(vt2 - vt3, vt1 - vt2);
       sy2[3] = minmod_t(ut2 - ut3, ut1 - ut2);
-      if (__any_sync(0xffffffffu, w3 || w2)) {
+      if (ANYW(w3 || w2)) {
         T F0, F1, F2;
         hll_bf(Q.g, fma(T(0.5), sy3[0], eta3), fma(T(0.5), sy3[1], H3), fma(T(0.5), sy3[2], vt3),
                  fma(T(0.5), sy3[3], ut3), fma(T(-0.5), sy2[0], eta2), fma(T(-0.5), sy2[1], H2),
@@ -473,7 +500,7 @@ __global__ void __launch_bounds__(NT, MINB)
         Gn[0] = any ? F0 : T(0);
         Gn[2] = any ? F1 : T(0);  // normal momentum of a y-face -> Qy
         Gn[1] = any ? F2 : T(0);  // tangential -> Qx
-        Gn[3] = (any && P.transport) ? sed_face_t(Q, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2)
+        Gn[3] = (any && TRANSP) ? sed_face_t(Q, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2)
                                      : T(0);
       }
       ut3 = ut2; vt3 = vt2; ut2 = ut1; vt2 = vt1;
@@ -491,7 +518,7 @@ __global__ void __launch_bounds__(NT, MINB)
       {
         const T HR = RG(F_H, km1, 1);
         const bool any = w1 || HR > Q.eps;
-        if (__any_sync(0xffffffffu, any)) {
+        if (ANYW(any)) {
           const T bR = RG(F_B, km1, 1);
           const T eR = HR + bR;
           const T uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
@@ -502,13 +529,16 @@ __global__ void __launch_bounds__(NT, MINB)
           Fn[0] = any ? F0 : T(0);
           Fn[1] = any ? F1 : T(0);  // normal momentum of an x-face -> Qx
           Fn[2] = any ? F2 : T(0);  // tangential -> Qy
-          Fn[3] = (any && P.transport) ? sed_face_t(Q, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
+          Fn[3] = (any && TRANSP) ? sed_face_t(Q, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
                                                   XG(sm.X2[4], 1), b1, bR)
                                        : T(0);
         }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = Fn[q];
+      // phase A of the next row, unconditionally (a wasted row at a wet -> dry change;
+      // beyond the last row it reads a stale but finite ring slot and feeds nothing)
+      phaseA(k + 1);
       // ---- K8 update of row L-3 ----
       if (col_out && j >= y0 && j < y1) {
         const T W3 = HASW ? RG(F_W, km3, 0) : T(S.Wc);
@@ -563,7 +593,8 @@ void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
   using SM = Smem<T, NT, HASW, D>;
   constexpr int TX = NT - 8;
   static bool configured = false;
-  const size_t smem = sizeof(SM);
+  static const size_t pad = getenv("CSPH_SMEM_PAD") ? (size_t)atol(getenv("CSPH_SMEM_PAD")) : 0;
+  const size_t smem = sizeof(SM) + pad;  // pad: development knob (occupancy experiments)
   if (!configured) {
     cudaFuncSetAttribute(fused_step_kernel<T, NT, HASW, D, PF, MINB, GEN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -584,8 +615,9 @@ void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
     else launch_t<float, NT, false, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
     return;
   }
-  // GEN: NEXT-3/4 features present; otherwise the hot-path specialisation
-  const bool gen = P.m_grass != 2 || P.aj_mode || S.cg || S.beta || S.aj0 || S.bc_xlo != 1 ||
+  // GEN: NEXT-3/4 features present or a physics term switched off; otherwise the
+  // hot-path specialisation
+  const bool gen = !P.fric || !P.transport || P.m_grass != 2 || P.aj_mode || S.cg || S.beta || S.aj0 || S.bc_xlo != 1 ||
                    S.bc_xhi != 1 || S.wall_lo == 2 || S.wall_hi == 2;
   if (S.W) {
     if (gen) launch_t<double, NT, true, D, PF, MINB, true>(S, C, P, gM, row0, row1, TY, h, st);
@@ -614,6 +646,8 @@ void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long
   int TY = tile_rows > 0 ? tile_rows : 128;
   switch (fused_variant()) {
     case 6: launch_v<128, 10, 5, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 8: launch_v<128, 6, 1, 4>(S, C, P, gM, row0, row1, TY, hg, st); break;
+    case 9: launch_v<128, 6, 1, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
     default: launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
   }
   *nlaunch += 1;

@@ -28,11 +28,14 @@ __device__ __forceinline__ PT<T> make_pt(const Phys& P) {
 template <typename T> __device__ __forceinline__ T smin_t(T a, T b) { return (a < b) ? a : b; }
 template <typename T> __device__ __forceinline__ T smax_t(T a, T b) { return (a > b) ? a : b; }
 
+// minmod of R without branches: for a, b both > 0 R's min(a, b) = (a < b ? a : b) and for
+// both < 0 R's max(a, b) = (a > b ? a : b) are the same selection (|a| < |b| ? a : b); all
+// other cases (opposite signs, a zero, a NaN) give +0.  Bitwise identical to R.
 template <typename T>
 __device__ __forceinline__ T minmod_t(T a, T b) {
-  if (a > T(0) && b > T(0)) return smin_t(a, b);
-  if (a < T(0) && b < T(0)) return smax_t(a, b);
-  return T(0);
+  const bool same = ((a > T(0)) & (b > T(0))) | ((a < T(0)) & (b < T(0)));
+  const T pick = (fabs(a) < fabs(b)) ? a : b;
+  return same ? pick : T(0);
 }
 
 __device__ __forceinline__ double rcp_t(double x) { return rcp_nb(x); }
@@ -75,22 +78,17 @@ __device__ __forceinline__ void grass_t(const PT<T>& P, T ut, T vt, T H, T A, T&
   T s2 = ut * ut + vt * vt;
   T sa = sqrt0_t(s2);
   T a = A * pow_m_t<GEN>(P.m_grass, s2, sa);
-  bool gate = (P.C_Sh == T(0)) || ((s2 * s2) * s2 > P.kappa * H);
-  if (gate) {
-    jx = a * ut; jy = a * vt; ja = a * sa;
-  } else {
-    jx = T(0); jy = T(0); ja = T(0);
-  }
+  const bool gate = (P.C_Sh == T(0)) | ((s2 * s2) * s2 > P.kappa * H);
+  jx = gate ? a * ut : T(0); jy = gate ? a * vt : T(0); ja = gate ? a * sa : T(0);
 }
 
 template <typename T>
 __device__ __forceinline__ T sed_face_t(const PT<T>& P, T unL, T unR, T JnL, T JnR, T JaL, T JaR,
                                         T bL, T bR) {
-  T us = unL + unR;
-  T Jn, Ja;
-  if (us > T(0)) { Jn = JnL; Ja = JaL; }
-  else if (us < T(0)) { Jn = JnR; Ja = JaR; }
-  else { Jn = T(0.5) * (JnL + JnR); Ja = T(0.5) * (JaL + JaR); }
+  const T us = unL + unR;
+  const bool up = us > T(0), dn = us < T(0);
+  const T Jn = up ? JnL : (dn ? JnR : T(0.5) * (JnL + JnR));
+  const T Ja = up ? JaL : (dn ? JaR : T(0.5) * (JaL + JaR));
   return Jn - (P.C_J * Ja) * ((bR - bL) * P.inv_h);
 }
 
