@@ -402,6 +402,14 @@ __global__ void selftest_math_kernel(long long n, unsigned long long seed, int l
     if (sqrt_nb(x) != sqrt(x)) nb++;
     double t = x * 0x1p-1000;  // tiny and subnormal arguments of sqrt0nb
     if (sqrt0nb(t) != sqrt(t)) nb++;
+    if (sqrt0nb(x) != sqrt(x)) nb++;
+    if (i == 0) {  // zeros keep their sign; negatives and NaN pass through
+      if (__double_as_longlong(sqrt0nb(0.0)) != 0ll) nb++;
+      if (__double_as_longlong(sqrt0nb(-0.0)) != __double_as_longlong(-0.0)) nb++;
+      if (sqrt0nb(-1.0) != -1.0) nb++;
+      if (sqrt0nb(0x1p-1074) != 0x1p-537) nb++;
+      if (sqrt0nb(0x1p-900) != 0x1p-450 || sqrt0nb(0x1.fffffffffffffp-901) != sqrt(0x1.fffffffffffffp-901)) nb++;
+    }
   }
   if (nb) atomicAdd(bad, nb);
 }
@@ -537,7 +545,7 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
     const size_t nt = (size_t)s.ntx * s.nty;
     if ((st = dalloc(s, (void**)&s.tflag, 2 * nt))) return st;
     if ((st = dalloc(s, (void**)&s.tstate, nt))) return st;
-    CK(cudaMemset(s.tflag, 1, 2 * nt));
+    CK(cudaMemset(s.tflag, HGS_ALL, 2 * nt));
     CK(cudaMemset(s.tstate, 0, nt));
     if ((st = dalloc(s, (void**)&s.hstats, 4 * sizeof(unsigned long long)))) return st;
     CK(cudaMemset(s.hstats, 0, 4 * sizeof(unsigned long long)));
@@ -1059,7 +1067,7 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
     if ((st = upload_rows(H, s, j_begin, j_end, h, hu, hv, b, psi))) return st;
     init_ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
     CK(cudaMemsetAsync(s.gM, 0, 4 * sizeof(unsigned long long), s.st));
-    CK(cudaMemsetAsync(s.tflag, 1, 2 * (size_t)s.ntx * s.nty, s.st));  // all tiles active
+    CK(cudaMemsetAsync(s.tflag, HGS_ALL, 2 * (size_t)s.ntx * s.nty, s.st));  // all tiles active
     CK(cudaMemsetAsync(s.tstate, 0, (size_t)s.ntx * s.nty, s.st));
     CK(cudaMemsetAsync(s.hstats, 0, 4 * sizeof(unsigned long long), s.st));
     // walls: ghosts of buffer 0 (W is read only on owned cells: no ghosts needed)

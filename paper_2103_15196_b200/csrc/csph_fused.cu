@@ -91,6 +91,7 @@ struct Smem {
   T X4[4][XW];     // row L-1: x-face fluxes (t|t+1): F^H, F^Qx, F^Qy, F^J
   alignas(8) unsigned long long bar[D];
   unsigned long long red[3][NT / 32];
+  unsigned wm[NT / 32];
 };
 
 enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
@@ -168,17 +169,23 @@ __global__ void __launch_bounds__(NT, MINB)
   const int y0 = row0 + blockIdx.y * TY;
   const int y1 = min(y0 + TY, row1);
   if (y0 >= y1) return;
-  // ---- HGS: a tile whose 3x3 tile neighbourhood had
-  // no wet cell after the previous step updates to the identity ----
+  // ---- HGS.  Under R a dry cell whose 4
+  // edge neighbours are dry updates to the identity: its 4 faces are both-dry (no flux, no
+  // sediment flux), Q^L = 0, so H' = H - lam*0, Q' = +0, b' = b - (lam W)*0 + (tau W)*src.
+  // A tile is therefore an identity when no cell of it and no cell of the facing 1-cell
+  // bands of its 4 edge neighbours was wet after the previous step (band-mask flags). ----
   const int tr = y0 / TY;
   const int ti = tr * hg.ntx + (int)blockIdx.x;
-  if (hg.enable && (S.wall_lo || tr > 0) && (S.wall_hi || tr < hg.nty - 1)) {
-    bool dry = true;
-    for (int a = -1; a <= 1; ++a)
-      for (int c2 = -1; c2 <= 1; ++c2) {
-        const int r = tr + a, q = (int)blockIdx.x + c2;
-        if (r >= 0 && r < hg.nty && q >= 0 && q < hg.ntx) dry = dry && hg.fprev[r * hg.ntx + q] == 0;
-      }
+  // a tile whose boundary row faces an interior strip edge reads halo rows of another strip,
+  // whose wetness the flags do not record: it always marches
+  if (hg.enable && (S.wall_lo || y0 > 0) && (S.wall_hi || y1 < S.ny)) {
+    auto fl = [&](int r, int q) -> unsigned {
+      return (r >= 0 && r < hg.nty && q >= 0 && q < hg.ntx) ? hg.fprev[r * hg.ntx + q] : 0u;
+    };
+    const int q0 = (int)blockIdx.x;
+    const bool dry = !(fl(tr, q0) & HGS_ANY) && !(fl(tr - 1, q0) & HGS_BOT) &&
+                     !(fl(tr + 1, q0) & HGS_TOP) && !(fl(tr, q0 - 1) & HGS_RIGHT) &&
+                     !(fl(tr, q0 + 1) & HGS_LEFT);
     if (dry) {
       const unsigned char stt = hg.tstate[ti];
       if (stt < 2 || Q.src != T(0) || S.beta) {
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(NT, MINB)
         const bool any = __syncthreads_or(cwet);
         if (t == 0) {
           hg.tstate[ti] = any ? 0 : (unsigned char)(stt + 1);
-          hg.fnext[ti] = any ? 1 : 0;
+          hg.fnext[ti] = any ? HGS_ALL : 0;  // conservative: every band
           atomicAdd(&hg.stats[1], 1ull);
         }
         // a cell made wet by a source has Q' = +0: its Eq.7 terms are those of a
@@ -298,10 +305,12 @@ __global__ void __launch_bounds__(NT, MINB)
 
   // K8 epilogue for one cell: dry-momentum zeroing, negative-depth flag, stores,
   // wall ghosts and the next step's Eq.7 terms.
-  bool anywet = false;
+  // HGS band mask of this thread's output cells (wet anywhere / in the first or last row
+  // of the tile); the first / last column add HGS_LEFT / HGS_RIGHT at the end
+  unsigned wmask = 0;
   auto store_update = [&](T Hn, T Qxn, T Qyn, T bn, T W3, int j) {
     const bool wet = Hn > Q.eps;
-    anywet |= wet;
+    wmask |= wet ? (HGS_ANY | (j == y0 ? HGS_TOP : 0u) | (j == y1 - 1 ? HGS_BOT : 0u)) : 0u;
     if (!wet) { Qxn = T(0); Qyn = T(0); }
     if (Hn < -Q.neg_tol) neg = true;
     if constexpr (GEN)
@@ -364,6 +373,7 @@ __global__ void __launch_bounds__(NT, MINB)
   bool cta_dry = __syncthreads_and(hist == 0u);
   if (!cta_dry) phaseA(0);
 
+#pragma unroll kUnroll
   for (int k = 0; k < niter; ++k) {
     const int L = rfirst + k;  // newest row (strip-local index)
     const int km1 = k - 1 + D, km2 = k - 2 + D, km3 = k - 3 + D;  // non-negative ring rows
@@ -573,9 +583,18 @@ __global__ void __launch_bounds__(NT, MINB)
   if ((t & 31) == 0) {
     sm.red[0][t >> 5] = m0; sm.red[1][t >> 5] = m1; sm.red[2][t >> 5] = m2;
   }
-  const bool tile_wet = __syncthreads_or(anywet);
+  {
+    const int xe = min(x0 + TX, nx);  // the tile's last column + 1
+    if (wmask & HGS_ANY) wmask |= (col == x0 ? HGS_LEFT : 0u) | (col == xe - 1 ? HGS_RIGHT : 0u);
+  }
+  wmask = __reduce_or_sync(0xffffffffu, wmask);
+  if ((t & 31) == 0) sm.wm[t >> 5] = wmask;
+  __syncthreads();
   if (t == 0 && hg.enable) {
-    hg.fnext[ti] = tile_wet ? 1 : 0;
+    unsigned m = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) m |= sm.wm[w];
+    hg.fnext[ti] = (unsigned char)m;
     hg.tstate[ti] = 0;
   }
   if (t == 0 && hg.stats) atomicAdd(&hg.stats[0], 1ull);
@@ -618,7 +637,8 @@ void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
   // GEN: NEXT-3/4 features present or a physics term switched off; otherwise the
   // hot-path specialisation
   const bool gen = !P.fric || !P.transport || P.m_grass != 2 || P.aj_mode || S.cg || S.beta || S.aj0 || S.bc_xlo != 1 ||
-                   S.bc_xhi != 1 || S.wall_lo == 2 || S.wall_hi == 2;
+                   S.bc_xhi != 1 || S.wall_lo == 2 || S.wall_hi == 2 ||
+                   !(P.g * P.eps >= 0x1p-890);  // dt_terms: sqrt(g H) without the zero guard
   if (S.W) {
     if (gen) launch_t<double, NT, true, D, PF, MINB, true>(S, C, P, gM, row0, row1, TY, h, st);
     else launch_t<double, NT, true, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);

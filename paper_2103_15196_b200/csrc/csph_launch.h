@@ -17,9 +17,13 @@ void launch_staged_step(const StripView& S, Ctrl* C, const Scratch& T, const Phy
                         unsigned long long* gM, cudaStream_t st, long long* nlaunch);
 
 // HGS tile flags of the fused path: a tile is the TX x TY chunk
-// one CTA marches.  fprev/fnext: "some output cell of the tile was wet" for the
-// previous / this step; tstate: consecutive identity copies of the tile (2 = both
+// one CTA marches.  fprev/fnext: band masks (HGS_*) of the tile's wet output cells for
+// the previous / this step; tstate: consecutive identity copies of the tile (2 = both
 // ping-pong buffers hold the same values, the tile may be skipped outright).
+// Band bits of a tile flag: some output cell wet anywhere / in the first row / the last
+// row / the first column / the last column of the tile.
+enum : unsigned { HGS_ANY = 1, HGS_TOP = 2, HGS_BOT = 4, HGS_LEFT = 8, HGS_RIGHT = 16, HGS_ALL = 31 };
+
 struct Hgs {
   const unsigned char* fprev;
   unsigned char* fnext;

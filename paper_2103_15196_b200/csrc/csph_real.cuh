@@ -42,6 +42,12 @@ __device__ __forceinline__ double rcp_t(double x) { return rcp_nb(x); }
 __device__ __forceinline__ float rcp_t(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double sqrt0_t(double x) { return sqrt0nb(x); }
 __device__ __forceinline__ float sqrt0_t(float x) { return x > 0.0f ? __fsqrt_rn(x) : x; }
+// sqrt of g*H for a wet depth: in the hot specialisation g*eps_dry >= 2^-890 (launch_v),
+// so the argument is a normal number >= 2^-890 and the plain fast path is exact
+template <bool GEN> __device__ __forceinline__ double sqrt_gh_t(double x) {
+  return GEN ? sqrt0nb(x) : sqrt_nb(x);
+}
+template <bool GEN> __device__ __forceinline__ float sqrt_gh_t(float x) { return sqrt0_t(x); }
 __device__ __forceinline__ double icbrt_t(double x) { return icbrt(x); }
 // fp32 x^(-1/3): bit-trick seed and 3 Newton steps (fp32 mode only)
 __device__ __forceinline__ float icbrt_t(float x) {
@@ -100,7 +106,7 @@ __device__ __forceinline__ void dt_terms_t(const PT<T>& P, T H, T Qx, T Qy, T W,
   T s2 = u * u + v * v;
   T a = sqrt0_t(s2);
   t1 = s2;
-  t2 = a + sqrt0_t(P.g * H);
+  t2 = a + sqrt_gh_t<GEN>(P.g * H);
   bool gate = (P.C_Sh == T(0)) || ((s2 * s2) * s2 > P.kappa * H);
   t3 = gate ? ((A * pow_m_t<GEN>(P.m_grass, s2, a)) * a) * W : T(0);
 }

@@ -1,0 +1,148 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(fused path, HGS on, default tiling).
+
+* C3 4096^2 (the third config, 16.7 M cells): the whole grid against the oracle over
+  3 steps -- every cell and the dt log bitwise.
+* C5 16384^2 (the bench workload, 268 M cells): the oracle cannot run the whole grid in
+  test time, so (a) tau_0 is computed by the oracle from the Eq.7 maxima of the initial
+  state, reduced strip by strip (max is exact and order-free); (b) after
+  one GPU step, sampled 48 x 48 patches (the 4 wall corners, wet/dry fronts, random
+  interior points) are recomputed by the oracle one by one: a patch plus its 3 ghost
+  layers taken from the real neighbours (walls mirrored by the oracle itself) determines
+  the patch's update exactly (stencil radius 3), stepped with tau_0;
+  (c) properties that hold at any size over 12 steps: HGS on == HGS off bitwise, exact
+  volume bookkeeping of the walled domain, no negative depth."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+GH = oracle.GHOST
+
+
+@pytest.fixture(scope="module")
+def cs():
+    from paper_2103_15196_b200 import build, csph
+    build.build()
+    return csph
+
+
+def test_C3_full_grid_3_steps_bitwise(cs):
+    c = synth.config("C3")
+    assert (c.nx, c.ny) == (4096, 4096)
+    f = synth.fill(c)
+    ref = oracle.Oracle(c.nx, c.ny, c.dx, oracle.Params(**c.params))
+    assert ref.set_state(*f) == 0
+    st, dt_ref, lim_ref = ref.step(3)
+    assert st == 0
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params))
+    g.set_state(*f)
+    g.step(3)
+    dt, lim = g.get_dt_log(3)
+    assert np.array_equal(dt, dt_ref) and np.array_equal(lim, lim_ref)
+    for a, r in zip(g.get_state(), ref.get_state()):
+        assert np.array_equal(a, r)
+    g.destroy()
+
+
+def _window(a, i0, i1, j0, j1, fill):
+    """Padded window of rows j0-3..j1+3, cols i0-3..i1+3; cells outside the grid get
+    `fill` (they are wall ghosts, which the oracle mirrors itself)."""
+    ny, nx = a.shape
+    out = np.full((j1 - j0 + 2 * GH, i1 - i0 + 2 * GH), fill)
+    ja, jb = max(0, j0 - GH), min(ny, j1 + GH)
+    ia, ib = max(0, i0 - GH), min(nx, i1 + GH)
+    out[ja - (j0 - GH):jb - (j0 - GH), ia - (i0 - GH):ib - (i0 - GH)] = a[ja:jb, ia:ib]
+    return out
+
+
+def _patches(wet, n, rng, size):
+    ny, nx = wet.shape
+    m = size
+    ps = [(0, 0), (nx - m, 0), (0, ny - m), (nx - m, ny - m)]  # wall corners
+    # wet/dry fronts: cells whose east neighbour differs
+    fr = np.argwhere(wet[:, :-1] != wet[:, 1:])
+    for k in rng.choice(len(fr), size=6, replace=False):
+        j, i = fr[k]
+        ps.append((int(np.clip(i - m // 2, 0, nx - m)), int(np.clip(j - m // 2, 0, ny - m))))
+    for _ in range(n):
+        ps.append((int(rng.integers(0, nx - m)), int(rng.integers(0, ny - m))))
+    return ps
+
+
+def test_C5_full_size_sampled_vs_oracle(cs):
+    c = synth.config("C5")
+    assert (c.nx, c.ny) == (16384, 16384)
+    P = oracle.Params(**c.params)
+    f = synth.fill(c)
+    h, hu, hv, b, psi = f
+    # (a) tau_0 from the oracle's Eq.7 maxima of the initial state, strip by strip
+    M = np.zeros(3)
+    step = 1024
+    for j0 in range(0, c.ny, step):
+        j1 = min(c.ny, j0 + step)
+        o = oracle.Oracle(c.nx, j1 - j0, c.dx, P)
+        assert o.set_state(h[j0:j1], hu[j0:j1], hv[j0:j1], b[j0:j1], psi[j0:j1]) == 0
+        M = np.maximum(M, o.reduce_M())
+        del o
+    st, tau0, lim0 = oracle.Oracle(8, 8, c.dx, P).tau_from_M(M)
+    assert st == 0
+    # the GPU, bench configuration, one step
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params))
+    g.set_state(*f)
+    g.step(1)
+    dt, lim = g.get_dt_log(1)
+    assert dt[0] == tau0 and lim[0] == lim0
+    # (b) sampled patches recomputed by the oracle
+    size = 48
+    W = 1.0 / (1.0 - psi)
+    rng = np.random.default_rng(2103)
+    for (i0, j0) in _patches(h > P.eps_dry, 10, rng, size):
+        i1, j1 = i0 + size, j0 + size
+        o = oracle.Oracle(size, size, c.dx, P)
+        o.set_walls(i0 == 0, i1 == c.nx, j0 == 0, j1 == c.ny)
+        assert o.set_state_padded(*[_window(a, i0, i1, j0, j1, 0.0) for a in (h, hu, hv, b)],
+                                  _window(W, i0, i1, j0, j1, 1.0)) == 0
+        assert o.step_tau(tau0) == 0
+        ref = o.get_state()
+        got = g.get_state_rows(j0, j1)
+        for a, r in zip(got, ref):
+            assert np.array_equal(a[:, i0:i1], r), (i0, j0)
+    g.destroy()
+
+
+def test_C5_full_size_hgs_and_conservation(cs):
+    c = synth.config("C5")
+    f = synth.fill(c)
+    W = 1.0 / (1.0 - f[4])
+    vol0 = float(np.sum(f[0]))
+    sed0 = float(np.sum(f[3] / W))  # sum (1 - psi) b
+    steps = 12
+    gs = []
+    for hgs in (1, 0):  # both handles resident (2 x 19 GB of HBM)
+        g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, hgs=hgs))
+        g.set_state(*f)
+        g.step(steps)
+        gs.append(g)
+    del f
+    assert np.array_equal(gs[0].get_dt_log(steps)[0], gs[1].get_dt_log(steps)[0])
+    assert gs[0].tile_stats()[2] > 0  # HGS skipped tiles
+    vol = sed = 0.0
+    hmin = np.inf
+    for j0 in range(0, c.ny, 2048):  # row chunks: bounded host memory
+        a = gs[0].get_state_rows(j0, j0 + 2048)
+        r = gs[1].get_state_rows(j0, j0 + 2048)
+        for x, y in zip(a, r):
+            assert np.array_equal(x, y), j0
+        vol += float(np.sum(a[0]))
+        sed += float(np.sum(a[3] / W[j0:j0 + 2048]))
+        hmin = min(hmin, float(a[0].min()))
+    for g in gs:
+        g.destroy()
+    assert hmin >= -1e-12
+    # walls: no mass crosses the boundary; R's update is a flux difference, so the sums
+    # change only by rounding (268 M cells, 12 steps)
+    assert abs(vol - vol0) <= 1e-11 * vol0
+    assert abs(sed - sed0) <= 1e-11 * abs(sed0)

@@ -196,3 +196,37 @@ def test_hgs_with_bed_source_term(cs):
     c2 = synth.Config("C5q", 5, c.nx, c.ny, params=p)
     gpu, ref = run_both(cs, c2, 40, "fused", fields=f)
     assert_parity(gpu, ref)
+
+
+def _radial_dam(nx, ny, ci, cj, r=9.0):
+    """Flat-bed circular dam (C1-style, radius r cells around cell (ci, cj)): the front
+    crosses tile edges in every direction and at the corners."""
+    jj, ii = np.mgrid[0:ny, 0:nx]
+    h = np.where((ii - ci) ** 2 + (jj - cj) ** 2 < r * r, 1.0, 0.0)
+    z = np.zeros((ny, nx))
+    b = 0.01 * np.sin(0.3 * ii) * np.cos(0.2 * jj)
+    return h, z.copy(), z.copy(), b, np.full((ny, nx), 0.4)
+
+
+@pytest.mark.parametrize("strips", [1, 2, 3])
+def test_hgs_band_rule_narrow_tiles(cs, strips):
+    """HGS band-mask rule with 16-row tiles, a 1-column last tile column
+    (nx = 241 = 2 x 120 + 1) and strips whose last tile has 1-2 rows: a radial front
+    crossing tile edges, corners and strip edges must give the HGS-off result bitwise."""
+    nx, ny, steps = 241, 131, 150
+    f = _radial_dam(nx, ny, 120, 64)
+    phys = dict(n_manning=0.03, A_J=1e-3, C_J=2.0, C_Sh=4.0, d50=1e-3)
+    res = []
+    for hgs in (1, 0):
+        p = cs.params_from(phys, hgs=hgs, tile_rows=16)
+        g = (cs.csph_create(nx, ny, 1.0, p) if strips == 1
+             else cs.csph_create_multi(nx, ny, 1.0, p, [0] * strips))
+        g.set_state(*f)
+        g.step(steps)
+        res.append((g.get_dt_log(steps)[0], g.get_state(), g.tile_stats() if strips == 1 else None))
+        g.destroy()
+    assert np.array_equal(res[0][0], res[1][0])
+    for a, b in zip(res[0][1], res[1][1]):
+        assert np.array_equal(a, b)
+    if strips == 1:
+        assert res[0][2][2] > 0  # tiles were actually skipped
