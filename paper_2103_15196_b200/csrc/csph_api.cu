@@ -111,6 +111,7 @@ struct Strip {
   int* limlog = nullptr;             // device [LOGCAP]
   int* dflags = nullptr;             // device validation flags
   unsigned char* tflag = nullptr;    // HGS tile wet flags [2][ntiles]
+  int ty = 128;                      // rows per CTA tile of the fused kernel (= HGS tile)
   unsigned char* tstate = nullptr;   // HGS identity-copy counters [ntiles]
   unsigned long long* hstats = nullptr;  // HGS tile counters: marched, copied, skipped
   int ntx = 0, nty = 0;
@@ -148,7 +149,28 @@ struct csph {
   std::vector<cudaEvent_t> evs;  // pairs around the main kernel of each step (strip 0)
   double prof_ms = 0.0;
   long long prof_steps = 0;
+  // single-grid handles replay steps in pairs from CUDA graphs (one per starting buffer
+  // parity: the HGS flag buffers alternate); rebuilt after anything a launch bakes in
+  // (state upload, spatial fields) changes.  CSPH_NO_GRAPHS=1 turns them off.
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  long long graph_kernels = 0;  // kernel launches inside one pair graph
+  cudaStream_t cap = nullptr;   // private capture stream (the handle's may be the legacy default)
+  bool graphs = getenv("CSPH_NO_GRAPHS") == nullptr;
 };
+
+static void graphs_reset(csph* H) {
+  for (auto& g : H->gexec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
+static void graphs_free(csph* H) {
+  graphs_reset(H);
+  if (H->cap) cudaStreamDestroy(H->cap);
+  H->cap = nullptr;
+}
 
 // ---------------------------------------------------------------- kernels
 
@@ -539,8 +561,19 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
   if ((st = dalloc(s, (void**)&s.limlog, LOGCAP * sizeof(int)))) return st;
   if ((st = dalloc(s, (void**)&s.dflags, 4 * sizeof(int)))) return st;
   {
-    const int TY = H->p.tile_rows > 0 ? H->p.tile_rows : 128;
+    // tile rows: the caller's, or 128 halved (down to 16) until the grid holds two waves of
+    // 3 resident CTAs per SM -- small grids would otherwise leave SMs idle while a few CTAs
+    // march long columns
+    int TY = H->p.tile_rows;
     s.ntx = (v.nx + FUSED_TX - 1) / FUSED_TX;
+    if (TY <= 0) {
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s.dev);
+      const long long want = 2LL * 3 * nsm;
+      TY = 128;
+      while (TY > 16 && (long long)s.ntx * ((v.ny + TY - 1) / TY) < want) TY /= 2;
+    }
+    s.ty = TY;
     s.nty = (v.ny + TY - 1) / TY;
     const size_t nt = (size_t)s.ntx * s.nty;
     if ((st = dalloc(s, (void**)&s.tflag, 2 * nt))) return st;
@@ -774,6 +807,7 @@ csph_t* csph_create_dist(int nx, int ny, double dx, const csph_params* p, int ra
 void csph_destroy(csph_t* H) {
   if (!H) return;
   if (!H->s.empty()) cudaSetDevice(H->s[0].dev);
+  graphs_free(H);
   for (auto e : H->evs) cudaEventDestroy(e);
   for (auto& s : H->s) strip_free(s);
   if (H->gather) {
@@ -1061,6 +1095,7 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
   if (!H || !h || !hu || !hv || !b) return fail(CSPH_EINVAL, "NULL argument");
   if (j_begin < 0 || j_end > H->ny || j_end <= j_begin) return fail(CSPH_EINVAL, "bad row range");
   H->have_state = false;
+  graphs_reset(H);
   int st;
   for (auto& s : H->s) {
     CK(cudaSetDevice(s.dev));
@@ -1116,6 +1151,7 @@ static int upload_field_rows(Strip& s, double* dst, const double* src_rows, int 
 int csph_set_fields_rows(csph_t* H, int j_begin, int j_end, const double* n_manning,
                          const double* beta, const double* src) {
   if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  graphs_reset(H);
   if (j_begin < 0 || j_end > H->ny || j_end <= j_begin) return fail(CSPH_EINVAL, "bad row range");
   if (H->p.precision == 32)
     return fail(CSPH_EINVAL, "csph_set_fields: the fp32 mode runs the hot-path features only");
@@ -1205,6 +1241,61 @@ static Hgs hgs_of(const csph* H, const Strip& s) {
   return h;
 }
 
+// One step of a single-grid handle: the 3 launches (clear flags, step kernel(s), ctrl)
+// reading buffer host_parity.  Used directly and inside the CUDA-graph capture.
+static int single_step(csph* H, Strip& s) {
+  clear_flags_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
+  H->launches += 1;
+  if (H->p.path == CSPH_PATH_STAGED) {
+    launch_staged_step(s.v, s.ctrl, s.scr, H->P, s.gM, s.st, &H->launches);
+    launch_mirror(s.v, s.ctrl, 1, s.st, &H->launches);
+  } else {
+    launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, s.ty, hgs_of(H, s), s.st,
+                      &H->launches);
+  }
+  CK(cudaGetLastError());
+  ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 1);
+  H->launches += 1;
+  CK(cudaGetLastError());
+  H->host_parity ^= 1;
+  return CSPH_OK;
+}
+
+// Two steps from buffer parity p as one CUDA graph (captured once, replayed).
+static int graph_pair(csph* H, Strip& s, long long* per_launch) {
+  cudaGraphExec_t& ge = H->gexec[H->host_parity];
+  if (!ge) {
+    const long long l0 = H->launches;
+    const int p0 = H->host_parity;
+    cudaGraph_t gr = nullptr;
+    // capture on a private stream (the legacy default stream cannot be captured); the
+    // graph is then launched on the handle's stream
+    if (!H->cap) CK(cudaStreamCreateWithFlags(&H->cap, cudaStreamNonBlocking));
+    const cudaStream_t user = s.st;
+    s.st = H->cap;
+    cudaError_t e = cudaStreamBeginCapture(s.st, cudaStreamCaptureModeRelaxed);
+    int st = e == cudaSuccess ? CSPH_OK : fail(CSPH_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    if (!st) st = single_step(H, s);
+    if (!st) st = single_step(H, s);
+    e = cudaStreamEndCapture(s.st, &gr);
+    s.st = user;
+    H->host_parity = p0;
+    if (st) return st;
+    if (e != cudaSuccess) return fail(CSPH_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    const cudaError_t e2 = cudaGraphInstantiate(&ge, gr, 0);
+    cudaGraphDestroy(gr);
+    if (e2 != cudaSuccess) {
+      ge = nullptr;
+      return fail(CSPH_ECUDA, "graph instantiate: %s", cudaGetErrorString(e2));
+    }
+    H->graph_kernels = H->launches - l0;
+    H->launches = l0;
+  }
+  CK(cudaGraphLaunch(ge, s.st));
+  *per_launch = H->graph_kernels;
+  return CSPH_OK;
+}
+
 int csph_step(csph_t* H, int nsteps) {
   if (!H) return fail(CSPH_EINVAL, "handle is NULL");
   if (nsteps < 0) return fail(CSPH_EINVAL, "nsteps < 0");
@@ -1226,7 +1317,7 @@ int csph_step(csph_t* H, int nsteps) {
       // boundary rows first; their halo exchange (NCCL stream) overlaps the interior
       // boundary tile rows first (aligned to the HGS tiling), then the interior
       Strip& s = H->s[0];
-      const int ny = s.v.ny, ty = H->p.tile_rows > 0 ? H->p.tile_rows : 128;
+      const int ny = s.v.ny, ty = s.ty;
       const Hgs hg = hgs_of(H, s);
       const int lo = ty < ny ? ty : ny, hi = (s.nty - 1) * ty;
       clear_flags_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
@@ -1253,6 +1344,22 @@ int csph_step(csph_t* H, int nsteps) {
       H->host_parity = q;
       continue;
     }
+    if (H->mode == SINGLE && H->s.size() == 1 && !H->profiling) {
+      // (profiling runs take the strip loop below: events around the step kernel)
+      Strip& s = H->s[0];
+      CK(cudaSetDevice(s.dev));
+      if (H->graphs && n + 2 <= nsteps) {
+        long long k = 0;
+        int st = graph_pair(H, s, &k);
+        if (st) return st;
+        H->launches += k;
+        ++n;  // two steps replayed; host_parity is back where it was
+        continue;
+      }
+      int st = single_step(H, s);
+      if (st) return st;
+      continue;
+    }
     for (size_t si = 0; si < H->s.size(); ++si) {
       Strip& s = H->s[si];
       CK(cudaSetDevice(s.dev));
@@ -1262,7 +1369,7 @@ int csph_step(csph_t* H, int nsteps) {
       if (H->p.path == CSPH_PATH_STAGED)
         launch_staged_step(s.v, s.ctrl, s.scr, H->P, s.gM, s.st, &H->launches);
       else
-        launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, H->p.tile_rows, hgs_of(H, s),
+        launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, s.ty, hgs_of(H, s),
                           s.st, &H->launches);  // writes the wall ghosts in its epilogue
       if (H->profiling && si == 0) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
       if (H->p.path == CSPH_PATH_STAGED) launch_mirror(s.v, s.ctrl, 1, s.st, &H->launches);

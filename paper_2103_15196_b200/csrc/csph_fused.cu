@@ -26,6 +26,10 @@ namespace ck {
 namespace {
 
 constexpr int kUnroll = CSPH_UNROLL;  // y-march unroll (register renaming of the carries)
+#ifndef CSPH_MINB32
+#define CSPH_MINB32 4
+#endif
+constexpr int kMinB32 = CSPH_MINB32;  // resident CTAs per SM of the fp32 instance
 
 #ifndef CSPH_GUARD
 #define CSPH_GUARD 0
@@ -101,19 +105,22 @@ enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
 // the value is bitwise identical.  Callers have already excluded both-dry cells.
 template <typename T>
 __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T eta_p, T H_p,
-                                       T un_p, T ut_p, T& F0, T& F1, T& F2) {
+                                       T un_p, T ut_p, bool off, T& F0, T& F1, T& F2) {
   const T bs = smax_t(eta_m - H_m, eta_p - H_p);
   const T Hm = smax_t(T(0), eta_m - bs);
   const T Hp = smax_t(T(0), eta_p - bs);
-  const bool dm = !(Hm > T(0)), dp = !(Hp > T(0));
+  // wet flags of the two reconstructed sides (opaque: "both dry" stays two compares)
+  const unsigned wm = gt_u(Hm, T(0)), wp = gt_u(Hp, T(0));
+  const bool dp = wp == 0u;
   const T mm = Hm * un_m, mp = Hp * un_p;
   const T cm = sqrt0_t(g * Hm), cp = sqrt0_t(g * Hp);
   // the three wave-speed cases of R, all evaluated, then selected
   const T aL = un_m - cm, aR = un_p - cp, bL2 = un_m + cm, bR2 = un_p + cp;
-  const bool both = !dm & !dp;
+  const bool both = (wm & wp) != 0u;
   const T SL = both ? smin_t(aL, aR) : (dp ? aL : fma(T(-2), cp, un_p));
   const T SR = both ? smax_t(bL2, bR2) : (dp ? fma(T(2), cm, un_m) : bR2);
-  const bool none = dm && dp;
+  // both reconstructed sides dry, or a both-dry face of cells (off): the face carries 0
+  const bool none = ((wm | wp) == 0u) | off;
   const T den = none ? T(1) : (SR - SL);
   const T inv = rcp_t(den);
   const T SLSR = SL * SR;
@@ -502,14 +509,11 @@ __global__ void __launch_bounds__(NT, MINB)
       sy2[2] = minmod_t(vt2 - vt3, vt1 - vt2);
       sy2[3] = minmod_t(ut2 - ut3, ut1 - ut2);
       if (ANYW(w3 || w2)) {
-        T F0, F1, F2;
+        const bool any = w3 || w2;
         hll_bf(Q.g, fma(T(0.5), sy3[0], eta3), fma(T(0.5), sy3[1], H3), fma(T(0.5), sy3[2], vt3),
                  fma(T(0.5), sy3[3], ut3), fma(T(-0.5), sy2[0], eta2), fma(T(-0.5), sy2[1], H2),
-                 fma(T(-0.5), sy2[2], vt2), fma(T(-0.5), sy2[3], ut2), F0, F1, F2);
-        const bool any = w3 || w2;
-        Gn[0] = any ? F0 : T(0);
-        Gn[2] = any ? F1 : T(0);  // normal momentum of a y-face -> Qy
-        Gn[1] = any ? F2 : T(0);  // tangential -> Qx
+                 fma(T(-0.5), sy2[2], vt2), fma(T(-0.5), sy2[3], ut2), !any,
+                 Gn[0], Gn[2], Gn[1]);  // normal momentum of a y-face -> Qy, tangential -> Qx
         Gn[3] = (any && TRANSP) ? sed_face_t(Q, vt3, vt2, J0y3, J0y2, J0a3, J0a2, b3, b2)
                                      : T(0);
       }
@@ -527,18 +531,15 @@ __global__ void __launch_bounds__(NT, MINB)
       T Fn[4] = {T(0), T(0), T(0), T(0)};
       {
         const T HR = RG(F_H, km1, 1);
-        const bool any = w1 || HR > Q.eps;
+        const bool any = (gt_u(H1, Q.eps) | gt_u(HR, Q.eps)) != 0u;
         if (ANYW(any)) {
           const T bR = RG(F_B, km1, 1);
           const T eR = HR + bR;
           const T uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
-          T F0, F1, F2;
           hll_bf(Q.g, fma(T(0.5), sx1[0], eta1), fma(T(0.5), sx1[1], H1), fma(T(0.5), sx1[2], ut1),
                    fma(T(0.5), sx1[3], vt1), fma(T(-0.5), XG(sm.X3[1], 1), eR), fma(T(-0.5), XG(sm.X3[2], 1), HR),
-                   fma(T(-0.5), XG(sm.X3[3], 1), uR), fma(T(-0.5), XG(sm.X3[4], 1), vR), F0, F1, F2);
-          Fn[0] = any ? F0 : T(0);
-          Fn[1] = any ? F1 : T(0);  // normal momentum of an x-face -> Qx
-          Fn[2] = any ? F2 : T(0);  // tangential -> Qy
+                   fma(T(-0.5), XG(sm.X3[3], 1), uR), fma(T(-0.5), XG(sm.X3[4], 1), vR), !any,
+                   Fn[0], Fn[1], Fn[2]);  // normal momentum of an x-face -> Qx, tangential -> Qy
           Fn[3] = (any && TRANSP) ? sed_face_t(Q, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
                                                   XG(sm.X2[4], 1), b1, bR)
                                        : T(0);
@@ -630,8 +631,9 @@ void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
   Hgs h = hg;
   if (NT - 8 != FUSED_TX) h.enable = 0;  // tiling of the flags is FUSED_TX wide
   if (S.prec == 4) {  // NEXT-2 fp32 mode: hot-path features only (checked at create)
-    if (S.W) launch_t<float, NT, true, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
-    else launch_t<float, NT, false, D, PF, MINB, false>(S, C, P, gM, row0, row1, TY, h, st);
+    // fp32 state halves the ring and the registers: one more resident CTA per SM
+    if (S.W) launch_t<float, NT, true, D, PF, kMinB32, false>(S, C, P, gM, row0, row1, TY, h, st);
+    else launch_t<float, NT, false, D, PF, kMinB32, false>(S, C, P, gM, row0, row1, TY, h, st);
     return;
   }
   // GEN: NEXT-3/4 features present or a physics term switched off; otherwise the

@@ -25,6 +25,16 @@ __device__ __forceinline__ PT<T> make_pt(const Phys& P) {
   return q;
 }
 
+// Opaque copy of a 0/1 flag: stops the compiler from folding "x > c || y > c" into
+// "fmax(x, y) > c", which sm_100 has no fp64 instruction for (an 8-instruction emulation
+// instead of two compares).
+__device__ __forceinline__ unsigned opq(unsigned x) {
+  unsigned y;
+  asm("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+template <typename T> __device__ __forceinline__ unsigned gt_u(T x, T c) { return opq(x > c ? 1u : 0u); }
+
 template <typename T> __device__ __forceinline__ T smin_t(T a, T b) { return (a < b) ? a : b; }
 template <typename T> __device__ __forceinline__ T smax_t(T a, T b) { return (a > b) ? a : b; }
 
@@ -36,6 +46,16 @@ __device__ __forceinline__ T minmod_t(T a, T b) {
   const bool same = ((a > T(0)) & (b > T(0))) | ((a < T(0)) & (b < T(0)));
   const T pick = (fabs(a) < fabs(b)) ? a : b;
   return same ? pick : T(0);
+}
+// fp64: the same value with two fp64 compares instead of five.  pick is the operand of
+// smaller magnitude, so pick != 0 <=> both are nonzero; equal sign bits (integer test on
+// the high words) then means both > 0 or both < 0.  Identical to R for every non-NaN a, b
+// (a NaN slope only arises from a non-finite state, which Eq.7 reports as ENONFINITE).
+template <>
+__device__ __forceinline__ double minmod_t<double>(double a, double b) {
+  const double pick = (fabs(a) < fabs(b)) ? a : b;
+  const bool same = ((__double2hiint(a) ^ __double2hiint(b)) >= 0) & (pick != 0.0);
+  return same ? pick : 0.0;
 }
 
 __device__ __forceinline__ double rcp_t(double x) { return rcp_nb(x); }

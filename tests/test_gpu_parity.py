@@ -230,3 +230,43 @@ def test_hgs_band_rule_narrow_tiles(cs, strips):
         assert np.array_equal(a, b)
     if strips == 1:
         assert res[0][2][2] > 0  # tiles were actually skipped
+
+
+def test_cuda_graph_replay_is_exact(cs, monkeypatch):
+    """csph_step replays step pairs from CUDA graphs (one per starting buffer parity).
+    Odd and even step counts, a re-upload of the state between calls (graph rebuild) and
+    both paths: bitwise equal to plain launches (CSPH_NO_GRAPHS=1) and to the oracle."""
+    c = synth.config("C5", 300, 260)
+    f = synth.fill(c)
+    f2 = synth.fill(synth.config("C3", 300, 260))
+    plan = [3, 4, 1, 2]
+    for path in (0, 1):
+        res = []
+        for nog, default_stream in ((False, False), (True, False), (False, True)):
+            if nog:
+                monkeypatch.setenv("CSPH_NO_GRAPHS", "1")
+            else:
+                monkeypatch.delenv("CSPH_NO_GRAPHS", raising=False)
+            g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, path=path))
+            if default_stream:  # what bench.py does: torch's (legacy default) stream
+                g.set_stream(0)
+            g.set_state(*f)
+            for n in plan:
+                g.step(n)
+            a = (g.get_dt_log(sum(plan))[0], g.get_state(), g.last_launch_count())
+            g.set_state(*f2)  # rebuilds the graphs (W and the state changed)
+            g.step(5)
+            res.append((a, g.get_dt_log(5)[0], g.get_state()))
+            g.destroy()
+        (a0, d0, s0) = res[0]
+        for (a1, d1, s1) in res[1:]:
+            assert np.array_equal(a0[0], a1[0]) and np.array_equal(d0, d1)
+            for x, y in zip(a0[1] + s0, a1[1] + s1):
+                assert np.array_equal(x, y)
+            assert a0[2] == a1[2]  # kernels launched by the last call (graph or not)
+    ref = oracle.Oracle(c.nx, c.ny, c.dx, oracle.Params(**c.params))
+    ref.set_state(*f)
+    st, dt_ref, _ = ref.step(sum(plan))
+    assert np.array_equal(dt_ref, a0[0])
+    for x, y in zip(ref.get_state(), a0[1]):
+        assert np.array_equal(x, y)

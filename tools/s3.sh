@@ -1,0 +1,17 @@
+# profile session: tests, bench line, launch list, representative full capture (step 7)
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+T=${TAG:-s3}
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -8 > gpurun_out/${T}_pytest.txt
+timeout 600 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+    --log-file gpurun_out/${T}_launches.csv \
+    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_step -s 6 -c 1 \
+    -o gpurun_out/${T}_fused_full -f \
+    python bench.py --steps 2 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/${T}_ncu_full.log 2>&1
+timeout 300 python bench.py --precision 32 --no-cpu-baseline --no-e2e > gpurun_out/${T}_bench32.json 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_step -s 6 -c 1 \
+    -o gpurun_out/${T}_fused32_full -f \
+    python bench.py --precision 32 --steps 2 --warmup 5 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+ls gpurun_out | grep ${T}_
