@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override the grid size (n x n)")
     ap.add_argument("--path", choices=["fused", "staged"], default="fused")
     ap.add_argument("--tile-rows", type=int, default=0)
+    ap.add_argument("--partition", choices=["balanced", "even"], default="balanced",
+                    help="N > 1 row strips: balanced by the initial wet cells per row "
+                         "(csph_balance_rows, DESIGN.md 9) or the paper's even Ny_dev split")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                     help="strong: the whole 16384^2 C5 grid split over N GPUs (default); "
                          "weak: rows [0, 2048 N) of the same C5 field, 2048 rows per GPU")
@@ -187,6 +190,33 @@ def run_reference(a, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def strip_bounds(gen, ny, nx, world, rank, kind, device):
+    """Row-strip bounds [0, ..., ny] for `world` ranks (identical on every rank).
+    kind "even": the paper's Ny_dev split (csph_strip_rows).  kind "balanced": per-row cost
+    of the fused kernel ~ wet cells (full-cost work) + 0.03 nx (dry rows, skipped tiles)
+    of the initial state; each rank counts its even strip of the field
+    `gen`, the counts are all-gathered and every rank runs csph_balance_rows on them."""
+    from paper_2103_15196_b200 import csph
+    if world == 1:
+        return [0, ny]
+    bounds = [csph.csph_strip_rows(ny, world, r)[0] for r in range(world)] + [ny]
+    if kind == "even":
+        return bounds
+    import torch
+    import torch.distributed as dist
+    import synth
+    e0, e1 = bounds[rank], bounds[rank + 1]
+    cnt = (synth.fill(gen, e0, e1)[0] > 1e-6).sum(axis=1).astype(np.float64)
+    mx = max(bounds[r + 1] - bounds[r] for r in range(world))
+    buf = torch.zeros(mx, dtype=torch.float64, device=device)
+    buf[:e1 - e0] = torch.from_numpy(cnt)
+    parts = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    w = np.concatenate([parts[r][:bounds[r + 1] - bounds[r]].cpu().numpy()
+                        for r in range(world)]) + 0.03 * nx
+    return csph.csph_balance_rows(ny, world, w)
+
+
 def run_ours(a, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -207,7 +237,8 @@ def run_ours(a, rank, world, local):
     path = csph.CSPH_PATH_FUSED if a.path == "fused" else csph.CSPH_PATH_STAGED
     p = csph.params_from(c.params, path=path, device=local, tile_rows=a.tile_rows,
                          precision=a.precision)
-    j0, j1 = csph.csph_strip_rows(c.ny, world, rank)
+    bounds = strip_bounds(gen, c.ny, c.nx, world, rank, a.partition, "cuda")
+    j0, j1 = bounds[rank], bounds[rank + 1]
     wa, wb = max(0, j0 - 3), min(c.ny, j1 + 3)
     fields = synth.fill(gen, wa, wb)
     wet_local = float(np.count_nonzero(fields[0][j0 - wa:j1 - wa] > 1e-6))
@@ -216,8 +247,8 @@ def run_ours(a, rank, world, local):
         if rank == 0:
             idt.copy_(torch.frombuffer(bytearray(csph.csph_make_nccl_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
-        g = csph.csph_create_dist(c.nx, c.ny, c.dx, p, rank, world, local,
-                                  bytes(idt.cpu().numpy().tobytes()))
+        g = csph.csph_create_dist_rows(c.nx, c.ny, c.dx, p, rank, world, bounds, local,
+                                       bytes(idt.cpu().numpy().tobytes()))
     else:
         g = csph.csph_create(c.nx, c.ny, c.dx, p)
     stream = torch.cuda.current_stream()
@@ -350,6 +381,7 @@ def run_ours(a, rank, world, local):
                 "psi": "field" if psi_field else "uniform", "physics": c.params,
                 "path": a.path, "parallelism": f"row strips x{world} (NCCL halos + allreduce)"
                 if world > 1 else "single GPU",
+                "partition": {"kind": a.partition, "bounds": bounds} if world > 1 else None,
                 "l2": "state (>= 19 GB) larger than the 126 MB L2; no flush needed",
                 "tau_mean": float(np.mean(dtl)) if len(dtl) else None,
                 "limiter_hist": np.bincount(liml, minlength=4).tolist() if len(liml) else None,

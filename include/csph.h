@@ -147,6 +147,15 @@ int         csph_set_stream(csph_t*, void* cuda_stream);
  * Host-only; CSPH_EINVAL if a strip would have fewer than 3 rows. */
 int         csph_strip_rows(int ny, int nranks, int rank, int* j0, int* j1);
 
+/* Load-balanced row partition (host-only).  w[0..ny) are non-negative per-row costs
+ * (e.g. the wet cells of each row plus a small per-row constant: the fused kernel's time
+ * is set by its wet tiles).  Writes bounds[0..nranks] with bounds[0] = 0,
+ * bounds[nranks] = ny, every strip >= 3 rows, minimising the largest strip cost (bisection
+ * on it; feasibility by a reachability sweep, O(nranks * ny) per probe).  All-zero weights
+ * give the even split.  CSPH_EINVAL
+ * on a NULL pointer, a negative/NaN weight, or ny < 3 * nranks. */
+int         csph_balance_rows(int ny, int nranks, const double* w, int* bounds);
+
 void        csph_destroy(csph_t*);
 const char* csph_strerror(int code);
 const char* csph_last_error(void);
@@ -160,6 +169,13 @@ int         csph_nccl_id_bytes(void);
 int         csph_make_nccl_id(void* out);
 csph_t*     csph_create_dist(int nx, int ny, double dx, const csph_params* p,
                              int rank, int nranks, int local_device, const void* nccl_id);
+/* The same with a caller-chosen partition: rank r owns rows [bounds[r], bounds[r+1])
+ * (bounds[0..nranks], identical on every rank; e.g. from csph_balance_rows).  NULL and
+ * CSPH_EINVAL (csph_last_error) unless 0 = bounds[0] < ... < bounds[nranks] = ny with every
+ * strip >= 3 rows. */
+csph_t*     csph_create_dist_rows(int nx, int ny, double dx, const csph_params* p,
+                                  int rank, int nranks, const int* bounds, int local_device,
+                                  const void* nccl_id);
 
 /* Single-process row-strip decomposition: nstrips strips on the devices
  * listed in `devices` (strips may share a device), halos copied with
@@ -168,6 +184,9 @@ csph_t*     csph_create_dist(int nx, int ny, double dx, const csph_params* p,
  * one-host-thread-drives-all-GPUs arrangement). */
 csph_t*     csph_create_multi(int nx, int ny, double dx, const csph_params* p,
                               int nstrips, const int* devices);
+/* The same with caller-chosen strip rows bounds[0..nstrips] (as csph_create_dist_rows). */
+csph_t*     csph_create_multi_rows(int nx, int ny, double dx, const csph_params* p,
+                                   int nstrips, const int* devices, const int* bounds);
 
 /* Kernel timing (bench): when enabled, csph_step records CUDA events on the
  * handle's stream around each step's main kernel(s) (the fused step kernel, or

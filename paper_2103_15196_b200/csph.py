@@ -25,7 +25,8 @@ EXPORTS = [
     "csph_get_state", "csph_get_state_rows", "csph_get_time", "csph_get_dt_log",
     "csph_get_maxima", "csph_set_stream", "csph_strip_rows", "csph_destroy", "csph_strerror",
     "csph_last_error", "csph_nccl_id_bytes", "csph_make_nccl_id", "csph_create_dist",
-    "csph_create_multi", "csph_last_launch_count", "csph_profile", "csph_get_profile",
+    "csph_create_multi", "csph_create_multi_rows", "csph_create_dist_rows", "csph_balance_rows",
+    "csph_last_launch_count", "csph_profile", "csph_get_profile",
     "csph_selftest_math", "csph_get_tile_stats", "csph_reset_tile_stats",
     "csph_set_fields", "csph_set_fields_rows",
 ]
@@ -74,6 +75,14 @@ def lib():
         L.csph_create_multi.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                         ctypes.POINTER(csph_params), ctypes.c_int, _I]
         L.csph_create_multi.restype = _vp
+        L.csph_create_dist_rows.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                            ctypes.POINTER(csph_params), ctypes.c_int,
+                                            ctypes.c_int, _I, ctypes.c_int, ctypes.c_void_p]
+        L.csph_create_dist_rows.restype = _vp
+        L.csph_create_multi_rows.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                             ctypes.POINTER(csph_params), ctypes.c_int, _I, _I]
+        L.csph_create_multi_rows.restype = _vp
+        L.csph_balance_rows.argtypes = [ctypes.c_int, ctypes.c_int, _D, _I]
         L.csph_set_state.argtypes = [_vp, _D, _D, _D, _D, _D]
         L.csph_set_state_rows.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D, _D]
         L.csph_step.argtypes = [_vp, ctypes.c_int]
@@ -142,6 +151,16 @@ def csph_strip_rows(ny: int, nranks: int, rank: int):
     j0, j1 = ctypes.c_int(), ctypes.c_int()
     _check(lib().csph_strip_rows(ny, nranks, rank, ctypes.byref(j0), ctypes.byref(j1)), "csph_strip_rows")
     return j0.value, j1.value
+
+
+def csph_balance_rows(ny: int, nranks: int, w) -> list:
+    """Load-balanced partition bounds[0..nranks] of ny rows with per-row costs w."""
+    import numpy as np
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    assert w.shape == (ny,)
+    b = (ctypes.c_int * (nranks + 1))()
+    _check(lib().csph_balance_rows(ny, nranks, w.ctypes.data_as(_D), b), "csph_balance_rows")
+    return list(b)
 
 
 def csph_selftest_math(n: int, seed: int = 1) -> int:
@@ -273,6 +292,23 @@ def csph_create_multi(nx: int, ny: int, dx: float, params, devices) -> Csph:
     p = _params(params)
     arr = (ctypes.c_int * len(devices))(*devices)
     return Csph(lib().csph_create_multi(nx, ny, dx, ctypes.byref(p), len(devices), arr), nx, ny, dx, p)
+
+
+def csph_create_multi_rows(nx: int, ny: int, dx: float, params, devices, bounds) -> Csph:
+    p = _params(params)
+    arr = (ctypes.c_int * len(devices))(*devices)
+    b = (ctypes.c_int * len(bounds))(*bounds)
+    return Csph(lib().csph_create_multi_rows(nx, ny, dx, ctypes.byref(p), len(devices), arr, b),
+                nx, ny, dx, p)
+
+
+def csph_create_dist_rows(nx: int, ny: int, dx: float, params, rank: int, nranks: int, bounds,
+                          local_device: int, nccl_id: bytes) -> Csph:
+    p = _params(params)
+    buf = ctypes.create_string_buffer(nccl_id, len(nccl_id))
+    b = (ctypes.c_int * len(bounds))(*bounds)
+    return Csph(lib().csph_create_dist_rows(nx, ny, dx, ctypes.byref(p), rank, nranks, b,
+                                            local_device, buf), nx, ny, dx, p)
 
 
 def csph_create_dist(nx: int, ny: int, dx: float, params, rank: int, nranks: int,

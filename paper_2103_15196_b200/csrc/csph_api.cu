@@ -718,21 +718,103 @@ csph_t* csph_create(int nx, int ny, double dx, const csph_params* p) {
   return H;
 }
 
+// bounds[0..n]: 0 = bounds[0] < ... < bounds[n] = ny, every strip >= GY rows
+static int check_bounds(int ny, int n, const int* bounds) {
+  if (!bounds) return fail(CSPH_EINVAL, "bounds is NULL");
+  if (bounds[0] != 0 || bounds[n] != ny) return fail(CSPH_EINVAL, "bounds must run from 0 to ny");
+  for (int r = 0; r < n; ++r)
+    if (bounds[r + 1] - bounds[r] < GY)
+      return fail(CSPH_EINVAL, "strip %d has %d rows (< %d)", r, bounds[r + 1] - bounds[r], GY);
+  return CSPH_OK;
+}
+
+static int even_bounds(int ny, int n, std::vector<int>& b) {
+  b.assign(n + 1, 0);
+  for (int r = 0; r < n; ++r) {
+    int st = csph_strip_rows(ny, n, r, &b[r], &b[r + 1]);
+    if (st) return st;
+  }
+  return CSPH_OK;
+}
+
+int csph_balance_rows(int ny, int nranks, const double* w, int* bounds) {
+  if (ny < GY || nranks < 1 || !w || !bounds || (long long)nranks * GY > ny)
+    return fail(CSPH_EINVAL, "bad balance request (ny=%d, nranks=%d)", ny, nranks);
+  double tot = 0.0;
+  for (int j = 0; j < ny; ++j) {
+    if (!(w[j] >= 0.0) || !std::isfinite(w[j])) return fail(CSPH_EINVAL, "row weight %d invalid", j);
+    tot += w[j];
+  }
+  std::vector<int> b;
+  if (!(tot > 0.0)) {  // nothing to balance: the even split
+    int st = even_bounds(ny, nranks, b);
+    if (st) return st;
+    for (int r = 0; r <= nranks; ++r) bounds[r] = b[r];
+    return CSPH_OK;
+  }
+  // feasible(T): can rows [0, ny) be cut into nranks contiguous strips of >= GY rows, each
+  // of cost <= T?  reach[r][e] = rows [0, e) split into r such strips; the best start for
+  // an end e is the largest reachable s <= e - GY (costs are >= 0).  O(nranks * ny).
+  std::vector<double> pre(ny + 1, 0.0);
+  for (int j = 0; j < ny; ++j) pre[j + 1] = pre[j] + w[j];
+  std::vector<std::vector<char>> reach(nranks + 1, std::vector<char>(ny + 1, 0));
+  auto feasible = [&](double T) {
+    for (auto& v : reach) std::fill(v.begin(), v.end(), 0);
+    reach[0][0] = 1;
+    for (int r = 1; r <= nranks; ++r) {
+      int last = -1;
+      for (int e = GY; e <= ny; ++e) {
+        if (reach[r - 1][e - GY]) last = e - GY;
+        if (last >= 0 && pre[e] - pre[last] <= T) reach[r][e] = 1;
+      }
+    }
+    return reach[nranks][ny] != 0;
+  };
+  // bisection on the largest strip cost T, then walk the cuts back from ny
+  double lo = 0.0, hi = tot;
+  for (int it = 0; it < 200 && hi - lo > 1e-13 * hi; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (feasible(mid)) hi = mid; else lo = mid;
+  }
+  if (!feasible(hi)) return fail(CSPH_EINVAL, "no partition of %d rows into %d strips", ny, nranks);
+  b.assign(nranks + 1, 0);
+  b[nranks] = ny;
+  for (int r = nranks; r >= 1; --r) {
+    const int e = b[r];
+    int s0 = e - GY;
+    while (s0 >= 0 && !(reach[r - 1][s0] && pre[e] - pre[s0] <= hi)) --s0;
+    if (s0 < 0) return fail(CSPH_EINVAL, "partition walk-back failed");
+    b[r - 1] = s0;
+  }
+  for (int r = 0; r <= nranks; ++r) bounds[r] = b[r];
+  return check_bounds(ny, nranks, bounds);
+}
+
 csph_t* csph_create_multi(int nx, int ny, double dx, const csph_params* p, int nstrips,
                           const int* devices) {
+  std::vector<int> b;
+  if (nstrips < 1 || even_bounds(ny, nstrips, b)) {
+    if (nstrips < 1) fail(CSPH_EINVAL, "nstrips < 1");
+    return nullptr;
+  }
+  return csph_create_multi_rows(nx, ny, dx, p, nstrips, devices, b.data());
+}
+
+csph_t* csph_create_multi_rows(int nx, int ny, double dx, const csph_params* p, int nstrips,
+                               const int* devices, const int* bounds) {
   if (nstrips < 1 || !devices) {
     fail(CSPH_EINVAL, "nstrips < 1 or devices NULL");
     return nullptr;
   }
+  if (check_bounds(ny, nstrips, bounds)) return nullptr;
   csph* H = make_handle(nx, ny, dx, p);
   if (!H) return nullptr;
   H->mode = MULTI;
   H->nranks = nstrips;
   H->s.resize(nstrips);
   for (int r = 0; r < nstrips; ++r) {
-    int j0, j1;
-    if (csph_strip_rows(ny, nstrips, r, &j0, &j1) ||
-        strip_init(H, H->s[r], devices[r], j0, j1 - j0, p->path == CSPH_PATH_STAGED)) {
+    const int j0 = bounds[r], j1 = bounds[r + 1];
+    if (strip_init(H, H->s[r], devices[r], j0, j1 - j0, p->path == CSPH_PATH_STAGED)) {
       std::string keep = g_err;
       csph_destroy(H);
       g_err = keep;
@@ -770,12 +852,23 @@ int csph_make_nccl_id(void* out) {
 
 csph_t* csph_create_dist(int nx, int ny, double dx, const csph_params* p, int rank,
                          int nranks, int local_device, const void* nccl_id) {
+  std::vector<int> b;
+  if (nranks < 1 || even_bounds(ny, nranks, b)) {
+    if (nranks < 1) fail(CSPH_EINVAL, "nranks < 1");
+    return nullptr;
+  }
+  return csph_create_dist_rows(nx, ny, dx, p, rank, nranks, b.data(), local_device, nccl_id);
+}
+
+csph_t* csph_create_dist_rows(int nx, int ny, double dx, const csph_params* p, int rank,
+                              int nranks, const int* bounds, int local_device,
+                              const void* nccl_id) {
   if (nranks < 1 || rank < 0 || rank >= nranks || !nccl_id) {
     fail(CSPH_EINVAL, "bad rank/nranks/nccl_id");
     return nullptr;
   }
-  int j0, j1;
-  if (csph_strip_rows(ny, nranks, rank, &j0, &j1)) return nullptr;
+  if (check_bounds(ny, nranks, bounds)) return nullptr;
+  const int j0 = bounds[rank], j1 = bounds[rank + 1];
   if (!load_nccl()) return nullptr;
   csph* H = make_handle(nx, ny, dx, p);
   if (!H) return nullptr;

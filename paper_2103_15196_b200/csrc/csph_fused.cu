@@ -615,8 +615,7 @@ void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
   using SM = Smem<T, NT, HASW, D>;
   constexpr int TX = NT - 8;
   static bool configured = false;
-  static const size_t pad = getenv("CSPH_SMEM_PAD") ? (size_t)atol(getenv("CSPH_SMEM_PAD")) : 0;
-  const size_t smem = sizeof(SM) + pad;  // pad: development knob (occupancy experiments)
+  const size_t smem = sizeof(SM);
   if (!configured) {
     cudaFuncSetAttribute(fused_step_kernel<T, NT, HASW, D, PF, MINB, GEN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -652,28 +651,16 @@ void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
   }
 }
 
-int fused_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CSPH_FUSED_VARIANT");  // development knob
-    v = e ? atoi(e) : 5;
-  }
-  return v;
-}
-
 }  // namespace
 
 void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM,
                        int row0, int row1, int tile_rows, const Hgs& hg, cudaStream_t st,
                        long long* nlaunch) {
   if (row1 <= row0) return;
-  int TY = tile_rows > 0 ? tile_rows : 128;
-  switch (fused_variant()) {
-    case 6: launch_v<128, 10, 5, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 8: launch_v<128, 6, 1, 4>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    case 9: launch_v<128, 6, 1, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
-    default: launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, hg, st); break;
-  }
+  const int TY = tile_rows > 0 ? tile_rows : 128;
+  // 128 threads (120 output columns), an 8-row TMA ring prefetching 3 rows ahead,
+  // 3 resident CTAs per SM in fp64 (4 in fp32)
+  launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, hg, st);
   *nlaunch += 1;
 }
 

@@ -108,3 +108,34 @@ def test_strip_decomposition_bitwise(tmp_path, world, cfg):
         assert np.array_equal(d["dt"], dt_ref)
         assert np.array_equal(d["h"], H[j0:j1]) and np.array_equal(d["b"], b[j0:j1])
         assert np.array_equal(d["hu"], Qx[j0:j1]) and np.array_equal(d["hv"], Qy[j0:j1])
+
+
+def _bounds_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    c = synth.config("C5", 600, 700)
+    b = bench.strip_bounds(c, c.ny, c.nx, world, rank, "balanced", "cpu")
+    np.save(os.path.join(out_dir, f"b{rank}.npy"), np.array(b))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_balanced_partition(tmp_path, world):
+    """bench.py's load-balanced strips: every rank derives the same bounds
+    from all-gathered wet-row counts, equal to csph_balance_rows on the whole field."""
+    from paper_2103_15196_b200 import csph
+    c = synth.config("C5", 600, 700)
+    h = synth.fill(c)[0]
+    w = (h > 1e-6).sum(axis=1).astype(np.float64) + 0.03 * c.nx
+    ref = csph.csph_balance_rows(c.ny, world, w)
+    mp.spawn(_bounds_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert np.load(tmp_path / f"b{r}.npy").tolist() == ref
+    per = [w[ref[r]:ref[r + 1]].sum() for r in range(world)]
+    even = [w[csph.csph_strip_rows(c.ny, world, r)[0]:csph.csph_strip_rows(c.ny, world, r)[1]].sum()
+            for r in range(world)]
+    assert max(per) <= max(even) + 1e-9

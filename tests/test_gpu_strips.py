@@ -67,3 +67,39 @@ def test_dist_single_rank_nccl(cs):
     for a, r in zip(g.get_state(), ref):
         assert np.array_equal(a, r)
     g.destroy()
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_uneven_strips_bitwise(cs, path):
+    """Caller-chosen (load-balanced) strip rows, csph_create_multi_rows: strips of 3, 17,
+    150 and 33 rows are bitwise the single grid; bounds from csph_balance_rows too."""
+    c = synth.config("C4", 160, 203)
+    f = synth.fill(c)
+    dt0, ref = single(cs, c, f, 50, path)
+    w = (f[0] > 1e-6).sum(axis=1) + 0.03 * c.nx
+    for bounds in ([0, 3, 20, 170, 203], cs.csph_balance_rows(c.ny, 3, w)):
+        g = cs.csph_create_multi_rows(c.nx, c.ny, c.dx, cs.params_from(c.params, path=path),
+                                      [0] * (len(bounds) - 1), bounds)
+        g.set_state(*f)
+        g.step(50)
+        assert np.array_equal(g.get_dt_log(50)[0], dt0)
+        for a, r in zip(g.get_state(), ref):
+            assert np.array_equal(a, r)
+        g.destroy()
+    with pytest.raises(cs.CsphError):
+        cs.csph_create_multi_rows(c.nx, c.ny, c.dx, cs.params_from(c.params), [0, 0], [0, 2, 203])
+
+
+def test_dist_rows_single_rank(cs):
+    """csph_create_dist_rows with one rank and bounds [0, ny]."""
+    c = synth.config("C3", 128, 96)
+    f = synth.fill(c)
+    dt0, ref = single(cs, c, f, 30, 0)
+    g = cs.csph_create_dist_rows(c.nx, c.ny, c.dx, cs.params_from(c.params), 0, 1, [0, c.ny], 0,
+                                 cs.csph_make_nccl_id())
+    g.set_state(*f)
+    g.step(30)
+    assert np.array_equal(g.get_dt_log(30)[0], dt0)
+    for a, r in zip(g.get_state(), ref):
+        assert np.array_equal(a, r)
+    g.destroy()

@@ -29,10 +29,7 @@ for name, f, p in [("wet", wet, phys), ("C5", synth.fill(c), c.params)]:
     g.destroy()
 print(" | ".join(out))
 ''' % ROOT
-for arg in sys.argv[1:]:  # lib[:variant]
-    lib, _, var = arg.partition(":")
+for lib in sys.argv[1:]:
     env = dict(os.environ, CSPH_LIB_DEV=os.path.abspath(lib))
-    if var:
-        env["CSPH_FUSED_VARIANT"] = var
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
-    print(os.path.basename(arg), r.stdout.strip(), r.stderr.strip()[-400:], flush=True)
+    print(os.path.basename(lib), r.stdout.strip(), r.stderr.strip()[-400:], flush=True)

@@ -1,4 +1,6 @@
-# profile session: tests, bench line, launch list, representative full capture (step 7)
+# Profiling session (one gpurun call): GPU tests, the bench line, the ncu launch list of the
+# bench command and representative --set full captures (step 7) of the fp64 and fp32 fused
+# kernels. Outputs gpurun_out/${TAG}_*; summarise with tools/ncu_summarize.py into profiles/.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 T=${TAG:-s3}

@@ -1,0 +1,42 @@
+"""Predicted strong scaling of C5 16384^2 on one GPU (dev aid): each rank's strip
+of rows [j0, j1) is run alone as a walled domain and its step time measured; the N-GPU step
+time is bounded below by the slowest strip (halo exchange and the allreduce are overlapped /
+small).  Compares the paper's even Ny_dev split with the wet-count-balanced one."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import synth
+from paper_2103_15196_b200 import csph
+
+c = synth.config("C5")
+n = c.nx
+steps = int(os.environ.get("STEPS", "10"))
+wet_rows = np.zeros(c.ny)
+for j0 in range(0, c.ny, 2048):
+    wet_rows[j0:j0 + 2048] = (synth.fill(c, j0, j0 + 2048)[0] > 1e-6).sum(axis=1)
+w = wet_rows + 0.03 * n
+
+
+def strip_ms(j0, j1):
+    f = synth.fill(c, j0, j1)
+    g = csph.csph_create(n, j1 - j0, c.dx, csph.params_from(c.params))
+    g.set_state(*f)
+    g.step(3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); g.step(steps); e1.record(); torch.cuda.synchronize()
+    g.destroy()
+    return e0.elapsed_time(e1) / steps
+
+
+t1 = strip_ms(0, c.ny)
+print(f"N=1: {t1:.3f} ms/step, {c.cells / t1 / 1e6:.1f} Gcell/s", flush=True)
+for N in (2, 4, 8):
+    for kind in ("even", "balanced"):
+        b = ([csph.csph_strip_rows(c.ny, N, r)[0] for r in range(N)] + [c.ny]) if kind == "even" \
+            else csph.csph_balance_rows(c.ny, N, w)
+        ts = [strip_ms(b[r], b[r + 1]) for r in range(N)]
+        tN = max(ts)
+        print(f"N={N} {kind:8s}: strips {[b[r + 1] - b[r] for r in range(N)]} ms "
+              f"{[round(x, 3) for x in ts]} -> {c.cells / tN / 1e6:.1f} Gcell/s, "
+              f"efficiency {t1 / (N * tN):.2f}", flush=True)
