@@ -561,15 +561,16 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
   if ((st = dalloc(s, (void**)&s.limlog, LOGCAP * sizeof(int)))) return st;
   if ((st = dalloc(s, (void**)&s.dflags, 4 * sizeof(int)))) return st;
   {
-    // tile rows: the caller's, or 128 halved (down to 16) until the grid holds two waves of
-    // 3 resident CTAs per SM -- small grids would otherwise leave SMs idle while a few CTAs
-    // march long columns
+    // tile rows: the caller's, or 128 halved (down to 16) until the grid holds four waves of
+    // 3 resident CTAs per SM.  With HGS only the wet tiles (a third on C5) do real work, and
+    // a grid with few of them leaves SMs idle while a few CTAs march long columns (measured:
+    // C3 4096^2 +12 %, C5 8-GPU strips +3 % against the two-wave rule)
     int TY = H->p.tile_rows;
     s.ntx = (v.nx + FUSED_TX - 1) / FUSED_TX;
     if (TY <= 0) {
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s.dev);
-      const long long want = 2LL * 3 * nsm;
+      const long long want = 4LL * 3 * nsm;
       TY = 128;
       while (TY > 16 && (long long)s.ntx * ((v.ny + TY - 1) / TY) < want) TY /= 2;
     }
@@ -1402,8 +1403,9 @@ int csph_step(csph_t* H, int nsteps) {
       H->evs.push_back(e);
     }
   }
-  const bool overlap = H->mode == DIST && H->nranks > 1 && H->p.path == CSPH_PATH_FUSED &&
-                       H->s[0].nty >= 2;
+  // (a single rank takes the same split-launch path -- its NCCL calls are no-ops -- so the
+  // launch sequence of the multi-GPU step is exercised on one GPU)
+  const bool overlap = H->mode == DIST && H->p.path == CSPH_PATH_FUSED && H->s[0].nty >= 2;
   for (int n = 0; n < nsteps; ++n) {
     const int q = H->host_parity ^ 1;
     if (overlap) {
@@ -1417,7 +1419,8 @@ int csph_step(csph_t* H, int nsteps) {
       H->launches += 1;
       if (H->profiling) CK(cudaEventRecord(H->evs[2 * n], s.st));
       launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, lo, ty, hg, s.st, &H->launches);
-      if (hi > lo) launch_fused_step(s.v, s.ctrl, H->P, s.gM, hi, ny, ty, hg, s.st, &H->launches);
+      // last tile row (nty >= 2, so hi >= lo: with 2 tile rows there is no interior)
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, hi, ny, ty, hg, s.st, &H->launches);
       CK(cudaEventRecord(s.ev_edge, s.st));
       CK(cudaStreamWaitEvent(s.cst, s.ev_edge, 0));
       int st = halo_nccl(H, q, s.cst);

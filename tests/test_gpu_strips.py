@@ -103,3 +103,22 @@ def test_dist_rows_single_rank(cs):
     for a, r in zip(g.get_state(), ref):
         assert np.array_equal(a, r)
     g.destroy()
+
+
+@pytest.mark.parametrize("tile_rows", [16, 40, 48, 64])
+def test_dist_split_launches(cs, tile_rows):
+    """The multi-GPU step's launch sequence (edge tile rows, NCCL halo on the comm stream,
+    interior, allreduce) on one rank: 2..6 tile rows, ragged last tile row,
+    HGS on -- bitwise the single grid."""
+    c = synth.config("C5", 200, 96)
+    f = synth.fill(c)
+    dt0, ref = single(cs, c, f, 40, 0)
+    g = cs.csph_create_dist_rows(c.nx, c.ny, c.dx, cs.params_from(c.params, tile_rows=tile_rows),
+                                 0, 1, [0, c.ny], 0, cs.csph_make_nccl_id())
+    g.set_state(*f)
+    g.step(40)
+    assert np.array_equal(g.get_dt_log(40)[0], dt0)
+    for a, r in zip(g.get_state(), ref):
+        assert np.array_equal(a, r)
+    assert g.last_launch_count() == 40 * (2 + (3 if c.ny > 2 * tile_rows else 2))
+    g.destroy()

@@ -11,6 +11,9 @@ from paper_2103_15196_b200 import csph
 c = synth.config("C5")
 n = c.nx
 steps = int(os.environ.get("STEPS", "10"))
+TY = int(os.environ.get("TY", "0"))  # tile rows (0 = the library's auto rule)
+NS = [int(x) for x in os.environ.get("NS", "2,4,8").split(",")]
+KINDS = os.environ.get("KINDS", "even,balanced").split(",")
 wet_rows = np.zeros(c.ny)
 for j0 in range(0, c.ny, 2048):
     wet_rows[j0:j0 + 2048] = (synth.fill(c, j0, j0 + 2048)[0] > 1e-6).sum(axis=1)
@@ -19,7 +22,7 @@ w = wet_rows + 0.03 * n
 
 def strip_ms(j0, j1):
     f = synth.fill(c, j0, j1)
-    g = csph.csph_create(n, j1 - j0, c.dx, csph.params_from(c.params))
+    g = csph.csph_create(n, j1 - j0, c.dx, csph.params_from(c.params, tile_rows=TY))
     g.set_state(*f)
     g.step(3)
     torch.cuda.synchronize()
@@ -31,8 +34,8 @@ def strip_ms(j0, j1):
 
 t1 = strip_ms(0, c.ny)
 print(f"N=1: {t1:.3f} ms/step, {c.cells / t1 / 1e6:.1f} Gcell/s", flush=True)
-for N in (2, 4, 8):
-    for kind in ("even", "balanced"):
+for N in NS:
+    for kind in KINDS:
         b = ([csph.csph_strip_rows(c.ny, N, r)[0] for r in range(N)] + [c.ny]) if kind == "even" \
             else csph.csph_balance_rows(c.ny, N, w)
         ts = [strip_ms(b[r], b[r + 1]) for r in range(N)]
