@@ -112,6 +112,10 @@ struct Strip {
   int* dflags = nullptr;             // device validation flags
   unsigned char* tflag = nullptr;    // HGS tile wet flags [2][ntiles]
   int ty = 128;                      // rows per CTA tile of the fused kernel (= HGS tile)
+  bool auto_ty = false;              // ty chosen from the state at set_state
+  size_t tflag_cap = 0;              // tiles the flag buffers hold (finest tiling)
+  unsigned char* wetblk = nullptr;   // auto_ty: wet flags of 120 x 16 blocks [ny/16][ntx]
+  int nsm = 148;
   unsigned char* tstate = nullptr;   // HGS identity-copy counters [ntiles]
   unsigned long long* hstats = nullptr;  // HGS tile counters: marched, copied, skipped
   int ntx = 0, nty = 0;
@@ -177,6 +181,7 @@ static void graphs_free(csph* H) {
 namespace {
 
 constexpr int kStatusFlagNeg = 1;
+constexpr int kTyMin = 16;  // finest automatic tiling (rows)
 
 __global__ void ctrl_kernel(Ctrl* C, unsigned long long* gM, double* Mlast, double* dtlog,
                             int* limlog, Phys P, int advance) {
@@ -561,26 +566,23 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
   if ((st = dalloc(s, (void**)&s.limlog, LOGCAP * sizeof(int)))) return st;
   if ((st = dalloc(s, (void**)&s.dflags, 4 * sizeof(int)))) return st;
   {
-    // tile rows: the caller's, or 128 halved (down to 16) until the grid holds four waves of
-    // 3 resident CTAs per SM.  With HGS only the wet tiles (a third on C5) do real work, and
-    // a grid with few of them leaves SMs idle while a few CTAs march long columns (measured:
-    // C3 4096^2 +12 %, C5 8-GPU strips +3 % against the two-wave rule)
-    int TY = H->p.tile_rows;
+    // tile rows: the caller's, or chosen from the state at every set_state (tile_rows_auto);
+    // until then 128.  The flag buffers are sized for the finest tiling (16 rows).
     s.ntx = (v.nx + FUSED_TX - 1) / FUSED_TX;
-    if (TY <= 0) {
-      int nsm = 148;
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s.dev);
-      const long long want = 4LL * 3 * nsm;
-      TY = 128;
-      while (TY > 16 && (long long)s.ntx * ((v.ny + TY - 1) / TY) < want) TY /= 2;
-    }
-    s.ty = TY;
-    s.nty = (v.ny + TY - 1) / TY;
-    const size_t nt = (size_t)s.ntx * s.nty;
+    s.auto_ty = H->p.tile_rows <= 0;
+    s.ty = s.auto_ty ? 128 : H->p.tile_rows;
+    s.nty = (v.ny + s.ty - 1) / s.ty;
+    const int tymin = s.auto_ty ? kTyMin : s.ty;
+    const size_t nt = (size_t)s.ntx * ((v.ny + tymin - 1) / tymin);
     if ((st = dalloc(s, (void**)&s.tflag, 2 * nt))) return st;
     if ((st = dalloc(s, (void**)&s.tstate, nt))) return st;
+    s.tflag_cap = nt;
     CK(cudaMemset(s.tflag, HGS_ALL, 2 * nt));
     CK(cudaMemset(s.tstate, 0, nt));
+    if (s.auto_ty) {
+      if ((st = dalloc(s, (void**)&s.wetblk, nt))) return st;
+      CK(cudaDeviceGetAttribute(&s.nsm, cudaDevAttrMultiProcessorCount, s.dev));
+    }
     if ((st = dalloc(s, (void**)&s.hstats, 4 * sizeof(unsigned long long)))) return st;
     CK(cudaMemset(s.hstats, 0, 4 * sizeof(unsigned long long)));
   }
@@ -629,6 +631,24 @@ static void strip_free(Strip& s) {
   s.st = nullptr;
   s.ev = nullptr;
 }
+
+namespace {
+// Wet flags of the 120-column x kTyMin-row blocks of the current state (buffer 0).
+template <typename T>
+__global__ void wet_blocks_kernel(StripView S, double eps, unsigned char* out) {
+  const int bx = blockIdx.x, by = blockIdx.y, t = threadIdx.x;
+  const int col = bx * FUSED_TX + t;
+  const T* H = reinterpret_cast<const T*>(S.H[0]);
+  bool wet = false;
+  if (t < FUSED_TX && col < S.nx) {
+    const int j1 = min(S.ny, (by + 1) * kTyMin);
+    for (int j = by * kTyMin; j < j1; ++j) wet |= (double)H[off(S.pitch, col, j)] > eps;
+  }
+  wet = __syncthreads_or(wet);
+  if (t == 0) out[by * gridDim.x + bx] = wet ? 1 : 0;
+}
+
+}  // namespace
 
 // ---------------------------------------------------------------- C-ABI
 
@@ -1184,6 +1204,43 @@ static int upload_rows(csph* H, Strip& s, int j_begin, int j_end, const double* 
   return CSPH_OK;
 }
 
+// Tile rows from the state: with HGS only tiles holding water do real work,
+// so the tiling must give enough of them to fill the GPU -- the largest ty in 128..16 whose
+// wet tiles make 2.5 waves of 3 resident CTAs per SM -- while keeping the launch of the
+// skipped ones cheap (at most 40 K tiles in all).  Measured on one B200: C3 4096^2 -> 32 rows
+// (+22 % over 128), C4 8192^2 -> 64 (+9 %), C5 16384^2 -> 128.
+static int choose_tile_rows(csph* H, Strip& s) {
+  const int nby = (s.v.ny + kTyMin - 1) / kTyMin;
+  dim3 grd((unsigned)s.ntx, (unsigned)nby);
+  if (s.v.prec == 4)
+    wet_blocks_kernel<float><<<grd, 128, 0, s.st>>>(s.v, H->P.eps, s.wetblk);
+  else
+    wet_blocks_kernel<double><<<grd, 128, 0, s.st>>>(s.v, H->P.eps, s.wetblk);
+  H->launches += 1;
+  CK(cudaGetLastError());
+  std::vector<unsigned char> w((size_t)s.ntx * nby);
+  CK(cudaMemcpyAsync(w.data(), s.wetblk, w.size(), cudaMemcpyDeviceToHost, s.st));
+  CK(cudaStreamSynchronize(s.st));
+  const long long want = 5LL * 3 * s.nsm / 2;
+  int pick = 0;
+  for (int ty = 128; ty >= kTyMin; ty /= 2) {
+    const int f = ty / kTyMin, nty = (s.v.ny + ty - 1) / ty;
+    if ((long long)nty * s.ntx > 40000) break;  // finer tilings only add skipped-CTA overhead
+    long long wet = 0;
+    for (int r = 0; r < nty; ++r)
+      for (int q = 0; q < s.ntx; ++q) {
+        bool any = false;
+        for (int k = r * f; k < (r + 1) * f && k < nby && !any; ++k) any = w[(size_t)k * s.ntx + q];
+        wet += any;
+      }
+    pick = ty;
+    if (wet >= want) break;
+  }
+  s.ty = pick ? pick : 128;
+  s.nty = (s.v.ny + s.ty - 1) / s.ty;
+  return CSPH_OK;
+}
+
 int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, const double* hu,
                         const double* hv, const double* b, const double* psi) {
   if (!H || !h || !hu || !hv || !b) return fail(CSPH_EINVAL, "NULL argument");
@@ -1194,10 +1251,11 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
   for (auto& s : H->s) {
     CK(cudaSetDevice(s.dev));
     if ((st = upload_rows(H, s, j_begin, j_end, h, hu, hv, b, psi))) return st;
+    if (s.auto_ty && H->p.path == CSPH_PATH_FUSED && (st = choose_tile_rows(H, s))) return st;
     init_ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
     CK(cudaMemsetAsync(s.gM, 0, 4 * sizeof(unsigned long long), s.st));
-    CK(cudaMemsetAsync(s.tflag, HGS_ALL, 2 * (size_t)s.ntx * s.nty, s.st));  // all tiles active
-    CK(cudaMemsetAsync(s.tstate, 0, (size_t)s.ntx * s.nty, s.st));
+    CK(cudaMemsetAsync(s.tflag, HGS_ALL, 2 * s.tflag_cap, s.st));  // all tiles active
+    CK(cudaMemsetAsync(s.tstate, 0, s.tflag_cap, s.st));
     CK(cudaMemsetAsync(s.hstats, 0, 4 * sizeof(unsigned long long), s.st));
     // walls: ghosts of buffer 0 (W is read only on owned cells: no ghosts needed)
     launch_mirror(s.v, s.ctrl, 0, s.st, &H->launches);

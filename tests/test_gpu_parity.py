@@ -270,3 +270,21 @@ def test_cuda_graph_replay_is_exact(cs, monkeypatch):
     assert np.array_equal(dt_ref, a0[0])
     for x, y in zip(ref.get_state(), a0[1]):
         assert np.array_equal(x, y)
+
+
+def test_tilings_are_bitwise_identical(cs):
+    """The CTA tile height (= HGS tile) is a pure performance parameter: the automatic
+    state-driven choice and fixed 16..128-row tilings give the same dt log and state."""
+    c = synth.config("C3", 700, 600)
+    f = synth.fill(c)
+    out = []
+    for ty in (0, 16, 32, 64, 128):
+        g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, tile_rows=ty))
+        g.set_state(*f)
+        g.step(60)
+        out.append((g.get_dt_log(60)[0], g.get_state()))
+        g.destroy()
+    for dt, st in out[1:]:
+        assert np.array_equal(dt, out[0][0])
+        for a, b in zip(st, out[0][1]):
+            assert np.array_equal(a, b)
