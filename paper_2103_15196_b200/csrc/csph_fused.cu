@@ -97,6 +97,9 @@ struct Smem {
   alignas(8) unsigned long long bar[D];
   unsigned long long red[3][NT / 32];
   unsigned wm[NT / 32];
+#ifdef CSPH_SMEM_EXTRA
+  char pad_[CSPH_SMEM_EXTRA];  // development knob: occupancy experiments
+#endif
 };
 
 enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
@@ -660,7 +663,12 @@ void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long
   const int TY = tile_rows > 0 ? tile_rows : 128;
   // 128 threads (120 output columns), an 8-row TMA ring prefetching 3 rows ahead,
   // 3 resident CTAs per SM in fp64 (4 in fp32)
-  launch_v<128, 8, 3, 3>(S, C, P, gM, row0, row1, TY, hg, st);
+#ifndef CSPH_RING
+#define CSPH_RING 8   // development knobs: ring slots, prefetch distance, CTAs per SM
+#define CSPH_PF 3
+#define CSPH_MINB 3
+#endif
+  launch_v<128, CSPH_RING, CSPH_PF, CSPH_MINB>(S, C, P, gM, row0, row1, TY, hg, st);
   *nlaunch += 1;
 }
 

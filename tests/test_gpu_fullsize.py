@@ -146,3 +146,32 @@ def test_C5_full_size_hgs_and_conservation(cs):
     # change only by rounding (268 M cells, 12 steps)
     assert abs(vol - vol0) <= 1e-11 * vol0
     assert abs(sed - sed0) <= 1e-11 * abs(sed0)
+
+
+def test_C5_full_size_long_run(cs):
+    """The bench workload over 400 steps (about 13 s of simulated flood): no error status,
+    positive finite tau every step, volume and Sum (1 - psi) b kept to rounding, no depth
+    below -neg_tol, no NaN."""
+    c = synth.config("C5")
+    f = synth.fill(c)
+    W = 1.0 / (1.0 - f[4])
+    vol0 = float(np.sum(f[0]))
+    sed0 = float(np.sum(f[3] / W))
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params))
+    g.set_state(*f)
+    del f
+    assert g.step(400) == 0
+    dt, lim = g.get_dt_log(400)
+    assert len(dt) == 400 and np.all(np.isfinite(dt)) and np.all(dt > 0)
+    t, n, _ = g.get_time()
+    assert n == 400 and t == pytest.approx(float(np.sum(dt)), rel=1e-12)
+    vol = sed = 0.0
+    for j0 in range(0, c.ny, 2048):
+        h, hu, hv, b = g.get_state_rows(j0, j0 + 2048)
+        assert np.all(np.isfinite(h)) and np.all(np.isfinite(hu)) and np.all(np.isfinite(b))
+        assert h.min() >= -1e-12
+        vol += float(np.sum(h))
+        sed += float(np.sum(b / W[j0:j0 + 2048]))
+    g.destroy()
+    assert abs(vol - vol0) <= 1e-10 * vol0
+    assert abs(sed - sed0) <= 1e-10 * abs(sed0)
