@@ -115,6 +115,7 @@ struct Strip {
   bool auto_ty = false;              // ty chosen from the state at set_state
   size_t tflag_cap = 0;              // tiles the flag buffers hold (finest tiling)
   unsigned char* wetblk = nullptr;   // auto_ty: wet flags of 120 x 16 blocks [ny/16][ntx]
+  unsigned char* gflag = nullptr;    // neighbours' facing tile-row flags [2 parity][2 side][ntx]
   int nsm = 148;
   unsigned char* tstate = nullptr;   // HGS identity-copy counters [ntiles]
   unsigned long long* hstats = nullptr;  // HGS tile counters: marched, copied, skipped
@@ -576,6 +577,8 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
     const size_t nt = (size_t)s.ntx * ((v.ny + tymin - 1) / tymin);
     if ((st = dalloc(s, (void**)&s.tflag, 2 * nt))) return st;
     if ((st = dalloc(s, (void**)&s.tstate, nt))) return st;
+    if ((st = dalloc(s, (void**)&s.gflag, 4 * (size_t)s.ntx))) return st;
+    CK(cudaMemset(s.gflag, HGS_ALL, 4 * (size_t)s.ntx));
     s.tflag_cap = nt;
     CK(cudaMemset(s.tflag, HGS_ALL, 2 * nt));
     CK(cudaMemset(s.tstate, 0, nt));
@@ -1012,7 +1015,21 @@ static int halo_nccl(csph* H, int q, cudaStream_t stream) {
   const ncclDataType_t dt = v.prec == 4 ? ncclFloat32 : ncclFloat64;
   char* f[4] = {(char*)v.H[q], (char*)v.Qx[q], (char*)v.Qy[q], (char*)v.b[q]};
   if (H->nranks == 1) return CSPH_OK;
+  // tile-row flags of the new state (parity q): my first row goes to r-1 (its ghi), my
+  // last to r+1 (its glo)
+  const size_t nt = (size_t)s.ntx * s.nty;
+  unsigned char* fq = s.tflag + nt * (size_t)q;
+  unsigned char* gq = s.gflag + 2 * (size_t)s.ntx * (size_t)q;
   NK(g_nccl.GroupStart());
+  if (H->rank > 0) {
+    NK(g_nccl.Send(fq, s.ntx, ncclUint8, H->rank - 1, H->comm, stream));
+    NK(g_nccl.Recv(gq, s.ntx, ncclUint8, H->rank - 1, H->comm, stream));
+  }
+  if (H->rank < H->nranks - 1) {
+    NK(g_nccl.Send(fq + (size_t)(s.nty - 1) * s.ntx, s.ntx, ncclUint8, H->rank + 1, H->comm,
+                   stream));
+    NK(g_nccl.Recv(gq + s.ntx, s.ntx, ncclUint8, H->rank + 1, H->comm, stream));
+  }
   for (int k = 0; k < 4; ++k) {
     if (H->rank > 0) {
       NK(g_nccl.Send(f[k] + es * off(v.pitch, -GX, 0), cnt, dt, H->rank - 1, H->comm, stream));
@@ -1071,6 +1088,7 @@ static int exchange(csph* H, int q) {
       const size_t es = (size_t)v.prec;
       const size_t bytes = (size_t)GY * v.pitch * es;
       char* f[4] = {(char*)v.H[q], (char*)v.Qx[q], (char*)v.Qy[q], (char*)v.b[q]};
+      unsigned char* gq = s.gflag + 2 * (size_t)s.ntx * (size_t)q;
       if (r > 0) {
         const Strip& o = H->s[r - 1];
         const char* g[4] = {(const char*)o.v.H[q], (const char*)o.v.Qx[q], (const char*)o.v.Qy[q],
@@ -1078,6 +1096,9 @@ static int exchange(csph* H, int q) {
         for (int k = 0; k < 4; ++k)
           CK(cudaMemcpyPeerAsync(f[k] + es * off(v.pitch, -GX, -GY), s.dev,
                                  g[k] + es * off(o.v.pitch, -GX, o.v.ny - GY), o.dev, bytes, s.st));
+        // the neighbour's last tile row of flags (parity q) -> my glo
+        const unsigned char* of = o.tflag + (size_t)o.ntx * o.nty * q + (size_t)(o.nty - 1) * o.ntx;
+        CK(cudaMemcpyPeerAsync(gq, s.dev, of, o.dev, (size_t)s.ntx, s.st));
       }
       if (r < n - 1) {
         const Strip& o = H->s[r + 1];
@@ -1086,6 +1107,8 @@ static int exchange(csph* H, int q) {
         for (int k = 0; k < 4; ++k)
           CK(cudaMemcpyPeerAsync(f[k] + es * off(v.pitch, -GX, v.ny), s.dev,
                                  g[k] + es * off(o.v.pitch, -GX, 0), o.dev, bytes, s.st));
+        const unsigned char* of = o.tflag + (size_t)o.ntx * o.nty * q;  // its first tile row
+        CK(cudaMemcpyPeerAsync(gq + s.ntx, s.dev, of, o.dev, (size_t)s.ntx, s.st));
       }
     }
     // every strip must finish reading its neighbours before they run ahead
@@ -1256,6 +1279,7 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
     CK(cudaMemsetAsync(s.gM, 0, 4 * sizeof(unsigned long long), s.st));
     CK(cudaMemsetAsync(s.tflag, HGS_ALL, 2 * s.tflag_cap, s.st));  // all tiles active
     CK(cudaMemsetAsync(s.tstate, 0, s.tflag_cap, s.st));
+    CK(cudaMemsetAsync(s.gflag, HGS_ALL, 4 * (size_t)s.ntx, s.st));
     CK(cudaMemsetAsync(s.hstats, 0, 4 * sizeof(unsigned long long), s.st));
     // walls: ghosts of buffer 0 (W is read only on owned cells: no ghosts needed)
     launch_mirror(s.v, s.ctrl, 0, s.st, &H->launches);
@@ -1386,6 +1410,10 @@ static Hgs hgs_of(const csph* H, const Strip& s) {
   h.fprev = s.tflag + nt * (size_t)H->host_parity;
   h.fnext = s.tflag + nt * (size_t)(H->host_parity ^ 1);
   h.tstate = s.tstate;
+  // ghost flags of parity host_parity, written by the previous step's exchange
+  const unsigned char* g = s.gflag + 2 * (size_t)s.ntx * (size_t)H->host_parity;
+  h.glo = s.v.wall_lo ? nullptr : g;
+  h.ghi = s.v.wall_hi ? nullptr : g + s.ntx;
   h.ntx = s.ntx;
   h.nty = s.nty;
   h.enable = H->p.hgs != 0 && H->p.path == CSPH_PATH_FUSED;

@@ -187,11 +187,14 @@ __global__ void __launch_bounds__(NT, MINB)
   // bands of its 4 edge neighbours was wet after the previous step (band-mask flags). ----
   const int tr = y0 / TY;
   const int ti = tr * hg.ntx + (int)blockIdx.x;
-  // a tile whose boundary row faces an interior strip edge reads halo rows of another strip,
-  // whose wetness the flags do not record: it always marches
-  if (hg.enable && (S.wall_lo || y0 > 0) && (S.wall_hi || y1 < S.ny)) {
+  // across an interior strip edge the facing tile row is the neighbouring strip's, whose
+  // flags arrive with the halo rows (hg.glo / hg.ghi); without them such a tile marches
+  if (hg.enable && (S.wall_lo || y0 > 0 || hg.glo) && (S.wall_hi || y1 < S.ny || hg.ghi)) {
     auto fl = [&](int r, int q) -> unsigned {
-      return (r >= 0 && r < hg.nty && q >= 0 && q < hg.ntx) ? hg.fprev[r * hg.ntx + q] : 0u;
+      if (q < 0 || q >= hg.ntx) return 0u;
+      if (r < 0) return hg.glo ? hg.glo[q] : 0u;          // a wall brings no water
+      if (r >= hg.nty) return hg.ghi ? hg.ghi[q] : 0u;
+      return hg.fprev[r * hg.ntx + q];
     };
     const int q0 = (int)blockIdx.x;
     const bool dry = !(fl(tr, q0) & HGS_ANY) && !(fl(tr - 1, q0) & HGS_BOT) &&

@@ -27,6 +27,10 @@ enum : unsigned { HGS_ANY = 1, HGS_TOP = 2, HGS_BOT = 4, HGS_LEFT = 8, HGS_RIGHT
 struct Hgs {
   const unsigned char* fprev;
   unsigned char* fnext;
+  // flags of the facing tile row of the neighbouring strips (previous step), [ntx] each;
+  // nullptr on a global edge.  Filled by the halo exchange with the halo rows.
+  const unsigned char* glo;
+  const unsigned char* ghi;
   unsigned char* tstate;
   int ntx, nty;
   int enable;

@@ -122,3 +122,33 @@ def test_dist_split_launches(cs, tile_rows):
         assert np.array_equal(a, r)
     assert g.last_launch_count() == 40 * (2 + (3 if c.ny > 2 * tile_rows else 2))
     g.destroy()
+
+
+@pytest.mark.parametrize("nstrips", [2, 4])
+def test_front_crosses_strip_edges_hgs(cs, nstrips):
+    """HGS across strip edges (ghost tile flags): a dam-break front starts
+    in the first strip and runs into dry strips whose edge tiles were being skipped; with
+    16-row tiles and uneven strips the result is bitwise the single grid without HGS."""
+    nx, ny = 150, 180
+    jj, ii = np.mgrid[0:ny, 0:nx]
+    h = np.where(jj < 30, 1.5, 0.0)
+    b = 0.4 - 0.002 * jj + 0.01 * np.sin(0.2 * ii)  # downhill, away from the dam
+    z = np.zeros((ny, nx))
+    f = (h, z.copy(), z.copy(), b, np.full((ny, nx), 0.4))
+    phys = dict(n_manning=0.02, A_J=1e-3, C_J=2.0, C_Sh=4.0, d50=1e-3)
+    steps = 500
+    g = cs.csph_create(nx, ny, 1.0, cs.params_from(phys, hgs=0))
+    g.set_state(*f)
+    g.step(steps)
+    dt0, ref = g.get_dt_log(steps)[0], g.get_state()
+    g.destroy()
+    bounds = [0, 37, 70, 131, 180] if nstrips == 4 else [0, 41, 180]
+    g = cs.csph_create_multi_rows(nx, ny, 1.0, cs.params_from(phys, tile_rows=16),
+                                  [0] * nstrips, bounds)
+    g.set_state(*f)
+    g.step(steps)
+    assert np.array_equal(g.get_dt_log(steps)[0], dt0)
+    for a, r in zip(g.get_state(), ref):
+        assert np.array_equal(a, r)
+    assert ref[0][76:].max() > 0  # the front crossed the strip edges at rows 37/41 and 70
+    g.destroy()
