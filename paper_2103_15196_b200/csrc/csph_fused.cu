@@ -91,7 +91,7 @@ struct Smem {
   alignas(128) T ring[D][NF][RW];
   T U[2][XW];      // u of the last two rows (div)
   T PE[XW];        // K2 x-face force (t|t+1), row L
-  T X2[5][XW];     // row L-1: H_half, u~, v~, J0x, |J0|
+  T X2[2][5][XW];  // K4 outputs by row parity: H_half, u~, v~, J0x, |J0|
   T X3[5][XW];     // row L-1: K5 x-face force, sigma_x (eta, H, u~, v~)
   T X4[4][XW];     // row L-1: x-face fluxes (t|t+1): F^H, F^Qx, F^Qy, F^J
   alignas(8) unsigned long long bar[D];
@@ -293,11 +293,10 @@ __global__ void __launch_bounds__(NT, MINB)
   // ---- carried registers (row offsets relative to the newest row L) ----
   // Depth-1 carries are overwritten in place right after their last use, so the
   // register allocator needs no moves for them.
-  T v1 = 0, v2 = 0;          // v(L-1), v(L-2)
-  T r1 = 0;                  // r(L-1)
+  T vm1 = 0;                 // v(L-1)
   T gam1 = 0, gam2 = 0;      // gamma(L-1), gamma(L-2)
-  T PS = 0;                  // K2 y-face force (L-2|L-1)
-  T phix1 = 0;               // Phi_x(L-1)
+  T PS = 0;                  // K2 y-face force (L-1|L)
+  T Hh1 = 0, ut1 = 0, vt1 = 0, J0x1 = 0, J0y1 = 0, J0a1 = 0;  // K4 outputs of row L-1
   T Hh2 = 0;                 // H_half(L-2)
   T PhS = 0;                 // K5 y-face force (L-3|L-2)
   T phx2h = 0;               // Phi_half_x(L-2)
@@ -406,18 +405,24 @@ __global__ void __launch_bounds__(NT, MINB)
     };
     const int j = L - 3;  // row updated in this iteration
     T Gn[4] = {T(0), T(0), T(0), T(0)};  // (G^H, G^Qx, G^Qy, G^J) at (L-3|L-2)
+    T* const X2w = &sm.X2[k & 1][0][0];         // K4 outputs of row L (written in phase D)
+    const T* const X2r = &sm.X2[(k - 1) & 1][0][0];  // K4 outputs of row L-1 (read)
+#define X2(q, dt) X2r[(q) * SM::XW + (t) + 1 + (dt)]
     if (cta_dry) {
       // Dry fast path (exact): every quantity of R on rows L-4..L is either 0 or the
       // identity, so only the carried window and the row L-3 update run.
-      const T H1 = RG(F_H, km1, 0);
-      phix1 = T(0);
-      v2 = v1; v1 = T(0);
-      r1 = T(0);
+      const T H0 = RG(F_H, k, 0);
       gam2 = gam1; gam1 = T(0);
-      Hh2 = H1;
+      Hh2 = Hh1;
       phx2h = T(0);
-      ut3 = ut2; vt3 = vt2; ut2 = T(0); vt2 = T(0);
-      J0y3 = J0y2; J0a3 = J0a2; J0y2 = T(0); J0a2 = T(0);
+      ut3 = ut2; vt3 = vt2; ut2 = ut1; vt2 = vt1;
+      J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = J0a1;
+      // K4 of the dry row L: H_half = H, u~ = v~ = 0, J0 = 0
+      Hh1 = H0; ut1 = T(0); vt1 = T(0); J0x1 = T(0); J0y1 = T(0); J0a1 = T(0);
+      vm1 = T(0);
+      X2w[0 * SM::XW + t + 1] = H0;
+#pragma unroll
+      for (int q = 1; q < 5; ++q) X2w[q * SM::XW + t + 1] = T(0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = T(0);
       if (col_out && j >= y0 && j < y1) {
@@ -445,44 +450,19 @@ __global__ void __launch_bounds__(NT, MINB)
     const T H1 = RG(F_H, km1, 0), b1 = RG(F_B, km1, 0);
     const bool w1 = H1 > Q.eps;
     const T eta1 = H1 + b1;
-    const bool w0 = aw0;
-    const T PE0 = aPE0, v0 = av0, r0 = ar0, gam0 = agam0, phiy1 = aphiy1;
     __syncthreads();  // ---------------------------------------------------- barrier 1
     {
-      // ================= phase B: K4 predictor + J0 (row L-1) =================
-      const T phix0 = w0 ? -(PE0 + XG(sm.PE, -1)) : T(0);
-      T Hh1 = H1, ut1 = T(0), vt1 = T(0);
-      if (ANYW(w1)) {
-        const T* Up = sm.U[(k - 1) & 1];
-        T div = ((XG(Up, 1) - XG(Up, -1)) + (v0 - v2)) * Q.inv_2h;
-        const T hh = H1 * (T(1) - theta * div);
-        const T f = FRIC ? rcp_t(T(1) + theta * gam1) : T(1);  // gam1 = 0 when dry
-        const T uu = ((RG(F_QX, km1, 0) + theta * phix1) * f) * r1;
-        const T vv = ((RG(F_QY, km1, 0) + theta * phiy1) * f) * r1;
-        Hh1 = w1 ? hh : H1; ut1 = w1 ? uu : T(0); vt1 = w1 ? vv : T(0);
-      }
-      phix1 = phix0;
-      v2 = v1; v1 = v0;
-      r1 = r0;
-      T J0x1 = T(0), J0y1 = T(0), J0a1 = T(0);
-      if (TRANSP)
-        grass_t<GEN>(Q, ut1, vt1, H1, aj_at(off(pitch, col, L - 1), H1),
-                         J0x1, J0y1, J0a1);
+      // ====== phase C: Phi_x (row L), Delta F_x (row L-2), K5 + sigma_x (row L-1),
+      //        K6 (row L-2), y-face (L-3|L-2) ======
+      const T phix0 = aw0 ? -(aPE0 + XG(sm.PE, -1)) : T(0);
       // Delta F_x of row L-2 from the own face (t|t+1) and the west face (t-1|t)
       T dF2[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) dF2[q] = XG(sm.X4[q], 0) - XG(sm.X4[q], -1);
-      XG(sm.X2[0], 0) = Hh1;
-      XG(sm.X2[1], 0) = ut1;
-      XG(sm.X2[2], 0) = vt1;
-      XG(sm.X2[3], 0) = J0x1;
-      XG(sm.X2[4], 0) = J0a1;
-      __syncthreads();  // -------------------------------------------------- barrier 2
-      // ============ phase C: K5, sigma_x (row L-1), K6 (row L-2), y-face (L-3|L-2) ====
       T PhE1;
       {
         const T bR = RG(F_B, km1, 1);
-        PhE1 = face_force_t(Q.cPh, Hh1 + b1, b1, XG(sm.X2[0], 1) + bR, bR);
+        PhE1 = face_force_t(Q.cPh, Hh1 + b1, b1, X2(0, 1) + bR, bR);
       }
       T sx1[4];
       {
@@ -490,8 +470,8 @@ __global__ void __launch_bounds__(NT, MINB)
         const T eL = HLm + RG(F_B, km1, -1), eR = HRp + RG(F_B, km1, 1);
         sx1[0] = minmod_t(eta1 - eL, eR - eta1);
         sx1[1] = minmod_t(H1 - HLm, HRp - H1);
-        sx1[2] = minmod_t(ut1 - XG(sm.X2[1], -1), XG(sm.X2[1], 1) - ut1);
-        sx1[3] = minmod_t(vt1 - XG(sm.X2[2], -1), XG(sm.X2[2], 1) - vt1);
+        sx1[2] = minmod_t(ut1 - X2(1, -1), X2(1, 1) - ut1);
+        sx1[3] = minmod_t(vt1 - X2(2, -1), X2(2, 1) - vt1);
       }
       const T H2 = RG(F_H, km2, 0), b2 = RG(F_B, km2, 0);
       const bool w2 = H2 > Q.eps;
@@ -506,7 +486,6 @@ __global__ void __launch_bounds__(NT, MINB)
       }
       PhS = PhN2;
       Hh2 = Hh1;
-      gam2 = gam1; gam1 = gam0;
       // y-face (L-3|L-2): sigma_y of row L-2 (always: it is carried), HLL, sediment
       const T H3 = RG(F_H, km3, 0), b3 = RG(F_B, km3, 0);
       const bool w3 = H3 > Q.eps;
@@ -533,8 +512,9 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
       for (int q = 0; q < 4; ++q) XG(sm.X3[1 + q], 0) = sx1[q];
       next_hist();
-      const bool dry_next = __syncthreads_and(hist == 0u);  // ---------------- barrier 3
-      // ====== phase D: Phi_half_x (row L-1), x-face flux (row L-1) ======
+      const bool dry_next = __syncthreads_and(hist == 0u);  // ---------------- barrier 2
+      // ====== phase D: Phi_half_x + x-face flux (row L-1), phase A (row L+1), K4 + J0
+      //        (row L), K8 (row L-3) ======
       phx2h = w1 ? -(PhE1 + XG(sm.X3[0], -1)) : T(0);
       T Fn[4] = {T(0), T(0), T(0), T(0)};
       {
@@ -543,21 +523,47 @@ __global__ void __launch_bounds__(NT, MINB)
         if (ANYW(any)) {
           const T bR = RG(F_B, km1, 1);
           const T eR = HR + bR;
-          const T uR = XG(sm.X2[1], 1), vR = XG(sm.X2[2], 1);
+          const T uR = X2(1, 1), vR = X2(2, 1);
           hll_bf(Q.g, fma(T(0.5), sx1[0], eta1), fma(T(0.5), sx1[1], H1), fma(T(0.5), sx1[2], ut1),
                    fma(T(0.5), sx1[3], vt1), fma(T(-0.5), XG(sm.X3[1], 1), eR), fma(T(-0.5), XG(sm.X3[2], 1), HR),
                    fma(T(-0.5), XG(sm.X3[3], 1), uR), fma(T(-0.5), XG(sm.X3[4], 1), vR), !any,
                    Fn[0], Fn[1], Fn[2]);  // normal momentum of an x-face -> Qx, tangential -> Qy
-          Fn[3] = (any && TRANSP) ? sed_face_t(Q, ut1, uR, J0x1, XG(sm.X2[3], 1), J0a1,
-                                                  XG(sm.X2[4], 1), b1, bR)
+          Fn[3] = (any && TRANSP) ? sed_face_t(Q, ut1, uR, J0x1, X2(3, 1), J0a1, X2(4, 1), b1, bR)
                                        : T(0);
         }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = Fn[q];
       // phase A of the next row, unconditionally (a wasted row at a wet -> dry change;
-      // beyond the last row it reads a stale but finite ring slot and feeds nothing)
+      // beyond the last row it reads a stale but finite ring slot and feeds nothing);
+      // the row-L values it replaces are kept for K4
+      const bool w0 = aw0;
+      const T r0 = ar0, gam0 = agam0, v0 = av0;
       phaseA(k + 1);
+      // ---- K4 predictor + J0 of row L (its x-neighbours' u and Phi_x: barrier 1) ----
+      {
+        const T H0 = RG(F_H, k, 0);
+        T Hh = H0, ut = T(0), vt = T(0);
+        if (ANYW(w0)) {
+          const T* Uc = sm.U[k & 1];
+          T div = ((XG(Uc, 1) - XG(Uc, -1)) + (av0 - vm1)) * Q.inv_2h;
+          const T hh = H0 * (T(1) - theta * div);
+          const T f = FRIC ? rcp_t(T(1) + theta * gam0) : T(1);  // gam0 = 0 when dry
+          const T uu = ((RG(F_QX, k, 0) + theta * phix0) * f) * r0;
+          const T vv = ((RG(F_QY, k, 0) + theta * aphiy1) * f) * r0;
+          Hh = w0 ? hh : H0; ut = w0 ? uu : T(0); vt = w0 ? vv : T(0);
+        }
+        T jx = T(0), jy = T(0), ja = T(0);
+        if (TRANSP) grass_t<GEN>(Q, ut, vt, H0, aj_at(off(pitch, col, L), H0), jx, jy, ja);
+        X2w[0 * SM::XW + t + 1] = Hh;
+        X2w[1 * SM::XW + t + 1] = ut;
+        X2w[2 * SM::XW + t + 1] = vt;
+        X2w[3 * SM::XW + t + 1] = jx;
+        X2w[4 * SM::XW + t + 1] = ja;
+        Hh1 = Hh; ut1 = ut; vt1 = vt; J0x1 = jx; J0y1 = jy; J0a1 = ja;
+        vm1 = v0;
+        gam2 = gam1; gam1 = gam0;
+      }
       // ---- K8 update of row L-3 ----
       if (col_out && j >= y0 && j < y1) {
         const T W3 = HASW ? RG(F_W, km3, 0) : T(S.Wc);
@@ -577,6 +583,7 @@ __global__ void __launch_bounds__(NT, MINB)
       for (int q = 0; q < 4; ++q) { dF3[q] = dF2[q]; Gs[q] = Gn[q]; }
       cta_dry = dry_next;
     }
+#undef X2
   }
 #undef RG
 #undef XG
