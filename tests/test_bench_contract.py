@@ -1,9 +1,11 @@
-"""bench.py's reference arm (the oracle, timed on the host) prints the contract's JSON line
-on CPU; the GPU arm is exercised by the driver on the B200."""
+"""bench.py's JSON line: the reference arm (the oracle, timed on the host) on CPU, and the
+GPU arm on a small grid (-m gpu)."""
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -24,3 +26,26 @@ def test_reference_arm_json_line():
     assert d["value"] > 0 and d["unit"] == "Gcell-updates/s" and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_line():
+    """bench.py's own arm on a small grid: the keys the driver reads, a roofline object for
+    the fused kernel, the clock sample, e2e through the C-ABI with host buffers, the oracle's
+    CPU baseline and a kernel-launch count."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C2", "--n",
+                        "1024", "--steps", "5", "--warmup", "3", "--cpu-crop", "96",
+                        "--cpu-steps", "2", "--e2e-steps", "5"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.strip()][-1])
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["value"] > 0
+    assert d["dtype"] == "f64" and d["scaling"] == "strong" and d["higher_is_better"] is True
+    ro = d["roofline"]
+    assert ro["bound"] == "hbm" and ro["unit"] == "GB/s" and 0 < ro["frac"] < 1
+    assert abs(ro["frac"] - ro["achieved"] / ro["peak"]) < 1e-9
+    assert d["gpu_launches"] >= 5 * 3  # clear flags + fused + ctrl per step
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
