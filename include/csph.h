@@ -62,7 +62,9 @@ typedef struct {
   double d50;        /* Eq.5 median grain size [m] (> 0 when C_Sh > 0) */
   double q_plus;     /* Eq.1 deposition source [m/s], default 0 */
   double q_minus;    /* Eq.1 erosion drain [m/s], default 0 */
-  int    precision;  /* 64 (fp64; the only mode of this build) */
+  int    precision;  /* 64 (default, fp64: the hot path, bitwise = the oracle) or 32 (NEXT-2
+                        fp32 state and arithmetic, fused path, walls, m = 2, constant A_J;
+                        DESIGN.md 3.14) */
   int    device;     /* CUDA ordinal for csph_create (single-process use) */
   int    path;       /* CSPH_PATH_FUSED (default) or CSPH_PATH_STAGED */
   int    tile_rows;  /* fused path: rows marched per CTA (0 = auto: 128, halved down to 16
@@ -114,7 +116,9 @@ int         csph_set_fields_rows(csph_t*, int j_begin, int j_end, const double* 
 
 /* Advance exactly nsteps CSPH-TVD steps, each with its own Eq.7 tau computed
  * on the device.  No host synchronisation inside the call except one status
- * readback at its end.  On CSPH_ENEGDEPTH/ENONFINITE/EDRY the steps up to the
+ * readback at its end.  A single-grid handle replays pairs of steps from CUDA
+ * graphs (captured on first use, rebuilt after set_state / set_fields;
+ * environment CSPH_NO_GRAPHS=1 disables them).  On CSPH_ENEGDEPTH/ENONFINITE/EDRY the steps up to the
  * failing one are done (see csph_get_time) and later calls return the same code. */
 int         csph_step(csph_t*, int nsteps);
 
@@ -199,7 +203,8 @@ int         csph_get_profile(csph_t*, double* main_kernel_ms, long long* steps_t
 /* HGS tile counters of the fused path since csph_set_state (or the last reset):
  * counts[0] tiles marched, counts[1] tiles updated by an identity copy (dry
  * neighbourhood), counts[2] tiles skipped (dry and already identical in both
- * state buffers).  A tile is the 120 x tile_rows chunk one CTA owns. */
+ * state buffers).  A tile is the 120-column x TY-row chunk one CTA owns (TY =
+ * params.tile_rows, or chosen from the state at set_state). */
 int         csph_get_tile_stats(csph_t*, long long counts[3]);
 int         csph_reset_tile_stats(csph_t*);
 
