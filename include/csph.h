@@ -67,8 +67,10 @@ typedef struct {
                         DESIGN.md 3.14) */
   int    device;     /* CUDA ordinal for csph_create (single-process use) */
   int    path;       /* CSPH_PATH_FUSED (default) or CSPH_PATH_STAGED */
-  int    tile_rows;  /* fused path: rows marched per CTA (0 = auto: 128, halved down to 16
-                        until the grid holds 4 waves of 3 resident CTAs per SM) */
+  int    tile_rows;  /* fused path: rows marched per CTA (= HGS tile height); 0 = auto:
+                        at every set_state the largest of 128/64/32/16 whose wet tiles fill
+                        2.5 waves of 3 resident CTAs per SM.  A pure
+                        performance parameter: results are bitwise identical for any value */
   int    hgs;        /* 1 (default): skip tiles whose neighbourhood is dry (the paper's
                         HGS; exact); 0: march every tile */
   int    aj_mode;    /* 0 (default): constant A_J; 1: Eq.4
