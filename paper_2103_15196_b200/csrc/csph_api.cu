@@ -1131,22 +1131,31 @@ static int exchange(csph* H, int q) {
 // outside [0,1)); bit 3 = psi is not uniform over this strip's rows.
 __global__ void validate_kernel(StripView S, int jlo, int jhi, const double* psi, double psi0,
                                 int* flags, int buf) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  int j = jlo + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+  // grid-stride over rows, flags accumulated per thread, one atomicOr per block (a per-warp
+  // atomic on one word serialises: with a psi field every warp sets bit 3)
+  __shared__ int bf;
+  if (threadIdx.x == 0 && threadIdx.y == 0) bf = 0;
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   int f = 0;
-  if (i < S.nx && j < jhi) {
-    size_t c = off(S.pitch, i, j);
-    double H = S.H[buf][c], qx = S.Qx[buf][c], qy = S.Qy[buf][c], b = S.b[buf][c];
-    if (!isfinite(H) || !isfinite(qx) || !isfinite(qy) || !isfinite(b)) f |= 1;
-    if (H < 0.0) f |= 2;
-    if (psi) {
-      double p = psi[c];
-      if (!(p >= 0.0 && p < 1.0)) f |= 4;
-      if (p != psi0) f |= 8;
+  if (i < S.nx) {
+    for (int j = jlo + (int)(blockIdx.y * blockDim.y + threadIdx.y); j < jhi;
+         j += (int)(gridDim.y * blockDim.y)) {
+      const size_t c = off(S.pitch, i, j);
+      const double H = S.H[buf][c], qx = S.Qx[buf][c], qy = S.Qy[buf][c], b = S.b[buf][c];
+      if (!isfinite(H) || !isfinite(qx) || !isfinite(qy) || !isfinite(b)) f |= 1;
+      if (H < 0.0) f |= 2;
+      if (psi) {
+        const double p = psi[c];
+        if (!(p >= 0.0 && p < 1.0)) f |= 4;
+        if (p != psi0) f |= 8;
+      }
     }
   }
   f = __reduce_or_sync(0xffffffffu, f);
-  if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+  if (f && (threadIdx.x & 31) == 0) atomicOr(&bf, f);
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0 && bf) atomicOr(flags, bf);
 }
 
 static double* src_dst0(const StripView& v, int k) {
@@ -1189,7 +1198,9 @@ static int upload_rows(csph* H, Strip& s, int j_begin, int j_end, const double* 
   }
   CK(cudaMemsetAsync(s.dflags, 0, sizeof(int), s.st));
   {
-    dim3 blk(32, 8), grd((nx + 31) / 32, (hi - lo + 7) / 8);
+    const int bx = (nx + 31) / 32;
+    const int by = std::max(1, std::min((hi - lo + 7) / 8, (8 * 148 + bx - 1) / bx));
+    dim3 blk(32, 8), grd(bx, by);
     validate_kernel<<<grd, blk, 0, s.st>>>(v, lo - s.gj0, hi - s.gj0, psid, psi0, s.dflags, ub);
     CK(cudaGetLastError());
   }

@@ -4,6 +4,7 @@ fp64 steps, identical step count, bitwise-identical dt sequence.  Under the
 arithmetic contract the fields are in fact bitwise equal,
 which is asserted as well."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -288,3 +289,50 @@ def test_tilings_are_bitwise_identical(cs):
         assert np.array_equal(dt, out[0][0])
         for a, b in zip(st, out[0][1]):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("CSPH_RAND_SEEDS", "16"))))
+def test_randomised_configs_bitwise(cs, seed):
+    """Randomised parity net: grid size, terrain/flow config, every physics switch (friction,
+    transport, Shamov gate, slope term, Grass exponent, Eq.4 A_J, Exner sources), Courant
+    number, dry threshold, open edges, HGS, tile height and path -- status, dt log and
+    state bitwise equal to the oracle after 30 steps."""
+    rng = np.random.default_rng(1000 + seed)
+    nx, ny = int(rng.integers(12, 300)), int(rng.integers(12, 260))
+    name = ["C2", "C3", "C4", "C5"][int(rng.integers(0, 4))]
+    c = synth.config(name, nx, ny)
+    f = synth.fill(c)
+    ph = dict(
+        n_manning=float(rng.choice([0.0, rng.uniform(0.01, 0.05)])),
+        A_J=float(rng.choice([0.0, rng.uniform(1e-4, 3e-3)])),
+        C_J=float(rng.uniform(0.0, 3.0)),
+        C_Sh=float(rng.choice([0.0, rng.uniform(2.0, 6.0)])),
+        d50=float(rng.uniform(5e-4, 2e-3)),
+        K=float(rng.uniform(0.1, 0.4)),
+        eps_dry=float(rng.choice([1e-6, 1e-4])),
+        m_grass=int(rng.choice([2, 2, 0, 1, 3, 4])),
+        aj_mode=int(rng.choice([0, 0, 1])),
+        q_plus=float(rng.choice([0.0, 0.0, 1e-6])),
+        q_minus=float(rng.choice([0.0, 0.0, 5e-7])),
+    )
+    if ph["aj_mode"] == 1 and ph["n_manning"] == 0.0:
+        ph["n_manning"] = 0.02
+    open_bc = int(rng.integers(0, 16)) if rng.random() < 0.4 else 0
+    walls = [2 if open_bc & m else 1 for m in (1, 2, 4, 8)]
+    steps = 30
+    ref = oracle.Oracle(nx, ny, c.dx, oracle.Params(**ph))
+    ref.set_walls(*walls)
+    assert ref.set_state(*f) == 0
+    st_ref, dt_ref, lim_ref = ref.step(steps)
+    kw = dict(path=int(rng.integers(0, 2)), hgs=int(rng.integers(0, 2)),
+              tile_rows=int(rng.choice([0, 16, 40])), open_bc=open_bc)
+    g = cs.csph_create(nx, ny, c.dx, cs.params_from(ph, **kw))
+    g.set_state(*f)
+    st = g.step(steps, check=False)
+    dt, lim = g.get_dt_log(steps)
+    out = g.get_state()
+    g.destroy()
+    assert st == st_ref, (ph, kw, st, st_ref)
+    assert np.array_equal(dt, dt_ref) and np.array_equal(lim, lim_ref), (ph, kw)
+    for a, r in zip(out, ref.get_state()):
+        assert np.array_equal(a, r), (ph, kw)
