@@ -321,7 +321,12 @@ def run_ours(a, rank, world, local):
             "algorithmic_bytes_per_launch": bytes_per_step,
             "hgs_tiles": {"marched": f_march, "identity_copy": f_copy, "skipped": f_skip},
             "kernel_ms_per_launch": kern_ms_per,
-            "kernel_share_of_step": kern_ms_per / (ms / a.steps), "peak_source": peak_src}
+            "kernel_share_of_step": kern_ms_per / (ms / a.steps), "peak_source": peak_src,
+            # SURVEY 8(d)'s dense count: bpc bytes for EVERY cell-update, HGS-skipped tiles
+            # included -- bytes the launch did not have to move (reported beside, not as, the
+            # achieved figure above)
+            "dense_equivalent": {"achieved": own_cells * bpc / (kern_ms_per / 1e3) / 1e9,
+                                 "frac": own_cells * bpc / (kern_ms_per / 1e3) / 1e9 / peak}}
     fp64 = None
     if tr and tr.get("fp64_inst_per_launch"):
         # fp64 pipe roof: 64 fp64 lanes/clk/SM x 148 SMs x the SM clock
