@@ -59,7 +59,8 @@ typedef struct {
   int    m_grass;    /* Grass exponent m of Eq.3, integer 0..8 (2 for fine sand) */
   double C_J;        /* Eq.2 slope coefficient (1.5..2.3, up to 5) */
   double C_Sh;       /* Eq.5 Shamov constant; 0 disables the gate */
-  double d50;        /* Eq.5 median grain size [m] (> 0 when C_Sh > 0) */
+  double d50;        /* Eq.5 median grain size [m] (> 0 when C_Sh > 0); also the depth at or
+                        below which no bedload moves (reading #31) */
   double q_plus;     /* Eq.1 deposition source [m/s], default 0 */
   double q_minus;    /* Eq.1 erosion drain [m/s], default 0 */
   int    precision;  /* 64 (default, fp64: the hot path, bitwise = the oracle) or 32 (NEXT-2

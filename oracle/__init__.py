@@ -111,6 +111,7 @@ def lib():
         L.orc_minmod.argtypes = [ctypes.c_double] * 2
         L.orc_hll_face.argtypes = [ctypes.c_double] * 9 + [ctypes.c_int] * 2 + [_D]
         L.orc_shamov_gate.argtypes = [ctypes.c_double] * 4
+        L.orc_bed_mobile.argtypes = [ctypes.c_double] * 2
         _lib = L
     return _lib
 
@@ -279,6 +280,11 @@ def hll_face(g, qm, qp, wL=1, wR=1):
 
 def shamov_gate(kappa, s2, H, C_Sh):
     return bool(lib().orc_shamov_gate(kappa, s2, H, C_Sh))
+
+
+def bed_mobile(H, d50):
+    """Reading #31: bedload only through a water column deeper than the grain."""
+    return bool(lib().orc_bed_mobile(H, d50))
 
 
 def tau_from_M(nx, ny, dx, params: Params, M):

@@ -114,6 +114,13 @@ int orc_shamov_gate(double kappa, double s2, double H, double C_Sh) {
   return ((s2 * s2) * s2 > kappa * H) ? 1 : 0;
 }
 
+/* Reading #31: bedload needs a water column deeper than the grain -- no transport where
+ * H <= d50 (Eq.5's critical velocity C_Sh d50^(1/3) H^(1/6) vanishes as H -> 0, so the gate
+ * alone would let films thinner than a grain carry sediment). */
+int orc_bed_mobile(double H, double d50) {
+  return H > d50 ? 1 : 0;
+}
+
 /* Manning friction coefficient (reading #19): gamma = g n^2 |v| / H^(4/3),
  * written as (c_gam*s)*(r*H^(-1/3)) with r = 1/H. */
 double orc_gamma(const orc_params* p, double H, double u, double v) {
@@ -308,7 +315,7 @@ static void reduce_M(orc_t* o, const double* H, const double* Qx, const double* 
       double t1 = s2;
       double t2 = a + sqrt(p->g * Hc);
       double t3 = 0.0;
-      if (orc_shamov_gate(o->kappa, s2, Hc, p->C_Sh)) {
+      if (orc_shamov_gate(o->kappa, s2, Hc, p->C_Sh) && orc_bed_mobile(Hc, p->d50)) {
         double pw = 1.0;  /* |v|^m as in orc_grass_m; m = 2: pw = s2 */
         for (int k = 0; k < p->m_grass / 2; ++k) pw = pw * s2;
         if (p->m_grass % 2) pw = pw * a;
@@ -558,7 +565,7 @@ int orc_step_tau(orc_t* o, double tau) {
       double jx, jy, ja;
       orc_grass_m(cell_aj(o, c, H[c]), p->m_grass, o->ut[c], o->vt[c], &jx, &jy, &ja);
       double s2 = o->ut[c] * o->ut[c] + o->vt[c] * o->vt[c];
-      if (orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh)) {
+      if (orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh) && orc_bed_mobile(H[c], p->d50)) {
         o->J0x[c] = jx; o->J0y[c] = jy; o->J0a[c] = ja;
       } else {
         o->J0x[c] = 0.0; o->J0y[c] = 0.0; o->J0a[c] = 0.0;

@@ -105,6 +105,8 @@ void   orc_hll_face(double g, double eta_m, double H_m, double un_m, double ut_m
                     double eta_p, double H_p, double un_p, double ut_p,
                     int wL, int wR, double out[3]);
 int    orc_shamov_gate(double kappa, double s2, double H, double C_Sh);
+/* reading #31: bedload only where H > d50 */
+int    orc_bed_mobile(double H, double d50);
 
 #ifdef __cplusplus
 }

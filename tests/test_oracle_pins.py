@@ -604,3 +604,31 @@ def test_ledge_force_is_hydrostatic(orc):
     other = np.delete(phix[1], [k - 1, k])
     assert np.all(other == 0.0)
     assert np.all(o.debug_interior("phiy") == 0.0)
+
+
+def test_film_cutoff_reading31(orc):
+    """Reading #31: bedload needs a water column deeper than the grain.
+    A uniform 2 m/s current over a sloping bed between walls (Shamov gate off, so Eq.3 alone
+    decides): with H = d50/2 the bed does not move and Eq.7's bed term is absent (M3 = 0);
+    with H = 4 d50 the wall ends erode/deposit and M3 = A_J |v|^3 / (1 - psi)."""
+    d50, A, psi = 1e-3, 1e-3, 0.4
+    assert orc.bed_mobile(2 * d50, d50) and not orc.bed_mobile(d50, d50)
+    nx, ny = 16, 3
+    x = np.arange(nx)
+    b = (0.01 * (nx - x))[None, :].repeat(ny, 0).astype(float)
+    for Hd, moves in ((0.5 * d50, False), (4 * d50, True)):
+        h = np.full((ny, nx), Hd)
+        hu = 2.0 * h
+        z = np.zeros((ny, nx))
+        p = orc.Params(A_J=A, C_J=2.0, C_Sh=0.0, d50=d50, eps_dry=1e-6)
+        o = orc.Oracle(nx, ny, 1.0, p)
+        assert o.set_state(h, hu, z, b, np.full((ny, nx), psi)) == 0
+        M = o.reduce_M()
+        if moves:
+            assert rel(M[2], A * 8.0 / (1 - psi)) < 1e-14
+        else:
+            assert M[2] == 0.0
+        st, _, _ = o.step(1)
+        assert st == 0
+        moved = np.any(o.get_state()[3] != b)
+        assert moved == moves
