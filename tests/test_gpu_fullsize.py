@@ -149,9 +149,9 @@ def test_C5_full_size_hgs_and_conservation(cs):
 
 
 def test_C5_full_size_long_run(cs):
-    """The bench workload over 400 steps (about 13 s of simulated flood): no error status,
-    positive finite tau every step, volume and Sum (1 - psi) b kept to rounding, no depth
-    below -neg_tol, no NaN."""
+    """The bench workload over 1200 steps (about 38 s of simulated flood; without reading
+    #31 the bed blew up after ~800): no error status, tau > 0.01 s every
+    step, volume and Sum (1 - psi) b kept to rounding, no depth below -neg_tol, no NaN."""
     c = synth.config("C5")
     f = synth.fill(c)
     W = 1.0 / (1.0 - f[4])
@@ -160,11 +160,12 @@ def test_C5_full_size_long_run(cs):
     g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params))
     g.set_state(*f)
     del f
-    assert g.step(400) == 0
-    dt, lim = g.get_dt_log(400)
-    assert len(dt) == 400 and np.all(np.isfinite(dt)) and np.all(dt > 0)
+    steps = 1200
+    assert g.step(steps) == 0
+    dt, lim = g.get_dt_log(steps)
+    assert len(dt) == steps and np.all(np.isfinite(dt)) and np.all(dt > 0.01)
     t, n, _ = g.get_time()
-    assert n == 400 and t == pytest.approx(float(np.sum(dt)), rel=1e-12)
+    assert n == steps and t == pytest.approx(float(np.sum(dt)), rel=1e-12)
     vol = sed = 0.0
     for j0 in range(0, c.ny, 2048):
         h, hu, hv, b = g.get_state_rows(j0, j0 + 2048)
