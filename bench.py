@@ -26,6 +26,13 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# The input generator (synth/gen.c) is OpenMP: its threads must sleep, not spin, once a fill is
+# done -- spinning threads starve the thread that launches the timed steps -- and under
+# torchrun the ranks share the host's cores.
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
+if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    os.environ.setdefault("OMP_NUM_THREADS",
+                          str(max(1, (os.cpu_count() or 1) // int(os.environ["WORLD_SIZE"]))))
 
 import numpy as np  # noqa: E402
 

@@ -3,6 +3,7 @@ of rows [j0, j1) is run alone as a walled domain and its step time measured; the
 time is bounded below by the slowest strip (halo exchange and the allreduce are overlapped /
 small).  Compares the paper's even Ny_dev split with the wet-count-balanced one."""
 import os, sys
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")  # see bench.py
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth
