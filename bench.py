@@ -315,8 +315,9 @@ def run_ours(a, rank, world, local):
     kern_ms_per = kern_ms / max(kern_steps, 1)
     # HGS: marched tiles move bpc B/cell, identity-copied tiles read H, b (+W) and write
     # 4 fields, skipped tiles move nothing
-    ntile = max(sum(tiles), 1)
-    f_march, f_copy, f_skip = (x / ntile for x in tiles)
+    ntile = sum(tiles)
+    # no HGS counters (the staged path): every cell's bytes move
+    f_march, f_copy, f_skip = (x / ntile for x in tiles) if ntile else (1.0, 0.0, 0.0)
     bpc_copy = ((3 if psi_field else 2) + 4) * es
     bytes_per_step = own_cells * (bpc * f_march + bpc_copy * f_copy)
     achieved = bytes_per_step / (kern_ms_per / 1e3) / 1e9
