@@ -44,7 +44,7 @@ class _Params(ctypes.Structure):
         ("n_manning", ctypes.c_double), ("A_J", ctypes.c_double), ("m_grass", ctypes.c_int),
         ("C_J", ctypes.c_double), ("C_Sh", ctypes.c_double), ("d50", ctypes.c_double),
         ("q_plus", ctypes.c_double), ("q_minus", ctypes.c_double),
-        ("aj_mode", ctypes.c_int), ("s_rel", ctypes.c_double),
+        ("aj_mode", ctypes.c_int), ("s_rel", ctypes.c_double), ("h_bed_min", ctypes.c_double),
     ]
 
 
@@ -65,11 +65,13 @@ class Params:
     q_minus: float = 0.0
     aj_mode: int = 0
     s_rel: float = 2.65
+    h_bed_min: float = -1.0  # reading #31 cut-off depth; < 0: d50
 
     def to_c(self) -> _Params:
         return _Params(self.g, self.K, self.eps_dry, self.dt_max, self.neg_tol,
                        self.n_manning, self.A_J, self.m_grass, self.C_J, self.C_Sh,
-                       self.d50, self.q_plus, self.q_minus, self.aj_mode, self.s_rel)
+                       self.d50, self.q_plus, self.q_minus, self.aj_mode, self.s_rel,
+                       self.h_bed_min)
 
 
 _lib = None

@@ -24,6 +24,7 @@ struct orc {
   orc_params p;
   /* host-side constants of R */
   double inv_h, inv_2h, cP, cgam, kappa;
+  double hbm;  /* reading #31 cut-off depth: h_bed_min, or d50 when h_bed_min < 0 */
   int wall[4];
   int have_state;
   /* state U = (H, Hu, Hv, b) of Eq.6 and W = 1/(1-psi) of Eq.1 */
@@ -114,11 +115,12 @@ int orc_shamov_gate(double kappa, double s2, double H, double C_Sh) {
   return ((s2 * s2) * s2 > kappa * H) ? 1 : 0;
 }
 
-/* Reading #31: bedload needs a water column deeper than the grain -- no transport where
- * H <= d50 (Eq.5's critical velocity C_Sh d50^(1/3) H^(1/6) vanishes as H -> 0, so the gate
- * alone would let films thinner than a grain carry sediment). */
-int orc_bed_mobile(double H, double d50) {
-  return H > d50 ? 1 : 0;
+/* Reading #31: bedload needs a water column deeper than h_bed_min, by default the grain
+ * size d50 -- no transport where H <= h_bed_min (Eq.5's critical velocity C_Sh d50^(1/3)
+ * H^(1/6) vanishes as H -> 0, so the gate alone would let films thinner than a grain carry
+ * sediment).  h_bed_min = 0 is the literal Eq.5. */
+int orc_bed_mobile(double H, double h_bed_min) {
+  return H > h_bed_min ? 1 : 0;
 }
 
 /* Manning friction coefficient (reading #19): gamma = g n^2 |v| / H^(4/3),
@@ -204,6 +206,7 @@ static int valid_params(const orc_params* p) {
   if (!(p->C_Sh >= 0.0) || !isfinite(p->C_Sh)) return 0;
   if (p->C_Sh > 0.0 && !(p->d50 > 0.0)) return 0;
   if (!isfinite(p->q_plus) || !isfinite(p->q_minus)) return 0;
+  if (!isfinite(p->h_bed_min)) return 0;
   return 1;
 }
 
@@ -221,6 +224,7 @@ orc_t* orc_create(int nx, int ny, double dx, const orc_params* p) {
     double c2 = p->C_Sh * p->C_Sh;
     o->kappa = ((c2 * c2) * c2) * (p->d50 * p->d50);
   }
+  o->hbm = p->h_bed_min < 0.0 ? p->d50 : p->h_bed_min;
   for (int s = 0; s < 4; ++s) o->wall[s] = 1;
   size_t n = (size_t)o->pw * (size_t)o->ph;
   double** arrs[] = {&o->H, &o->Qx, &o->Qy, &o->b, &o->W, &o->eta, &o->r, &o->u, &o->v,
@@ -315,7 +319,7 @@ static void reduce_M(orc_t* o, const double* H, const double* Qx, const double* 
       double t1 = s2;
       double t2 = a + sqrt(p->g * Hc);
       double t3 = 0.0;
-      if (orc_shamov_gate(o->kappa, s2, Hc, p->C_Sh) && orc_bed_mobile(Hc, p->d50)) {
+      if (orc_shamov_gate(o->kappa, s2, Hc, p->C_Sh) && orc_bed_mobile(Hc, o->hbm)) {
         double pw = 1.0;  /* |v|^m as in orc_grass_m; m = 2: pw = s2 */
         for (int k = 0; k < p->m_grass / 2; ++k) pw = pw * s2;
         if (p->m_grass % 2) pw = pw * a;
@@ -565,7 +569,7 @@ int orc_step_tau(orc_t* o, double tau) {
       double jx, jy, ja;
       orc_grass_m(cell_aj(o, c, H[c]), p->m_grass, o->ut[c], o->vt[c], &jx, &jy, &ja);
       double s2 = o->ut[c] * o->ut[c] + o->vt[c] * o->vt[c];
-      if (orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh) && orc_bed_mobile(H[c], p->d50)) {
+      if (orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh) && orc_bed_mobile(H[c], o->hbm)) {
         o->J0x[c] = jx; o->J0y[c] = jy; o->J0a[c] = ja;
       } else {
         o->J0x[c] = 0.0; o->J0y[c] = 0.0; o->J0a[c] = 0.0;

@@ -51,6 +51,7 @@ typedef struct {
   double q_plus, q_minus; /* Eq.1 sources (scalars) */
   int    aj_mode;  /* NEXT-4: 0 constant A_J; 1 Eq.4 A_J = 0.05 n_M^3/((s-1) sqrt(gH) d50) */
   double s_rel;    /* Eq.4 relative density rho_s/rho (> 1 in mode 1) */
+  double h_bed_min;/* reading #31: no bedload where H <= h_bed_min; < 0 means d50 */
 } orc_params;
 
 typedef struct orc orc_t;
@@ -105,8 +106,8 @@ void   orc_hll_face(double g, double eta_m, double H_m, double un_m, double ut_m
                     double eta_p, double H_p, double un_p, double ut_p,
                     int wL, int wR, double out[3]);
 int    orc_shamov_gate(double kappa, double s2, double H, double C_Sh);
-/* reading #31: bedload only where H > d50 */
-int    orc_bed_mobile(double H, double d50);
+/* reading #31: bedload only where H > h_bed_min (default d50) */
+int    orc_bed_mobile(double H, double h_bed_min);
 
 #ifdef __cplusplus
 }

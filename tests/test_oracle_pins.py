@@ -132,6 +132,10 @@ def test_eq7_worked_examples(orc):
     r = GOLD["eq7_rest"]
     M, (st, tau, lim) = _single_cell_tau(orc, 1.0, 0.0, 0.0, r["K"], 0.001, 0.4)
     assert st == 0 and rel(tau, r["tau"]) < 1e-15 and lim == 1
+    # supercritical flow (|v| > sqrt(gH)): the particle term h/(2 v_p) binds, limiter 0.
+    # H = 0.1, v = 3: t1 = 1/6 < t2 = 1/(3 + sqrt(0.981)) -> tau = K/6 exactly as written
+    M, (st, tau, lim) = _single_cell_tau(orc, 0.1, 3.0, 0.0, 0.25, 0.0, 0.4)
+    assert st == 0 and lim == 0 and rel(tau, 0.25 / 6.0) < 1e-15
     # dt_max cap -> limiter 3
     M, (st, tau, lim) = _single_cell_tau(orc, 1.0, 0.0, 0.0, 0.5, 0.0, 0.4, dt_max=0.01)
     assert st == 0 and tau == 0.01 and lim == 3
@@ -565,6 +569,29 @@ def test_eq7_bed_diffusion_limits(orc):
     assert rel(tau, K * 1.0 / (2 * D)) < 1e-15
 
 
+def test_wet_threshold_is_strict(orc):
+    """K1's wet test is strict, w = H > eps (P:188 listing `H > Eps`; SURVEY 8(c.1) step 1,
+    reading #15): a grid whose every cell holds exactly eps of water is all dry -- no
+    Eq.7 term, so EDRY without a cap -- and a cell at eps beside a wet one is a dry cell
+    (no velocity, no force) while a cell at the next double above eps is wet."""
+    eps = 1e-6
+    o = orc.Oracle(4, 3, 1.0, orc.Params(eps_dry=eps))
+    e = np.full((3, 4), eps)
+    assert o.set_state(e, 0.5 * e, 0 * e, 0 * e) == 0
+    assert np.all(o.reduce_M() == 0.0)
+    st, _, _ = o.step(1)
+    assert st == orc.EDRY
+    up = np.nextafter(eps, 1.0)
+    o = orc.Oracle(4, 3, 1.0, orc.Params(eps_dry=eps))
+    h = np.full((3, 4), eps); h[1, 2] = up
+    assert o.set_state(h, 0 * h, 0 * h, 0 * h) == 0
+    M = o.reduce_M()
+    assert M[1] == math.sqrt(G * up)  # only the cell above eps counts (|v| = 0)
+    o.step(1)
+    w = o.debug_interior("w")
+    assert w[1, 2] == 1.0 and np.sum(w) == 1.0
+
+
 def test_dry_cells_hold_no_momentum(orc):
     """Type invariant (reading #28): after every step, H <= eps implies
     hu = hv = +0 exactly, including cells that just dried."""
@@ -632,3 +659,14 @@ def test_film_cutoff_reading31(orc):
         assert st == 0
         moved = np.any(o.get_state()[3] != b)
         assert moved == moves
+    # h_bed_min (csph_params / orc_params): an explicit cut-off depth, and 0 = the literal
+    # Eq.5 under which the same film carries bedload
+    for hb, moves in ((0.25 * d50, True), (0.0, True), (0.75 * d50, False)):
+        h = np.full((ny, nx), 0.5 * d50)
+        z = np.zeros((ny, nx))
+        p = orc.Params(A_J=A, C_J=2.0, C_Sh=0.0, d50=d50, eps_dry=1e-6, h_bed_min=hb)
+        o = orc.Oracle(nx, ny, 1.0, p)
+        assert o.set_state(h, 2.0 * h, z, b, np.full((ny, nx), psi)) == 0
+        assert (o.reduce_M()[2] > 0.0) == moves
+        assert o.step(1)[0] == 0
+        assert np.any(o.get_state()[3] != b) == moves
