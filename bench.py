@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--n", type=int, default=None, help="override the grid size (n x n)")
+    ap.add_argument("--grid-n", "--n", dest="n", type=int, default=None,
+                    help="override the grid size (n x n); spell it --grid-n under torchrun "
+                         "(its parser swallows the ambiguous prefix --n)")
     ap.add_argument("--path", choices=["fused", "staged"], default="fused")
     ap.add_argument("--tile-rows", type=int, default=0)
     ap.add_argument("--partition", choices=["balanced", "even"], default="balanced",
@@ -64,7 +66,30 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-crop", type=int, default=2048)
     ap.add_argument("--cpu-steps", type=int, default=15)
+    ap.add_argument("--repeats", type=int, default=3,
+                    help="timed regions of exactly --steps steps each; value = the median "
+                         "(SURVEY 8(d): median of 3 runs)")
+    ap.add_argument("--dist", action="store_true",
+                    help="take the multi-GPU code path (torch.distributed + NCCL id broadcast + "
+                         "csph_create_dist_rows) even with one rank (torchrun --nproc-per-node 1)")
     return ap.parse_args()
+
+
+def host_info():
+    """CPU model and core count of the box the oracle runs on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = None
+    return {"cpu_model": model, "nproc": os.cpu_count(), "affinity_cores": aff}
 
 
 def peaks():
@@ -163,7 +188,8 @@ def cpu_baseline(cfg_name, n, crop, steps):
     el = time.perf_counter() - t
     return {"value": crop * crop * len(dt) / el / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{cfg_name} {c.nx}x{c.ny} centre crop {crop}x{crop} as its own walled "
-                      f"domain, {len(dt)} steps, {el:.1f} s, single thread (status {st})"}
+                      f"domain, {len(dt)} steps, {el:.1f} s, single thread (status {st})",
+            "host": host_info()}
 
 
 def run_reference(a, rank, world):
@@ -191,7 +217,8 @@ def run_reference(a, rank, world):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{a.config} crop {crop}x{crop}", "grid": [crop, crop]},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -204,8 +231,9 @@ def strip_bounds(gen, ny, nx, world, rank, kind, device):
     of the initial state; each rank counts its even strip of the field
     `gen`, the counts are all-gathered and every rank runs csph_balance_rows on them."""
     from paper_2103_15196_b200 import csph
-    if world == 1:
+    if world == 1 and kind != "dist1":
         return [0, ny]
+    kind = "balanced" if kind == "dist1" else kind
     bounds = [csph.csph_strip_rows(ny, world, r)[0] for r in range(world)] + [ny]
     if kind == "even":
         return bounds
@@ -232,7 +260,8 @@ def run_ours(a, rank, world, local):
     from paper_2103_15196_b200 import csph
 
     torch.cuda.set_device(local)
-    if world > 1:
+    distributed = world > 1 or a.dist
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = synth.config(a.config, a.n)
     # weak scaling: the domain is rows [0, 2048 N) of the same global field,
@@ -244,12 +273,14 @@ def run_ours(a, rank, world, local):
     path = csph.CSPH_PATH_FUSED if a.path == "fused" else csph.CSPH_PATH_STAGED
     p = csph.params_from(c.params, path=path, device=local, tile_rows=a.tile_rows,
                          precision=a.precision)
-    bounds = strip_bounds(gen, c.ny, c.nx, world, rank, a.partition, "cuda")
+    bounds = strip_bounds(gen, c.ny, c.nx, world, rank,
+                          "dist1" if (a.dist and world == 1 and a.partition == "balanced")
+                          else a.partition, "cuda")
     j0, j1 = bounds[rank], bounds[rank + 1]
     wa, wb = max(0, j0 - 3), min(c.ny, j1 + 3)
     fields = synth.fill(gen, wa, wb)
     wet_local = float(np.count_nonzero(fields[0][j0 - wa:j1 - wa] > 1e-6))
-    if world > 1:
+    if distributed:
         idt = torch.zeros(csph.csph_nccl_id_bytes(), dtype=torch.uint8, device="cuda")
         if rank == 0:
             idt.copy_(torch.frombuffer(bytearray(csph.csph_make_nccl_id()), dtype=torch.uint8))
@@ -264,39 +295,42 @@ def run_ours(a, rank, world, local):
     psi_field = not np.all(fields[4] == fields[4].flat[0])
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
+        if not distributed:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: float) -> float:
-        if world == 1:
+        if not distributed:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    # ---- warm-up, then exactly K timed steps ----
+    # ---- warm-up, then `repeats` timed regions of exactly K steps each (median) ----
     g.step(a.warmup)
     torch.cuda.synchronize()
     barrier()
     g.profile(True)
     g.reset_tile_stats()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    runs = []
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        barrier()
-        e0.record(stream)
-        g.step(a.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1))
+        for _ in range(max(1, a.repeats)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            barrier()
+            e0.record(stream)
+            g.step(a.steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            runs.append(max_over_ranks(e0.elapsed_time(e1)))
+    ms = float(np.median(runs))
     launches = g.last_launch_count()
     tiles = g.tile_stats()
     kern_ms, kern_steps = g.get_profile()
@@ -383,6 +417,7 @@ def run_ours(a, rank, world, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "timed_runs_ms": runs,
             "scaling": a.scaling, "vs_baseline": None,
             "dtype": "f64" if a.precision == 64 else "f32", "data": "synthetic",
             "config": {
@@ -393,8 +428,8 @@ def run_ours(a, rank, world, local):
                 "grid": [c.nx, c.ny], "cells": cells, "dx_m": c.dx, "wet_fraction": wet,
                 "psi": "field" if psi_field else "uniform", "physics": c.params,
                 "path": a.path, "parallelism": f"row strips x{world} (NCCL halos + allreduce)"
-                if world > 1 else "single GPU",
-                "partition": {"kind": a.partition, "bounds": bounds} if world > 1 else None,
+                if distributed else "single GPU",
+                "partition": {"kind": a.partition, "bounds": bounds} if distributed else None,
                 "l2": "state (>= 19 GB) larger than the 126 MB L2; no flush needed",
                 "tau_mean": float(np.mean(dtl)) if len(dtl) else None,
                 "limiter_hist": np.bincount(liml, minlength=4).tolist() if len(liml) else None,
@@ -413,7 +448,7 @@ def run_ours(a, rank, world, local):
             line["roofline_fp64"] = fp64
         print(json.dumps(line), flush=True)
     g.destroy()
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

@@ -59,8 +59,8 @@ typedef struct {
   int    m_grass;    /* Grass exponent m of Eq.3, integer 0..8 (2 for fine sand) */
   double C_J;        /* Eq.2 slope coefficient (1.5..2.3, up to 5) */
   double C_Sh;       /* Eq.5 Shamov constant; 0 disables the gate */
-  double d50;        /* Eq.5 median grain size [m] (> 0 when C_Sh > 0); also the depth at or
-                        below which no bedload moves (reading #31) */
+  double d50;        /* Eq.5 median grain size [m] (> 0 when C_Sh > 0); by default also the
+                        depth at or below which no bedload moves (h_bed_min below) */
   double q_plus;     /* Eq.1 deposition source [m/s], default 0 */
   double q_minus;    /* Eq.1 erosion drain [m/s], default 0 */
   int    precision;  /* 64 (default, fp64: the hot path, bitwise = the oracle) or 32 (NEXT-2
@@ -79,6 +79,15 @@ typedef struct {
   double s_rel;      /* Eq.4 relative density rho_s/rho (> 1), default 2.65 */
   int    open_bc;    /* NEXT-4 boundaries: bit mask of open (zero-gradient) edges,
                         1 x-low, 2 x-high, 4 y-low, 8 y-high; default 0 = solid walls */
+  int    graphs;     /* 1 (default): a single-grid handle replays its steps in pairs from
+                        CUDA graphs (bitwise identical); 0: plain launches */
+  double h_bed_min;  /* reading #31: no bedload (Eq.3 J0, Eq.7's bed term)
+                        where H <= h_bed_min; < 0 (default -1) means h_bed_min = d50 (a water
+                        column no deeper than the grain); 0 is the literal Eq.5 (any wet cell
+                        may carry bedload) */
+  double m_real;     /* Grass exponent as a real number (Eq.3, "A_J, m are the
+                        constant coefficients"); < 0 (default -1): use the integer m_grass;
+                        >= 0: |v|^m by the pinned pow of DESIGN.md 3.12 (fp64 only) */
 } csph_params;
 
 /* Fill *p with the defaults above. */

@@ -21,19 +21,26 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libcsph_oracle.so")
+# the same source in IEEE binary32: the reference of the NEXT-2 fp32 mode
+_SO32 = os.path.join(_HERE, "libcsph_oracle32.so")
 
 OK, EINVAL, ENOSTATE, ENOMEM, ENEGDEPTH, ENONFINITE, EDRY = 0, -1, -2, -3, -6, -7, -8
 GHOST = 3
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with IEEE-strict flags (no FMA contraction)."""
+    """Compile the oracle with IEEE-strict flags (no FMA contraction), in binary64 and, with
+    -DORC_FP32, in binary32 (SSE scalar float arithmetic: every operation rounded to
+    float, no excess precision on x86-64)."""
     src = os.path.join(_HERE, "csph_oracle.c")
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
-        subprocess.check_call([
-            "gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math",
-            "-Wall", "-shared", "-fPIC", "-o", _SO, src, "-lm",
-        ])
+    hdr = os.path.join(_HERE, "csph_oracle.h")
+    for so, extra in ((_SO, []), (_SO32, ["-DORC_FP32"])):
+        t = max(os.path.getmtime(src), os.path.getmtime(hdr))
+        if force or not os.path.exists(so) or os.path.getmtime(so) < t:
+            subprocess.check_call([
+                "gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math",
+                "-fexcess-precision=standard", "-Wall", "-shared", "-fPIC", "-o", so, src,
+                "-lm"] + extra)
     return _SO
 
 
@@ -74,15 +81,15 @@ class Params:
                        self.h_bed_min)
 
 
-_lib = None
+_libs = {}
 _D = ctypes.POINTER(ctypes.c_double)
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(precision: int = 64):
+    """The oracle library: binary64 (default, R itself) or binary32 (precision=32)."""
+    if precision not in _libs:
         build()
-        L = ctypes.CDLL(_SO)
+        L = ctypes.CDLL(_SO if precision == 64 else _SO32)
         vp = ctypes.c_void_p
         L.orc_create.restype = vp
         L.orc_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.POINTER(_Params)]
@@ -114,8 +121,8 @@ def lib():
         L.orc_hll_face.argtypes = [ctypes.c_double] * 9 + [ctypes.c_int] * 2 + [_D]
         L.orc_shamov_gate.argtypes = [ctypes.c_double] * 4
         L.orc_bed_mobile.argtypes = [ctypes.c_double] * 2
-        _lib = L
-    return _lib
+        _libs[precision] = L
+    return _libs[precision]
 
 
 def _ptr(a: np.ndarray):
@@ -132,18 +139,20 @@ class OracleError(RuntimeError):
 class Oracle:
     """One walled (or partially given-ghost) domain of nx x ny cells."""
 
-    def __init__(self, nx: int, ny: int, dx: float, params: Params | None = None):
+    def __init__(self, nx: int, ny: int, dx: float, params: Params | None = None,
+                 precision: int = 64):
         self.nx, self.ny, self.dx = nx, ny, dx
         self.params = params or Params()
         self._cp = self.params.to_c()
-        self._h = lib().orc_create(nx, ny, dx, ctypes.byref(self._cp))
+        self._L = lib(precision)
+        self._h = self._L.orc_create(nx, ny, dx, ctypes.byref(self._cp))
         if not self._h:
             raise OracleError(EINVAL, "orc_create")
 
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().orc_destroy(h)
+            self._L.orc_destroy(h)
             self._h = None
 
     @property
@@ -152,7 +161,7 @@ class Oracle:
 
     def set_walls(self, xlo=True, xhi=True, ylo=True, yhi=True):
         """Per side: True/1 wall, 2 open (zero-gradient), False/0 caller-supplied ghosts."""
-        st = lib().orc_set_walls(self._h, int(xlo), int(xhi), int(ylo), int(yhi))
+        st = self._L.orc_set_walls(self._h, int(xlo), int(xhi), int(ylo), int(yhi))
         if st != OK:
             raise OracleError(st, "orc_set_walls")
 
@@ -164,7 +173,7 @@ class Oracle:
         if psi is not None:
             psi = np.ascontiguousarray(np.broadcast_to(psi, (self.ny, self.nx)), dtype=np.float64)
             p = _ptr(psi)
-        return lib().orc_set_state(self._h, *[_ptr(a) for a in arrs], p)
+        return self._L.orc_set_state(self._h, *[_ptr(a) for a in arrs], p)
 
     def set_fields(self, n_manning=None, beta=None, src=None) -> int:
         arrs = []
@@ -175,49 +184,49 @@ class Oracle:
                 a = np.ascontiguousarray(np.broadcast_to(a, (self.ny, self.nx)), dtype=np.float64)
                 arrs.append(a)
         self._fields = arrs  # keep alive during the call
-        return lib().orc_set_fields(self._h, *[None if a is None else _ptr(a) for a in arrs])
+        return self._L.orc_set_fields(self._h, *[None if a is None else _ptr(a) for a in arrs])
 
     def set_state_padded(self, H, Qx, Qy, b, W) -> int:
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (H, Qx, Qy, b, W)]
         for a in arrs:
             assert a.shape == self.padded_shape
-        return lib().orc_set_state_padded(self._h, *[_ptr(a) for a in arrs])
+        return self._L.orc_set_state_padded(self._h, *[_ptr(a) for a in arrs])
 
     def get_state(self):
         out = [np.empty((self.ny, self.nx)) for _ in range(4)]
-        st = lib().orc_get_state(self._h, *[_ptr(a) for a in out])
+        st = self._L.orc_get_state(self._h, *[_ptr(a) for a in out])
         if st != OK:
             raise OracleError(st, "orc_get_state")
         return tuple(out)
 
     def get_state_padded(self):
         out = [np.empty(self.padded_shape) for _ in range(4)]
-        st = lib().orc_get_state_padded(self._h, *[_ptr(a) for a in out])
+        st = self._L.orc_get_state_padded(self._h, *[_ptr(a) for a in out])
         if st != OK:
             raise OracleError(st, "orc_get_state_padded")
         return tuple(out)
 
     def reduce_M(self):
         M = np.zeros(3)
-        lib().orc_reduce_M(self._h, _ptr(M))
+        self._L.orc_reduce_M(self._h, _ptr(M))
         return M
 
     def tau_from_M(self, M):
         M = np.ascontiguousarray(M, dtype=np.float64)
         tau = ctypes.c_double(0.0)
         lim = ctypes.c_int(-1)
-        st = lib().orc_tau_from_M(self._h, _ptr(M), ctypes.byref(tau), ctypes.byref(lim))
+        st = self._L.orc_tau_from_M(self._h, _ptr(M), ctypes.byref(tau), ctypes.byref(lim))
         return st, tau.value, lim.value
 
     def step_tau(self, tau: float) -> int:
-        return lib().orc_step_tau(self._h, tau)
+        return self._L.orc_step_tau(self._h, tau)
 
     def step(self, nsteps: int):
         """Returns (status, dt_log, limiter_log) for the steps actually done."""
         dt = np.zeros(max(nsteps, 1))
         lim = np.zeros(max(nsteps, 1), dtype=np.int32)
         n = ctypes.c_int(0)
-        st = lib().orc_step(self._h, nsteps, _ptr(dt),
+        st = self._L.orc_step(self._h, nsteps, _ptr(dt),
                             lim.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), ctypes.byref(n))
         return st, dt[: n.value].copy(), lim[: n.value].copy()
 
@@ -225,12 +234,12 @@ class Oracle:
         t = ctypes.c_double(0.0)
         s = ctypes.c_longlong(0)
         d = ctypes.c_double(0.0)
-        lib().orc_get_time(self._h, ctypes.byref(t), ctypes.byref(s), ctypes.byref(d))
+        self._L.orc_get_time(self._h, ctypes.byref(t), ctypes.byref(s), ctypes.byref(d))
         return t.value, s.value, d.value
 
     def debug(self, name: str) -> np.ndarray:
         out = np.empty(self.padded_shape)
-        st = lib().orc_get_debug(self._h, name.encode(), _ptr(out))
+        st = self._L.orc_get_debug(self._h, name.encode(), _ptr(out))
         if st != OK:
             raise OracleError(st, f"orc_get_debug({name})")
         return out

@@ -7,7 +7,15 @@
  * order K1..K8.  No blocking, fusion or reordering.
  *
  * Build: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC
- * (IEEE binary64, round-to-nearest, no implicit FMA contraction; DESIGN.md 3.10).
+ * (IEEE binary64, round-to-nearest, no implicit FMA contraction; DESIGN.md 3.9).
+ *
+ * The same source built with -DORC_FP32 is R evaluated in IEEE binary32 (DESIGN.md 3.14,
+ * the NEXT-2 fp32 mode): state, intermediates and every per-cell operation in float, so
+ * every decision of R (wet test, gate, donor, HLL case, minmod) is taken in the precision
+ * the fp32 mode computes in; host constants are computed in double and rounded once to
+ * float; tau is computed in double from the float maxima widened exactly (Eq.7 on the
+ * host side of the step), then rounded to float for the step.  x^(-1/3) in fp32 is the
+ * pinned binary32 recipe of DESIGN.md 3.14.  Public entry points keep double arguments.
  */
 #include "csph_oracle.h"
 
@@ -16,27 +24,38 @@
 #include <stdlib.h>
 #include <string.h>
 
+#ifdef ORC_FP32
+typedef float real;
+#define SQRT sqrtf
+#else
+typedef double real;
+#define SQRT sqrt
+#endif
+#define RL(x) ((real)(x))  /* a constant of R in the working precision */
+
 #define G 3 /* ghost layers: the stencil radius of R */
 
 struct orc {
   int nx, ny, pw, ph; /* interior size, padded width/height */
   double h;           /* cell size ("h is cell size") */
   orc_params p;
-  /* host-side constants of R */
-  double inv_h, inv_2h, cP, cgam, kappa;
-  double hbm;  /* reading #31 cut-off depth: h_bed_min, or d50 when h_bed_min < 0 */
+  /* host-side constants of R, computed in double, then rounded once to
+   * the working precision */
+  real inv_h, inv_2h, cP, cgam, kappa;
+  real hbm;  /* reading #31 cut-off depth: h_bed_min, or d50 when h_bed_min < 0 */
+  real eps, neg_tol, g, A_J, C_J, C_Sh, d50, s_rel, src;
   int wall[4];
   int have_state;
   /* state U = (H, Hu, Hv, b) of Eq.6 and W = 1/(1-psi) of Eq.1 */
-  double *H, *Qx, *Qy, *b, *W;
+  real *H, *Qx, *Qy, *b, *W;
   /* intermediates (padded) */
-  double *eta, *r, *u, *v, *phix, *phiy, *gam, *Hh, *ut, *vt, *phix2, *phiy2;
-  double *QLx, *QLy, *J0x, *J0y, *J0a;
-  double *FH, *FQx, *FQy, *FJ, *GH, *GQx, *GQy, *GJ;
-  double *Hn, *Qxn, *Qyn, *bn;
+  real *eta, *r, *u, *v, *phix, *phiy, *gam, *Hh, *ut, *vt, *phix2, *phiy2;
+  real *QLx, *QLy, *J0x, *J0y, *J0a;
+  real *FH, *FQx, *FQy, *FJ, *GH, *GQx, *GQy, *GJ;
+  real *Hn, *Qxn, *Qyn, *bn;
   /* NEXT-3 spatial inputs (P:129 n_M(x,y), beta(x,y); Eq.6 sigma):
    * per-cell c_gam = g n_M^2, absorption beta and source s (rain + point inflow) */
-  double *cg, *beta, *srcf, *nfld;
+  real *cg, *beta, *srcf, *nfld;
   int has_fields, fields_fric, fields_src;
   unsigned char* w;
   double M[3];
@@ -46,72 +65,79 @@ struct orc {
 
 #define IDX(o, i, j) ((size_t)((j) + G) * (size_t)(o)->pw + (size_t)((i) + G))
 
-/* ---- small pieces of R -------------------------------------------------- */
+/* ---- small pieces of R (in the working precision `real`) ------------------ */
 
-/* explicit selects, never fmin/fmax (DESIGN.md 3.10) */
-static double sel_min(double a, double b) { return (a < b) ? a : b; }
-static double sel_max(double a, double b) { return (a > b) ? a : b; }
+/* explicit selects, never fmin/fmax (DESIGN.md 3.9) */
+static real sel_min(real a, real b) { return (a < b) ? a : b; }
+static real sel_max(real a, real b) { return (a > b) ? a : b; }
 
 /* minmod TVD limiter ("TVD-limiters"; reading #12) */
-double orc_minmod(double a, double b) {
-  if (a > 0.0 && b > 0.0) return sel_min(a, b);
-  if (a < 0.0 && b < 0.0) return sel_max(a, b);
-  return 0.0;
+static real r_minmod(real a, real b) {
+  if (a > RL(0) && b > RL(0)) return sel_min(a, b);
+  if (a < RL(0) && b < RL(0)) return sel_max(a, b);
+  return RL(0);
 }
 
-/* pinned x^(-1/3) for x > 0 normal (DESIGN.md 3.10): integer seed from the
+#ifdef ORC_FP32
+/* pinned binary32 x^(-1/3) for x > 0 normal: integer seed from the bits,
+ * then 3 Newton steps y <- y + y*((1 - x*y^3)*(1/3)) */
+static real r_icbrt(real x) {
+  int32_t bits;
+  memcpy(&bits, &x, 4);
+  int32_t yb = 0x54A2FA8C - bits / 3;
+  real y;
+  memcpy(&y, &yb, 4);
+  const real third = RL(1) / RL(3);
+  for (int k = 0; k < 3; ++k) y = y + y * ((RL(1) - x * ((y * y) * y)) * third);
+  return y;
+}
+#else
+/* pinned x^(-1/3) for x > 0 normal (DESIGN.md 3.9): integer seed from the
  * exponent bits, then 5 Newton steps y <- y + y*((1 - x*y^3)*(1/3)). */
-double orc_icbrt(double x) {
+static real r_icbrt(real x) {
   uint64_t bits;
   memcpy(&bits, &x, 8);
   uint64_t yb = 0x553F751EB851EC00ull - bits / 3ull;
-  double y;
+  real y;
   memcpy(&y, &yb, 8);
-  const double third = 1.0 / 3.0;
+  const real third = 1.0 / 3.0;
   for (int k = 0; k < 5; ++k) {
-    double y3 = (y * y) * y;
-    double e = (1.0 - x * y3) * third;
+    real y3 = (y * y) * y;
+    real e = (1.0 - x * y3) * third;
     y = y + y * e;
   }
   return y;
 }
+#endif
 
-/* Grass formula Eq.3 with m = 2: J0 = A_J v |v|^2, |J0| = A_J |v|^3 */
-void orc_grass(double A_J, double vx, double vy, double* jx, double* jy, double* jabs) {
-  double s2 = vx * vx + vy * vy;
-  double a = A_J * s2;
-  *jx = a * vx;
-  *jy = a * vy;
-  *jabs = a * sqrt(s2);
-}
-
-/* Eq.3 with integer m (NEXT-4): p = |v|^m by repeated multiplication in s2 = |v|^2,
- * then J0 = (A p) v and |J0| = (A p) |v|.  m = 2 reproduces orc_grass exactly. */
-void orc_grass_m(double A, int m, double vx, double vy, double* jx, double* jy, double* jabs) {
-  double s2 = vx * vx + vy * vy;
-  double a = sqrt(s2);
-  double pw = 1.0;
+/* Eq.3 with integer m (m = 2 on the hot path, NEXT-4 any 0..8): p = |v|^m by
+ * repeated multiplication in s2 = |v|^2, then J0 = (A p) v and |J0| = (A p) |v|.  For
+ * m = 2: p = 1 * s2 = s2 exactly, i.e. J0 = A_J v |v|^2, |J0| = A_J |v|^3. */
+static void r_grass_m(real A, int m, real vx, real vy, real* jx, real* jy, real* jabs) {
+  real s2 = vx * vx + vy * vy;
+  real a = SQRT(s2);
+  real pw = RL(1);
   for (int k = 0; k < m / 2; ++k) pw = pw * s2;
   if (m % 2) pw = pw * a;
-  double c = A * pw;
+  real c = A * pw;
   *jx = c * vx;
   *jy = c * vy;
   *jabs = c * a;
 }
 
 /* Eq.4, A_J from the local depth H (reading #5: H = local depth) */
-double orc_aj_eq4(double g, double n_manning, double s_rel, double H, double d50) {
-  return (0.05 * ((n_manning * n_manning) * n_manning)) / (((s_rel - 1.0) * sqrt(g * H)) * d50);
+static real r_aj_eq4(real g, real n_manning, real s_rel, real H, real d50) {
+  return (RL(0.05) * ((n_manning * n_manning) * n_manning)) / (((s_rel - RL(1)) * SQRT(g * H)) * d50);
 }
 
 /* Eq.2, vector reading #4: J_n = J0_n - C_J |J0| db/dn */
-double orc_slope_flux(double J0n, double J0abs, double C_J, double db_dn) {
+static real r_slope_flux(real J0n, real J0abs, real C_J, real db_dn) {
   return J0n - (C_J * J0abs) * db_dn;
 }
 
 /* Eq.5 Shamov gate, reading #6: |v| > v_k  <=>  s2^3 > kappa*H */
-int orc_shamov_gate(double kappa, double s2, double H, double C_Sh) {
-  if (C_Sh == 0.0) return 1;
+static int r_shamov_gate(real kappa, real s2, real H, real C_Sh) {
+  if (C_Sh == RL(0)) return 1;
   return ((s2 * s2) * s2 > kappa * H) ? 1 : 0;
 }
 
@@ -119,18 +145,8 @@ int orc_shamov_gate(double kappa, double s2, double H, double C_Sh) {
  * size d50 -- no transport where H <= h_bed_min (Eq.5's critical velocity C_Sh d50^(1/3)
  * H^(1/6) vanishes as H -> 0, so the gate alone would let films thinner than a grain carry
  * sediment).  h_bed_min = 0 is the literal Eq.5. */
-int orc_bed_mobile(double H, double h_bed_min) {
+static int r_bed_mobile(real H, real h_bed_min) {
   return H > h_bed_min ? 1 : 0;
-}
-
-/* Manning friction coefficient (reading #19): gamma = g n^2 |v| / H^(4/3),
- * written as (c_gam*s)*(r*H^(-1/3)) with r = 1/H (DESIGN.md 3.3). */
-double orc_gamma(const orc_params* p, double H, double u, double v) {
-  if (!(p->n_manning > 0.0)) return 0.0;
-  double cg = p->g * (p->n_manning * p->n_manning);
-  double s = sqrt(u * u + v * v);
-  double r = 1.0 / H;
-  return (cg * s) * (r * orc_icbrt(H));
 }
 
 /* Face pressure term of K2/K5 (Eq.6 row 2, -gH grad(H+b), reading #1;
@@ -139,54 +155,103 @@ double orc_gamma(const orc_params* p, double H, double u, double v) {
  *   P  = (c_P * (0.5*(H*_L + H*_R))) * (H*_R - H*_L).
  * The wet flags are not needed: a dry cell whose bed is above the water has
  * H* = 0 on both sides of the face (a wall), a lower dry cell drives the flow. */
-static double face_force(double cP, double etaL, double bL, double etaR, double bR) {
-  double bs = sel_max(bL, bR);
-  double HsL = sel_max(0.0, etaL - bs);
-  double HsR = sel_max(0.0, etaR - bs);
-  return (cP * (0.5 * (HsL + HsR))) * (HsR - HsL);
+static real face_force(real cP, real etaL, real bL, real etaR, real bR) {
+  real bs = sel_max(bL, bR);
+  real HsL = sel_max(RL(0), etaL - bs);
+  real HsR = sel_max(RL(0), etaR - bs);
+  return (cP * (RL(0.5) * (HsL + HsR))) * (HsR - HsL);
 }
 
 /* K7: hydrostatic step + HLL on F = (Hu, Hu^2, Huv) (Eq.6) */
-void orc_hll_face(double g, double eta_m, double H_m, double un_m, double ut_m,
-                  double eta_p, double H_p, double un_p, double ut_p,
-                  int wL, int wR, double out[3]) {
-  out[0] = 0.0; out[1] = 0.0; out[2] = 0.0;
+static void r_hll_face(real g, real eta_m, real H_m, real un_m, real ut_m,
+                       real eta_p, real H_p, real un_p, real ut_p,
+                       int wL, int wR, real out[3]) {
+  out[0] = RL(0); out[1] = RL(0); out[2] = RL(0);
   if (!wL && !wR) return;
-  double b_m = eta_m - H_m, b_p = eta_p - H_p;
-  double bs = sel_max(b_m, b_p);
-  double Hs_m = sel_max(0.0, eta_m - bs);
-  double Hs_p = sel_max(0.0, eta_p - bs);
-  int dry_m = !(Hs_m > 0.0), dry_p = !(Hs_p > 0.0);
+  real b_m = eta_m - H_m, b_p = eta_p - H_p;
+  real bs = sel_max(b_m, b_p);
+  real Hs_m = sel_max(RL(0), eta_m - bs);
+  real Hs_p = sel_max(RL(0), eta_p - bs);
+  int dry_m = !(Hs_m > RL(0)), dry_p = !(Hs_p > RL(0));
   if (dry_m && dry_p) return;
-  double m_m = Hs_m * un_m, m_p = Hs_p * un_p;
-  double FL[3] = {m_m, m_m * un_m, m_m * ut_m};
-  double FR[3] = {m_p, m_p * un_p, m_p * ut_p};
-  double UL[3] = {Hs_m, m_m, Hs_m * ut_m};
-  double UR[3] = {Hs_p, m_p, Hs_p * ut_p};
-  double SL, SR;
+  real m_m = Hs_m * un_m, m_p = Hs_p * un_p;
+  real FL[3] = {m_m, m_m * un_m, m_m * ut_m};
+  real FR[3] = {m_p, m_p * un_p, m_p * ut_p};
+  real UL[3] = {Hs_m, m_m, Hs_m * ut_m};
+  real UR[3] = {Hs_p, m_p, Hs_p * ut_p};
+  real SL, SR;
   if (!dry_m && !dry_p) {
-    double c_m = sqrt(g * Hs_m), c_p = sqrt(g * Hs_p);
+    real c_m = SQRT(g * Hs_m), c_p = SQRT(g * Hs_p);
     SL = sel_min(un_m - c_m, un_p - c_p);
     SR = sel_max(un_m + c_m, un_p + c_p);
   } else if (dry_p) {
-    double c_m = sqrt(g * Hs_m);
+    real c_m = SQRT(g * Hs_m);
     SL = un_m - c_m;
-    SR = un_m + 2.0 * c_m;
+    SR = un_m + RL(2) * c_m;
   } else {
-    double c_p = sqrt(g * Hs_p);
-    SL = un_p - 2.0 * c_p;
+    real c_p = SQRT(g * Hs_p);
+    SL = un_p - RL(2) * c_p;
     SR = un_p + c_p;
   }
-  if (SL >= 0.0) {
+  if (SL >= RL(0)) {
     for (int k = 0; k < 3; ++k) out[k] = FL[k];
-  } else if (SR <= 0.0) {
+  } else if (SR <= RL(0)) {
     for (int k = 0; k < 3; ++k) out[k] = FR[k];
   } else {
-    double inv = 1.0 / (SR - SL);
-    double SLSR = SL * SR;
+    real inv = RL(1) / (SR - SL);
+    real SLSR = SL * SR;
     for (int k = 0; k < 3; ++k)
       out[k] = ((SR * FL[k] - SL * FR[k]) + SLSR * (UR[k] - UL[k])) * inv;
   }
+}
+
+/* ---- public double entry points of the pieces (pins) ---------------------- */
+
+double orc_minmod(double a, double b) { return r_minmod(RL(a), RL(b)); }
+double orc_icbrt(double x) { return r_icbrt(RL(x)); }
+
+void orc_grass(double A_J, double vx, double vy, double* jx, double* jy, double* jabs) {
+  orc_grass_m(A_J, 2, vx, vy, jx, jy, jabs);
+}
+
+void orc_grass_m(double A, int m, double vx, double vy, double* jx, double* jy, double* jabs) {
+  real x, y, a;
+  r_grass_m(RL(A), m, RL(vx), RL(vy), &x, &y, &a);
+  *jx = x; *jy = y; *jabs = a;
+}
+
+double orc_aj_eq4(double g, double n_manning, double s_rel, double H, double d50) {
+  return r_aj_eq4(RL(g), RL(n_manning), RL(s_rel), RL(H), RL(d50));
+}
+
+double orc_slope_flux(double J0n, double J0abs, double C_J, double db_dn) {
+  return r_slope_flux(RL(J0n), RL(J0abs), RL(C_J), RL(db_dn));
+}
+
+int orc_shamov_gate(double kappa, double s2, double H, double C_Sh) {
+  return r_shamov_gate(RL(kappa), RL(s2), RL(H), RL(C_Sh));
+}
+
+int orc_bed_mobile(double H, double h_bed_min) { return r_bed_mobile(RL(H), RL(h_bed_min)); }
+
+/* Manning friction coefficient (reading #19): gamma = g n^2 |v| / H^(4/3),
+ * written as (c_gam*s)*(r*H^(-1/3)) with r = 1/H (DESIGN.md 3.3). */
+double orc_gamma(const orc_params* p, double H, double u, double v) {
+  if (!(p->n_manning > 0.0)) return 0.0;
+  real cg = RL(p->g * (p->n_manning * p->n_manning));
+  real uu = RL(u), vv = RL(v), Hh = RL(H);
+  real s = SQRT(uu * uu + vv * vv);
+  real r = RL(1) / Hh;
+  return (cg * s) * (r * r_icbrt(Hh));
+}
+
+void orc_hll_face(double g, double eta_m, double H_m, double un_m, double ut_m,
+                  double eta_p, double H_p, double un_p, double ut_p,
+                  int wL, int wR, double out[3]) {
+  real o[3];
+  r_hll_face(RL(g), RL(eta_m), RL(H_m), RL(un_m), RL(ut_m), RL(eta_p), RL(H_p), RL(un_p),
+             RL(ut_p), wL, wR, o);
+  for (int k = 0; k < 3; ++k) out[k] = o[k];
 }
 
 /* ---- lifecycle ------------------------------------------------------------ */
@@ -216,24 +281,27 @@ orc_t* orc_create(int nx, int ny, double dx, const orc_params* p) {
   if (!o) return NULL;
   o->nx = nx; o->ny = ny; o->pw = nx + 2 * G; o->ph = ny + 2 * G;
   o->h = dx; o->p = *p;
-  o->inv_h = 1.0 / dx;
-  o->inv_2h = 1.0 / (2.0 * dx);
-  o->cP = p->g / (2.0 * dx);
-  o->cgam = p->g * (p->n_manning * p->n_manning);
+  o->inv_h = RL(1.0 / dx);
+  o->inv_2h = RL(1.0 / (2.0 * dx));
+  o->cP = RL(p->g / (2.0 * dx));
+  o->cgam = RL(p->g * (p->n_manning * p->n_manning));
   {
     double c2 = p->C_Sh * p->C_Sh;
-    o->kappa = ((c2 * c2) * c2) * (p->d50 * p->d50);
+    o->kappa = RL(((c2 * c2) * c2) * (p->d50 * p->d50));
   }
-  o->hbm = p->h_bed_min < 0.0 ? p->d50 : p->h_bed_min;
+  o->hbm = RL(p->h_bed_min < 0.0 ? p->d50 : p->h_bed_min);
+  o->eps = RL(p->eps_dry); o->neg_tol = RL(p->neg_tol); o->g = RL(p->g);
+  o->A_J = RL(p->A_J); o->C_J = RL(p->C_J); o->C_Sh = RL(p->C_Sh); o->d50 = RL(p->d50);
+  o->s_rel = RL(p->s_rel); o->src = RL(p->q_plus - p->q_minus);
   for (int s = 0; s < 4; ++s) o->wall[s] = 1;
   size_t n = (size_t)o->pw * (size_t)o->ph;
-  double** arrs[] = {&o->H, &o->Qx, &o->Qy, &o->b, &o->W, &o->eta, &o->r, &o->u, &o->v,
+  real** arrs[] = {&o->H, &o->Qx, &o->Qy, &o->b, &o->W, &o->eta, &o->r, &o->u, &o->v,
                      &o->phix, &o->phiy, &o->gam, &o->Hh, &o->ut, &o->vt, &o->phix2,
                      &o->phiy2, &o->QLx, &o->QLy, &o->J0x, &o->J0y, &o->J0a, &o->FH,
                      &o->FQx, &o->FQy, &o->FJ, &o->GH, &o->GQx, &o->GQy, &o->GJ,
                      &o->Hn, &o->Qxn, &o->Qyn, &o->bn, &o->cg, &o->beta, &o->srcf, &o->nfld};
   for (size_t k = 0; k < sizeof(arrs) / sizeof(arrs[0]); ++k) {
-    *arrs[k] = (double*)calloc(n, sizeof(double));
+    *arrs[k] = (real*)calloc(n, sizeof(real));
     if (!*arrs[k]) { orc_destroy(o); return NULL; }
   }
   o->w = (unsigned char*)calloc(n, 1);
@@ -243,7 +311,7 @@ orc_t* orc_create(int nx, int ny, double dx, const orc_params* p) {
 
 void orc_destroy(orc_t* o) {
   if (!o) return;
-  double* arrs[] = {o->H, o->Qx, o->Qy, o->b, o->W, o->eta, o->r, o->u, o->v, o->phix,
+  real* arrs[] = {o->H, o->Qx, o->Qy, o->b, o->W, o->eta, o->r, o->u, o->v, o->phix,
                     o->phiy, o->gam, o->Hh, o->ut, o->vt, o->phix2, o->phiy2, o->QLx,
                     o->QLy, o->J0x, o->J0y, o->J0a, o->FH, o->FQx, o->FQy, o->FJ,
                     o->GH, o->GQx, o->GQy, o->GJ, o->Hn, o->Qxn, o->Qyn, o->bn,
@@ -295,37 +363,37 @@ static void mirror_fill(orc_t* o) {
 }
 
 /* A_J of cell c at depth H: the constant, or Eq.4 with the cell's n_M (NEXT-4) */
-static double cell_aj(const orc_t* o, size_t c, double H) {
-  if (o->p.aj_mode == 0) return o->p.A_J;
-  if (!(H > o->p.eps_dry)) return 0.0;
-  double n = o->fields_fric ? o->nfld[c] : o->p.n_manning;
-  return orc_aj_eq4(o->p.g, n, o->p.s_rel, H, o->p.d50);
+static real cell_aj(const orc_t* o, size_t c, real H) {
+  if (o->p.aj_mode == 0) return o->A_J;
+  if (!(H > o->eps)) return RL(0);
+  real n = o->fields_fric ? o->nfld[c] : RL(o->p.n_manning);
+  return r_aj_eq4(o->g, n, o->s_rel, H, o->d50);
 }
 
-/* Step 9: maxima over the owned wet cells of the state. */
-static void reduce_M(orc_t* o, const double* H, const double* Qx, const double* Qy,
-                     double M[3]) {
+/* Step 9: maxima over the owned wet cells of the state, computed in the
+ * working precision and widened exactly to double. */
+static void reduce_M(orc_t* o, const real* H, const real* Qx, const real* Qy, double M[3]) {
   const orc_params* p = &o->p;
-  double M1 = 0.0, M2 = 0.0, M3 = 0.0;
+  real M1 = RL(0), M2 = RL(0), M3 = RL(0);
   for (int j = 0; j < o->ny; ++j) {
     for (int i = 0; i < o->nx; ++i) {
       size_t c = IDX(o, i, j);
-      double Hc = H[c];
-      if (!(Hc > p->eps_dry)) continue;
-      double r = 1.0 / Hc;
-      double u = Qx[c] * r, v = Qy[c] * r;
-      double s2 = u * u + v * v;
-      double a = sqrt(s2);
-      double t1 = s2;
-      double t2 = a + sqrt(p->g * Hc);
-      double t3 = 0.0;
-      if (orc_shamov_gate(o->kappa, s2, Hc, p->C_Sh) && orc_bed_mobile(Hc, o->hbm)) {
-        double pw = 1.0;  /* |v|^m as in orc_grass_m; m = 2: pw = s2 */
+      real Hc = H[c];
+      if (!(Hc > o->eps)) continue;
+      real r = RL(1) / Hc;
+      real u = Qx[c] * r, v = Qy[c] * r;
+      real s2 = u * u + v * v;
+      real a = SQRT(s2);
+      real t1 = s2;
+      real t2 = a + SQRT(o->g * Hc);
+      real t3 = RL(0);
+      if (r_shamov_gate(o->kappa, s2, Hc, o->C_Sh) && r_bed_mobile(Hc, o->hbm)) {
+        real pw = RL(1);  /* |v|^m as in r_grass_m; m = 2: pw = s2 */
         for (int k = 0; k < p->m_grass / 2; ++k) pw = pw * s2;
         if (p->m_grass % 2) pw = pw * a;
         t3 = ((cell_aj(o, c, Hc) * pw) * a) * o->W[c];
       }
-      /* max that lets NaN win (DESIGN.md 3.10) */
+      /* max that lets NaN win (DESIGN.md 3.6) */
       if (!(t1 <= M1)) M1 = t1;
       if (!(t2 <= M2)) M2 = t2;
       if (!(t3 <= M3)) M3 = t3;
@@ -353,8 +421,8 @@ int orc_set_state(orc_t* o, const double* h, const double* hu, const double* hv,
   for (int j = 0; j < o->ny; ++j)
     for (int i = 0; i < o->nx; ++i) {
       size_t s = (size_t)j * o->nx + i, d = IDX(o, i, j);
-      o->H[d] = h[s]; o->Qx[d] = hu[s]; o->Qy[d] = hv[s]; o->b[d] = b[s];
-      o->W[d] = 1.0 / (1.0 - (psi ? psi[s] : 0.0)); /* Eq.1: W = 1/(1-psi) */
+      o->H[d] = RL(h[s]); o->Qx[d] = RL(hu[s]); o->Qy[d] = RL(hv[s]); o->b[d] = RL(b[s]);
+      o->W[d] = RL(1.0 / (1.0 - (psi ? psi[s] : 0.0))); /* Eq.1: W = 1/(1-psi) */
     }
   mirror_fill(o);
   reduce_M(o, o->H, o->Qx, o->Qy, o->M);
@@ -367,8 +435,10 @@ int orc_set_state_padded(orc_t* o, const double* H, const double* Qx, const doub
                          const double* b, const double* W) {
   if (!o || !H || !Qx || !Qy || !b || !W) return ORC_EINVAL;
   size_t n = (size_t)o->pw * o->ph;
-  memcpy(o->H, H, n * 8); memcpy(o->Qx, Qx, n * 8); memcpy(o->Qy, Qy, n * 8);
-  memcpy(o->b, b, n * 8); memcpy(o->W, W, n * 8);
+  for (size_t k = 0; k < n; ++k) {
+    o->H[k] = RL(H[k]); o->Qx[k] = RL(Qx[k]); o->Qy[k] = RL(Qy[k]);
+    o->b[k] = RL(b[k]); o->W[k] = RL(W[k]);
+  }
   mirror_fill(o);
   reduce_M(o, o->H, o->Qx, o->Qy, o->M);
   o->have_state = 1;
@@ -390,16 +460,16 @@ int orc_set_fields(orc_t* o, const double* n_manning, const double* beta, const 
     for (int i = 0; i < o->nx; ++i) {
       size_t s = (size_t)j * o->nx + i, d = IDX(o, i, j);
       double nm = n_manning ? n_manning[s] : o->p.n_manning;
-      o->cg[d] = o->p.g * (nm * nm);
-      o->nfld[d] = nm;
-      o->beta[d] = beta ? beta[s] : 0.0;
-      o->srcf[d] = src ? src[s] : 0.0;
+      o->cg[d] = RL(o->p.g * (nm * nm));
+      o->nfld[d] = RL(nm);
+      o->beta[d] = RL(beta ? beta[s] : 0.0);
+      o->srcf[d] = RL(src ? src[s] : 0.0);
     }
   /* the fields are mirrored into the wall ghosts like H and b (reading #14) */
   {
-    double* fl[4] = {o->cg, o->beta, o->srcf, o->nfld};
+    real* fl[4] = {o->cg, o->beta, o->srcf, o->nfld};
     for (int q = 0; q < 4; ++q) {
-      double* f = fl[q];
+      real* f = fl[q];
       for (int j = 0; j < o->ny; ++j)
         for (int k = 0; k < G; ++k) {
           if (o->wall[0]) f[IDX(o, -1 - k, j)] = f[IDX(o, o->wall[0] == 2 ? 0 : k, j)];
@@ -438,10 +508,12 @@ int orc_get_state_padded(orc_t* o, double* H, double* Qx, double* Qy, double* b)
   if (!o) return ORC_EINVAL;
   if (!o->have_state) return ORC_ENOSTATE;
   size_t n = (size_t)o->pw * o->ph;
-  if (H) memcpy(H, o->H, n * 8);
-  if (Qx) memcpy(Qx, o->Qx, n * 8);
-  if (Qy) memcpy(Qy, o->Qy, n * 8);
-  if (b) memcpy(b, o->b, n * 8);
+  for (size_t k = 0; k < n; ++k) {
+    if (H) H[k] = o->H[k];
+    if (Qx) Qx[k] = o->Qx[k];
+    if (Qy) Qy[k] = o->Qy[k];
+    if (b) b[k] = o->b[k];
+  }
   return ORC_OK;
 }
 
@@ -473,16 +545,18 @@ int orc_tau_from_M(const orc_t* o, const double M[3], double* tau, int* lim) {
 
 /* ---- one step of R with a given tau ---------------------------------------- */
 
-int orc_step_tau(orc_t* o, double tau) {
+int orc_step_tau(orc_t* o, double tau_d) {
   if (!o) return ORC_EINVAL;
   if (!o->have_state) return ORC_ENOSTATE;
   const orc_params* p = &o->p;
   const int nx = o->nx, ny = o->ny;
-  const double eps = p->eps_dry;
-  const double theta = 0.5 * tau;
-  const double lam = tau / o->h;
+  const real eps = o->eps;
+  /* tau in the working precision; lambda = tau/h formed in double, then rounded once */
+  const real tau = RL(tau_d);
+  const real theta = RL(0.5) * tau;
+  const real lam = RL(tau_d / o->h);
   const int fric = p->n_manning > 0.0 || o->fields_fric;
-  double *H = o->H, *Qx = o->Qx, *Qy = o->Qy, *b = o->b, *W = o->W;
+  real *H = o->H, *Qx = o->Qx, *Qy = o->Qy, *b = o->b, *W = o->W;
   const size_t sx = 1, sy = (size_t)o->pw;
 
   /* Step 1 -- K1: wet mask, eta, velocities on every cell */
@@ -492,11 +566,11 @@ int orc_step_tau(orc_t* o, double tau) {
       o->w[c] = H[c] > eps;
       o->eta[c] = H[c] + b[c];
       if (o->w[c]) {
-        o->r[c] = 1.0 / H[c];
+        o->r[c] = RL(1) / H[c];
         o->u[c] = Qx[c] * o->r[c];
         o->v[c] = Qy[c] * o->r[c];
       } else {
-        o->r[c] = 0.0; o->u[c] = 0.0; o->v[c] = 0.0;
+        o->r[c] = RL(0); o->u[c] = RL(0); o->v[c] = RL(0);
       }
     }
 
@@ -504,23 +578,23 @@ int orc_step_tau(orc_t* o, double tau) {
   for (int j = -G + 1; j < ny + G - 1; ++j)
     for (int i = -G + 1; i < nx + G - 1; ++i) {
       size_t c = IDX(o, i, j);
-      if (!o->w[c]) { o->phix[c] = 0.0; o->phiy[c] = 0.0; o->gam[c] = 0.0; continue; }
+      if (!o->w[c]) { o->phix[c] = RL(0); o->phiy[c] = RL(0); o->gam[c] = RL(0); continue; }
       size_t e = c + sx, wv = c - sx, nn = c + sy, s = c - sy;
-      double PE = face_force(o->cP, o->eta[c], b[c], o->eta[e], b[e]);
-      double PW = face_force(o->cP, o->eta[wv], b[wv], o->eta[c], b[c]);
-      double PN = face_force(o->cP, o->eta[c], b[c], o->eta[nn], b[nn]);
-      double PS = face_force(o->cP, o->eta[s], b[s], o->eta[c], b[c]);
+      real PE = face_force(o->cP, o->eta[c], b[c], o->eta[e], b[e]);
+      real PW = face_force(o->cP, o->eta[wv], b[wv], o->eta[c], b[c]);
+      real PN = face_force(o->cP, o->eta[c], b[c], o->eta[nn], b[nn]);
+      real PS = face_force(o->cP, o->eta[s], b[s], o->eta[c], b[c]);
       o->phix[c] = -(PE + PW);
       o->phiy[c] = -(PN + PS);
       if (o->fields_fric) {
         /* friction field: c_gam = g n_M(x,y)^2 per cell (gamma = 0 where n_M = 0) */
-        double sp = sqrt(o->u[c] * o->u[c] + o->v[c] * o->v[c]);
-        o->gam[c] = (o->cg[c] * sp) * (o->r[c] * orc_icbrt(H[c]));
+        real sp = SQRT(o->u[c] * o->u[c] + o->v[c] * o->v[c]);
+        o->gam[c] = (o->cg[c] * sp) * (o->r[c] * r_icbrt(H[c]));
       } else if (fric) {
-        double sp = sqrt(o->u[c] * o->u[c] + o->v[c] * o->v[c]);
-        o->gam[c] = (o->cgam * sp) * (o->r[c] * orc_icbrt(H[c]));
+        real sp = SQRT(o->u[c] * o->u[c] + o->v[c] * o->v[c]);
+        o->gam[c] = (o->cgam * sp) * (o->r[c] * r_icbrt(H[c]));
       } else {
-        o->gam[c] = 0.0;
+        o->gam[c] = RL(0);
       }
     }
 
@@ -528,10 +602,10 @@ int orc_step_tau(orc_t* o, double tau) {
   for (int j = -G + 1; j < ny + G - 1; ++j)
     for (int i = -G + 1; i < nx + G - 1; ++i) {
       size_t c = IDX(o, i, j);
-      if (!o->w[c]) { o->Hh[c] = H[c]; o->ut[c] = 0.0; o->vt[c] = 0.0; continue; }
-      double div = ((o->u[c + sx] - o->u[c - sx]) + (o->v[c + sy] - o->v[c - sy])) * o->inv_2h;
-      o->Hh[c] = H[c] * (1.0 - theta * div);
-      double f = 1.0 / (1.0 + theta * o->gam[c]);
+      if (!o->w[c]) { o->Hh[c] = H[c]; o->ut[c] = RL(0); o->vt[c] = RL(0); continue; }
+      real div = ((o->u[c + sx] - o->u[c - sx]) + (o->v[c + sy] - o->v[c - sy])) * o->inv_2h;
+      o->Hh[c] = H[c] * (RL(1) - theta * div);
+      real f = RL(1) / (RL(1) + theta * o->gam[c]);
       o->ut[c] = ((Qx[c] + theta * o->phix[c]) * f) * o->r[c];
       o->vt[c] = ((Qy[c] + theta * o->phiy[c]) * f) * o->r[c];
     }
@@ -540,13 +614,13 @@ int orc_step_tau(orc_t* o, double tau) {
   for (int j = -G + 2; j < ny + G - 2; ++j)
     for (int i = -G + 2; i < nx + G - 2; ++i) {
       size_t c = IDX(o, i, j);
-      if (!o->w[c]) { o->phix2[c] = 0.0; o->phiy2[c] = 0.0; continue; }
+      if (!o->w[c]) { o->phix2[c] = RL(0); o->phiy2[c] = RL(0); continue; }
       size_t e = c + sx, wv = c - sx, nn = c + sy, s = c - sy;
-      double ec = o->Hh[c] + b[c];
-      double PE = face_force(o->cP, ec, b[c], o->Hh[e] + b[e], b[e]);
-      double PW = face_force(o->cP, o->Hh[wv] + b[wv], b[wv], ec, b[c]);
-      double PN = face_force(o->cP, ec, b[c], o->Hh[nn] + b[nn], b[nn]);
-      double PS = face_force(o->cP, o->Hh[s] + b[s], b[s], ec, b[c]);
+      real ec = o->Hh[c] + b[c];
+      real PE = face_force(o->cP, ec, b[c], o->Hh[e] + b[e], b[e]);
+      real PW = face_force(o->cP, o->Hh[wv] + b[wv], b[wv], ec, b[c]);
+      real PN = face_force(o->cP, ec, b[c], o->Hh[nn] + b[nn], b[nn]);
+      real PS = face_force(o->cP, o->Hh[s] + b[s], b[s], ec, b[c]);
       o->phix2[c] = -(PE + PW);
       o->phiy2[c] = -(PN + PS);
     }
@@ -555,8 +629,8 @@ int orc_step_tau(orc_t* o, double tau) {
   for (int j = 0; j < ny; ++j)
     for (int i = 0; i < nx; ++i) {
       size_t c = IDX(o, i, j);
-      if (!o->w[c]) { o->QLx[c] = 0.0; o->QLy[c] = 0.0; continue; }
-      double f = 1.0 / (1.0 + tau * o->gam[c]);
+      if (!o->w[c]) { o->QLx[c] = RL(0); o->QLy[c] = RL(0); continue; }
+      real f = RL(1) / (RL(1) + tau * o->gam[c]);
       o->QLx[c] = (Qx[c] + tau * o->phix2[c]) * f;
       o->QLy[c] = (Qy[c] + tau * o->phiy2[c]) * f;
     }
@@ -566,13 +640,13 @@ int orc_step_tau(orc_t* o, double tau) {
   for (int j = -G + 1; j < ny + G - 1; ++j)
     for (int i = -G + 1; i < nx + G - 1; ++i) {
       size_t c = IDX(o, i, j);
-      double jx, jy, ja;
-      orc_grass_m(cell_aj(o, c, H[c]), p->m_grass, o->ut[c], o->vt[c], &jx, &jy, &ja);
-      double s2 = o->ut[c] * o->ut[c] + o->vt[c] * o->vt[c];
-      if (orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh) && orc_bed_mobile(H[c], o->hbm)) {
+      real jx, jy, ja;
+      r_grass_m(cell_aj(o, c, H[c]), p->m_grass, o->ut[c], o->vt[c], &jx, &jy, &ja);
+      real s2 = o->ut[c] * o->ut[c] + o->vt[c] * o->vt[c];
+      if (r_shamov_gate(o->kappa, s2, H[c], o->C_Sh) && r_bed_mobile(H[c], o->hbm)) {
         o->J0x[c] = jx; o->J0y[c] = jy; o->J0a[c] = ja;
       } else {
-        o->J0x[c] = 0.0; o->J0y[c] = 0.0; o->J0a[c] = 0.0;
+        o->J0x[c] = RL(0); o->J0y[c] = RL(0); o->J0a[c] = RL(0);
       }
     }
 
@@ -581,73 +655,73 @@ int orc_step_tau(orc_t* o, double tau) {
    * x-faces: FH[(j, i)] is the face between cells (i-1, j) and (i, j). */
   for (int axis = 0; axis < 2; ++axis) {
     const size_t st = axis == 0 ? sx : sy;
-    const double* un = axis == 0 ? o->ut : o->vt;
-    const double* utn = axis == 0 ? o->vt : o->ut;
-    const double* J0n = axis == 0 ? o->J0x : o->J0y;
-    double* FH = axis == 0 ? o->FH : o->GH;
-    double* FQn = axis == 0 ? o->FQx : o->GQy;
-    double* FQt = axis == 0 ? o->FQy : o->GQx;
-    double* FJ = axis == 0 ? o->FJ : o->GJ;
+    const real* un = axis == 0 ? o->ut : o->vt;
+    const real* utn = axis == 0 ? o->vt : o->ut;
+    const real* J0n = axis == 0 ? o->J0x : o->J0y;
+    real* FH = axis == 0 ? o->FH : o->GH;
+    real* FQn = axis == 0 ? o->FQx : o->GQy;
+    real* FQt = axis == 0 ? o->FQy : o->GQx;
+    real* FJ = axis == 0 ? o->FJ : o->GJ;
     int i_end = axis == 0 ? nx + 1 : nx;
     int j_end = axis == 0 ? ny : ny + 1;
     for (int j = 0; j < j_end; ++j)
       for (int i = 0; i < i_end; ++i) {
         size_t R = IDX(o, i, j), L = R - st;
         size_t LL = L - st, RR = R + st;
-        double sL[4], sR[4];
-        const double* q[4] = {o->eta, H, un, utn};
+        real sL[4], sR[4];
+        const real* q[4] = {o->eta, H, un, utn};
         for (int k = 0; k < 4; ++k) {
-          sL[k] = orc_minmod(q[k][L] - q[k][LL], q[k][R] - q[k][L]);
-          sR[k] = orc_minmod(q[k][R] - q[k][L], q[k][RR] - q[k][R]);
+          sL[k] = r_minmod(q[k][L] - q[k][LL], q[k][R] - q[k][L]);
+          sR[k] = r_minmod(q[k][R] - q[k][L], q[k][RR] - q[k][R]);
         }
-        double qm[4], qp[4];
+        real qm[4], qp[4];
         for (int k = 0; k < 4; ++k) {
-          qm[k] = q[k][L] + 0.5 * sL[k];
-          qp[k] = q[k][R] - 0.5 * sR[k];
+          qm[k] = q[k][L] + RL(0.5) * sL[k];
+          qp[k] = q[k][R] - RL(0.5) * sR[k];
         }
-        double F[3];
-        orc_hll_face(p->g, qm[0], qm[1], qm[2], qm[3], qp[0], qp[1], qp[2], qp[3],
-                     o->w[L], o->w[R], F);
+        real F[3];
+        r_hll_face(o->g, qm[0], qm[1], qm[2], qm[3], qp[0], qp[1], qp[2], qp[3],
+                   o->w[L], o->w[R], F);
         FH[R] = F[0]; FQn[R] = F[1]; FQt[R] = F[2];
         /* sediment face flux: donor by sign of u~_n,L + u~_n,R; tie averages */
-        double Jn, Ja;
+        real Jn, Ja;
         if (!o->w[L] && !o->w[R]) {
-          FJ[R] = 0.0;
+          FJ[R] = RL(0);
           continue;
         }
-        double us = un[L] + un[R];
-        if (us > 0.0) { Jn = J0n[L]; Ja = o->J0a[L]; }
-        else if (us < 0.0) { Jn = J0n[R]; Ja = o->J0a[R]; }
-        else { Jn = 0.5 * (J0n[L] + J0n[R]); Ja = 0.5 * (o->J0a[L] + o->J0a[R]); }
-        FJ[R] = orc_slope_flux(Jn, Ja, p->C_J, (b[R] - b[L]) * o->inv_h);
+        real us = un[L] + un[R];
+        if (us > RL(0)) { Jn = J0n[L]; Ja = o->J0a[L]; }
+        else if (us < RL(0)) { Jn = J0n[R]; Ja = o->J0a[R]; }
+        else { Jn = RL(0.5) * (J0n[L] + J0n[R]); Ja = RL(0.5) * (o->J0a[L] + o->J0a[R]); }
+        FJ[R] = r_slope_flux(Jn, Ja, o->C_J, (b[R] - b[L]) * o->inv_h);
       }
   }
 
   /* Step 8 -- K8 (Eq.1, Eq.6): conservative update */
   int neg = 0;
-  const double src = p->q_plus - p->q_minus;
+  const real src = o->src;
   for (int j = 0; j < ny; ++j)
     for (int i = 0; i < nx; ++i) {
       size_t c = IDX(o, i, j);
       size_t e = c + sx, n = c + sy;
-      double dH = (o->FH[e] - o->FH[c]) + (o->GH[n] - o->GH[c]);
-      double dQx = (o->FQx[e] - o->FQx[c]) + (o->GQx[n] - o->GQx[c]);
-      double dQy = (o->FQy[e] - o->FQy[c]) + (o->GQy[n] - o->GQy[c]);
-      double dJ = (o->FJ[e] - o->FJ[c]) + (o->GJ[n] - o->GJ[c]);
-      double Hn = H[c] - lam * dH;
-      double Qxn = o->QLx[c] - lam * dQx;
-      double Qyn = o->QLy[c] - lam * dQy;
+      real dH = (o->FH[e] - o->FH[c]) + (o->GH[n] - o->GH[c]);
+      real dQx = (o->FQx[e] - o->FQx[c]) + (o->GQx[n] - o->GQx[c]);
+      real dQy = (o->FQy[e] - o->FQy[c]) + (o->GQy[n] - o->GQy[c]);
+      real dJ = (o->FJ[e] - o->FJ[c]) + (o->GJ[n] - o->GJ[c]);
+      real Hn = H[c] - lam * dH;
+      real Qxn = o->QLx[c] - lam * dQx;
+      real Qyn = o->QLy[c] - lam * dQy;
       if (o->fields_src) {
         /* sigma = s - beta H (reading #21): source explicit, absorption implicit,
          * H' = ((H - lam dF) + tau s) / (1 + tau beta); momenta scaled alike */
-        double a = 1.0 / (1.0 + tau * o->beta[c]);
+        real a = RL(1) / (RL(1) + tau * o->beta[c]);
         Hn = (Hn + tau * o->srcf[c]) * a;
         Qxn = Qxn * a;
         Qyn = Qyn * a;
       }
-      double bn = (b[c] - (lam * W[c]) * dJ) + (tau * W[c]) * src;
-      if (!(Hn > eps)) { Qxn = 0.0; Qyn = 0.0; }
-      if (Hn < -p->neg_tol) neg = 1;
+      real bn = (b[c] - (lam * W[c]) * dJ) + (tau * W[c]) * src;
+      if (!(Hn > eps)) { Qxn = RL(0); Qyn = RL(0); }
+      if (Hn < -o->neg_tol) neg = 1;
       o->Hn[c] = Hn; o->Qxn[c] = Qxn; o->Qyn[c] = Qyn; o->bn[c] = bn;
     }
   for (int j = 0; j < ny; ++j)
@@ -659,8 +733,8 @@ int orc_step_tau(orc_t* o, double tau) {
 
   /* Step 9: maxima for the next step's Eq.7 */
   reduce_M(o, H, Qx, Qy, o->M);
-  o->t += tau;
-  o->last_dt = tau;
+  o->t += tau_d;
+  o->last_dt = tau_d;
   o->steps += 1;
   return neg ? ORC_ENEGDEPTH : ORC_OK;
 }
@@ -698,7 +772,7 @@ int orc_get_debug(const orc_t* o, const char* name, double* out) {
     for (size_t k = 0; k < n; ++k) out[k] = o->w[k];
     return ORC_OK;
   }
-  struct { const char* nm; const double* a; } tab[] = {
+  struct { const char* nm; const real* a; } tab[] = {
       {"eta", o->eta}, {"u", o->u}, {"v", o->v}, {"phix", o->phix}, {"phiy", o->phiy},
       {"gam", o->gam}, {"Hh", o->Hh}, {"ut", o->ut}, {"vt", o->vt}, {"phix2", o->phix2},
       {"phiy2", o->phiy2}, {"QLx", o->QLx}, {"QLy", o->QLy}, {"J0x", o->J0x},
@@ -707,7 +781,7 @@ int orc_get_debug(const orc_t* o, const char* name, double* out) {
       {"W", o->W}};
   for (size_t k = 0; k < sizeof(tab) / sizeof(tab[0]); ++k)
     if (strcmp(name, tab[k].nm) == 0) {
-      memcpy(out, tab[k].a, n * 8);
+      for (size_t q = 0; q < n; ++q) out[q] = tab[k].a[q];
       return ORC_OK;
     }
   return ORC_EINVAL;

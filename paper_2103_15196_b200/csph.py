@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.environ.get("CSPH_LIB_DEV") or os.path.join(_HERE, "libcsph.so")  # dev A/B knob
+SO_PATH = os.path.join(_HERE, "libcsph.so")
 
 CSPH_OK, CSPH_EINVAL, CSPH_ENOSTATE, CSPH_ENOMEM, CSPH_ECUDA, CSPH_ENCCL = 0, -1, -2, -3, -4, -5
 CSPH_ENEGDEPTH, CSPH_ENONFINITE, CSPH_EDRY = -6, -7, -8
@@ -41,7 +41,8 @@ class csph_params(ctypes.Structure):
         ("q_plus", ctypes.c_double), ("q_minus", ctypes.c_double), ("precision", ctypes.c_int),
         ("device", ctypes.c_int), ("path", ctypes.c_int), ("tile_rows", ctypes.c_int),
         ("hgs", ctypes.c_int), ("aj_mode", ctypes.c_int), ("s_rel", ctypes.c_double),
-        ("open_bc", ctypes.c_int),
+        ("open_bc", ctypes.c_int), ("graphs", ctypes.c_int), ("h_bed_min", ctypes.c_double),
+        ("m_real", ctypes.c_double),
     ]
 
 

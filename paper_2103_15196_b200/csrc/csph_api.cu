@@ -160,7 +160,7 @@ struct csph {
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   long long graph_kernels = 0;  // kernel launches inside one pair graph
   cudaStream_t cap = nullptr;   // private capture stream (the handle's may be the legacy default)
-  bool graphs = getenv("CSPH_NO_GRAPHS") == nullptr;
+  bool graphs = true;  // csph_params.graphs
 };
 
 static void graphs_reset(csph* H) {
@@ -181,7 +181,6 @@ static void graphs_free(csph* H) {
 
 namespace {
 
-constexpr int kStatusFlagNeg = 1;
 constexpr int kTyMin = 16;  // finest automatic tiling (rows)
 
 __global__ void ctrl_kernel(Ctrl* C, unsigned long long* gM, double* Mlast, double* dtlog,
@@ -192,7 +191,7 @@ __global__ void ctrl_kernel(Ctrl* C, unsigned long long* gM, double* Mlast, doub
       C->parity ^= 1;
       C->step += 1;
       C->t += C->tau;
-      if (C->flags & kStatusFlagNeg) C->status = CSPH_ENEGDEPTH;
+      if (gM[3]) C->status = CSPH_ENEGDEPTH;  // any strip / rank (combined in gM[3])
     }
   }
   double M[3];
@@ -201,6 +200,7 @@ __global__ void ctrl_kernel(Ctrl* C, unsigned long long* gM, double* Mlast, doub
     Mlast[k] = M[k];
     gM[k] = 0ull;
   }
+  gM[3] = 0ull;
   if (C->status) return;
   if (!isfinite(M[0]) || !isfinite(M[1]) || !isfinite(M[2])) {
     C->status = CSPH_ENONFINITE;
@@ -395,7 +395,7 @@ __global__ void to_f64_kernel(double* dst, const float* src, size_t n) {
 
 __global__ void max_gather_kernel(unsigned long long* dst, const unsigned long long* src,
                                   int n) {
-  if (threadIdx.x < 3) {
+  if (threadIdx.x < 4) {  // the 3 Eq.7 maxima and the negative-depth flag
     unsigned long long m = 0;
     for (int k = 0; k < n; ++k) {
       unsigned long long v = src[4 * k + threadIdx.x];
@@ -407,10 +407,7 @@ __global__ void max_gather_kernel(unsigned long long* dst, const unsigned long l
 
 __global__ void init_ctrl_kernel(Ctrl* C) {
   C->tau = 0.0; C->t = 0.0; C->step = 0; C->lim = -1; C->status = 0; C->parity = 0;
-  C->flags = 0;
 }
-
-__global__ void clear_flags_kernel(Ctrl* C) { C->flags = 0; }
 
 // Self-test of the branch-free reciprocal / square root against IEEE / and sqrt
 // on counter-hashed positive normal inputs with exponents in [-lo, +lo].
@@ -488,6 +485,7 @@ static Phys make_phys(double dx, const csph_params& p) {
   P.aj0 = 0.05 * ((p.n_manning * p.n_manning) * p.n_manning);
   P.sm1 = p.s_rel - 1.0;
   P.d50 = p.d50;
+  P.hbm = p.h_bed_min < 0.0 ? p.d50 : p.h_bed_min;  // reading #31 film cut-off depth
   return P;
 }
 
@@ -518,6 +516,10 @@ static int check_params(int nx, int ny, double dx, const csph_params* p) {
                 "precision 32 (NEXT-2) runs the fused path with walls, m_grass = 2, constant A_J");
   if (p->path != CSPH_PATH_FUSED && p->path != CSPH_PATH_STAGED) return fail(CSPH_EINVAL, "path");
   if (p->open_bc < 0 || p->open_bc > 15) return fail(CSPH_EINVAL, "open_bc is a 4-bit mask");
+  if (std::isnan(p->h_bed_min) || !(p->h_bed_min < INFINITY))
+    return fail(CSPH_EINVAL, "h_bed_min must be finite (< 0 selects d50)");
+  if (!(p->m_real < 0.0)) return fail(CSPH_EINVAL, "m_real (non-integer Grass exponent) is not "
+                                                   "built yet: leave it < 0");
   return CSPH_OK;
 }
 
@@ -538,7 +540,10 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
   StripView& v = s.v;
   v.nx = H->nx;
   v.ny = rows;
-  v.pitch = ((H->nx + GX + 3) + 31) / 32 * 32;
+  // padded row: GX left + nx + 3 right ghosts, plus slack so that the fused kernel's TMA row
+  // copies (rounded up to 16 B: up to 3 fp32 / 1 fp64 element past the last ghost) stay
+  // inside the row; rounded up to 32 elements (256 B)
+  v.pitch = ((H->nx + GX + 3 + 4) + 31) / 32 * 32;
   // y edges: 0 halo (interior strip edge), 1 wall, 2 open; x edges: 1 wall, 2 open
   const int ob = H->p.open_bc;
   v.wall_lo = gj0 == 0 ? ((ob & 4) ? 2 : 1) : 0;
@@ -561,6 +566,7 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
     CK(cudaMemset(v.b[k], 0, n * 8));
   }
   if ((st = dalloc(s, (void**)&s.ctrl, sizeof(Ctrl)))) return st;
+  CK(cudaMemset(s.ctrl, 0, sizeof(Ctrl)));  // padding bytes too (they travel to the host)
   if ((st = dalloc(s, (void**)&s.gM, 4 * sizeof(unsigned long long)))) return st;
   if ((st = dalloc(s, (void**)&s.Mlast, 4 * sizeof(double)))) return st;
   if ((st = dalloc(s, (void**)&s.dtlog, LOGCAP * sizeof(double)))) return st;
@@ -680,6 +686,9 @@ void csph_default_params(csph_params* p) {
   p->aj_mode = 0;
   p->s_rel = 2.65;
   p->open_bc = 0;
+  p->graphs = 1;
+  p->h_bed_min = -1.0;
+  p->m_real = -1.0;
 }
 
 const char* csph_last_error(void) { return g_err.c_str(); }
@@ -725,6 +734,7 @@ static csph* make_handle(int nx, int ny, double dx, const csph_params* p) {
   H->dx = dx;
   H->p = *p;
   H->P = make_phys(dx, *p);
+  H->graphs = p->graphs != 0;
   return H;
 }
 
@@ -1004,58 +1014,147 @@ int csph_get_profile(csph_t* H, double* ms, long long* steps) {
 
 // -------- collective pieces of a step
 
-// NCCL halo exchange of buffer q: the 3 owned edge rows of each field (full padded
-// width, so x-ghosts travel too) to ranks r-1 / r+1 and the neighbours' rows into
-// the ghost rows.  No wrap-around (reading #18).
+// Where the halo of a strip lives (one place for the NCCL and the peer-copy transports,
+// so the multi-strip tests on one GPU exercise the offsets the NCCL path uses).
+// State rows, in elements of the padded layout, full padded width from column -GX (so the
+// x-ghosts travel too): the 3 owned rows sent to the neighbour below (send_lo, rows
+// 0..2) or above (send_hi, rows ny-3..ny-1) and the 3 ghost rows received from it
+// (recv_lo, rows -3..-1; recv_hi, rows ny..ny+2).  HGS tile flags of parity q: my first
+// tile row goes below, my last above; the neighbours' facing rows land in gflag.
+struct HaloMap {
+  size_t count;  // elements per field and side
+  size_t send_lo, recv_lo, send_hi, recv_hi;
+  size_t fsend_lo, fsend_hi;  // into s.tflag
+  size_t frecv_lo, frecv_hi;  // into s.gflag
+};
+
+static HaloMap halo_map(const Strip& s, int q) {
+  const StripView& v = s.v;
+  HaloMap m;
+  m.count = (size_t)GY * v.pitch;
+  m.send_lo = off(v.pitch, -GX, 0);
+  m.recv_lo = off(v.pitch, -GX, -GY);
+  m.send_hi = off(v.pitch, -GX, v.ny - GY);
+  m.recv_hi = off(v.pitch, -GX, v.ny);
+  const size_t nt = (size_t)s.ntx * s.nty;
+  m.fsend_lo = nt * (size_t)q;
+  m.fsend_hi = nt * (size_t)q + (size_t)(s.nty - 1) * s.ntx;
+  m.frecv_lo = 2 * (size_t)s.ntx * (size_t)q;
+  m.frecv_hi = m.frecv_lo + s.ntx;
+  return m;
+}
+
+static void state_fields(const StripView& v, int q, char* f[4]) {
+  f[0] = (char*)v.H[q]; f[1] = (char*)v.Qx[q]; f[2] = (char*)v.Qy[q]; f[3] = (char*)v.b[q];
+}
+
+// NCCL halo exchange of buffer q with ranks r-1 / r+1 (no wrap-around, reading #18).
 static int halo_nccl(csph* H, int q, cudaStream_t stream) {
+  if (H->nranks == 1) return CSPH_OK;
   Strip& s = H->s[0];
   const StripView& v = s.v;
-  const size_t cnt = (size_t)GY * v.pitch;
+  const HaloMap m = halo_map(s, q);
   const size_t es = (size_t)v.prec;  // element size: fp64 or fp32 state
   const ncclDataType_t dt = v.prec == 4 ? ncclFloat32 : ncclFloat64;
-  char* f[4] = {(char*)v.H[q], (char*)v.Qx[q], (char*)v.Qy[q], (char*)v.b[q]};
-  if (H->nranks == 1) return CSPH_OK;
-  // tile-row flags of the new state (parity q): my first row goes to r-1 (its ghi), my
-  // last to r+1 (its glo)
-  const size_t nt = (size_t)s.ntx * s.nty;
-  unsigned char* fq = s.tflag + nt * (size_t)q;
-  unsigned char* gq = s.gflag + 2 * (size_t)s.ntx * (size_t)q;
+  char* f[4];
+  state_fields(v, q, f);
+  const bool lo = H->rank > 0, hi = H->rank < H->nranks - 1;
   NK(g_nccl.GroupStart());
-  if (H->rank > 0) {
-    NK(g_nccl.Send(fq, s.ntx, ncclUint8, H->rank - 1, H->comm, stream));
-    NK(g_nccl.Recv(gq, s.ntx, ncclUint8, H->rank - 1, H->comm, stream));
+  if (lo) {
+    NK(g_nccl.Send(s.tflag + m.fsend_lo, s.ntx, ncclUint8, H->rank - 1, H->comm, stream));
+    NK(g_nccl.Recv(s.gflag + m.frecv_lo, s.ntx, ncclUint8, H->rank - 1, H->comm, stream));
   }
-  if (H->rank < H->nranks - 1) {
-    NK(g_nccl.Send(fq + (size_t)(s.nty - 1) * s.ntx, s.ntx, ncclUint8, H->rank + 1, H->comm,
-                   stream));
-    NK(g_nccl.Recv(gq + s.ntx, s.ntx, ncclUint8, H->rank + 1, H->comm, stream));
+  if (hi) {
+    NK(g_nccl.Send(s.tflag + m.fsend_hi, s.ntx, ncclUint8, H->rank + 1, H->comm, stream));
+    NK(g_nccl.Recv(s.gflag + m.frecv_hi, s.ntx, ncclUint8, H->rank + 1, H->comm, stream));
   }
   for (int k = 0; k < 4; ++k) {
-    if (H->rank > 0) {
-      NK(g_nccl.Send(f[k] + es * off(v.pitch, -GX, 0), cnt, dt, H->rank - 1, H->comm, stream));
-      NK(g_nccl.Recv(f[k] + es * off(v.pitch, -GX, -GY), cnt, dt, H->rank - 1, H->comm, stream));
+    if (lo) {
+      NK(g_nccl.Send(f[k] + es * m.send_lo, m.count, dt, H->rank - 1, H->comm, stream));
+      NK(g_nccl.Recv(f[k] + es * m.recv_lo, m.count, dt, H->rank - 1, H->comm, stream));
     }
-    if (H->rank < H->nranks - 1) {
-      NK(g_nccl.Send(f[k] + es * off(v.pitch, -GX, v.ny - GY), cnt, dt, H->rank + 1, H->comm,
-                     stream));
-      NK(g_nccl.Recv(f[k] + es * off(v.pitch, -GX, v.ny), cnt, dt, H->rank + 1, H->comm, stream));
+    if (hi) {
+      NK(g_nccl.Send(f[k] + es * m.send_hi, m.count, dt, H->rank + 1, H->comm, stream));
+      NK(g_nccl.Recv(f[k] + es * m.recv_hi, m.count, dt, H->rank + 1, H->comm, stream));
     }
   }
   NK(g_nccl.GroupEnd());
   return CSPH_OK;
 }
 
-// Eq.7 maxima over all ranks: max of the u64 bit patterns (exact, order-free).
-static int allreduce_nccl(csph* H, cudaStream_t stream) {
-  Strip& s = H->s[0];
-  NK(g_nccl.AllReduce(s.gM, s.gM, 3, ncclUint64, ncclMax, H->comm, stream));
+// The same exchange between strips of one process (MULTI): strip r pulls its ghost rows
+// and ghost flags from r-1 / r+1 with peer copies on `stream` (its own device current).
+static int halo_peer(csph* H, int r, int q, cudaStream_t stream) {
+  Strip& s = H->s[r];
+  const int n = (int)H->s.size();
+  const HaloMap m = halo_map(s, q);
+  const size_t es = (size_t)s.v.prec;
+  char* f[4];
+  state_fields(s.v, q, f);
+  if (r > 0) {  // my ghost rows below <- the last owned rows of r-1
+    const Strip& o = H->s[r - 1];
+    const HaloMap mo = halo_map(o, q);
+    char* g[4];
+    state_fields(o.v, q, g);
+    for (int k = 0; k < 4; ++k)
+      CK(cudaMemcpyPeerAsync(f[k] + es * m.recv_lo, s.dev, g[k] + es * mo.send_hi, o.dev,
+                             m.count * es, stream));
+    CK(cudaMemcpyPeerAsync(s.gflag + m.frecv_lo, s.dev, o.tflag + mo.fsend_hi, o.dev,
+                           (size_t)s.ntx, stream));
+  }
+  if (r < n - 1) {  // my ghost rows above <- the first owned rows of r+1
+    const Strip& o = H->s[r + 1];
+    const HaloMap mo = halo_map(o, q);
+    char* g[4];
+    state_fields(o.v, q, g);
+    for (int k = 0; k < 4; ++k)
+      CK(cudaMemcpyPeerAsync(f[k] + es * m.recv_hi, s.dev, g[k] + es * mo.send_lo, o.dev,
+                             m.count * es, stream));
+    CK(cudaMemcpyPeerAsync(s.gflag + m.frecv_hi, s.dev, o.tflag + mo.fsend_lo, o.dev,
+                           (size_t)s.ntx, stream));
+  }
   return CSPH_OK;
 }
 
-// Halo exchange of buffer q (3 owned edge rows x 4 fields, full padded width)
-// and the maxima combine.  NCCL for DIST, peer copies for MULTI.
+// Eq.7 maxima and the negative-depth flag over all ranks: max of the u64 bit patterns
+// (exact, order-free).
+static int allreduce_nccl(csph* H, cudaStream_t stream) {
+  Strip& s = H->s[0];
+  NK(g_nccl.AllReduce(s.gM, s.gM, 4, ncclUint64, ncclMax, H->comm, stream));
+  return CSPH_OK;
+}
+
+// MULTI: combine the 4 accumulator slots of every strip on strip 0 and send the result
+// back, after each strip's `ready` event; each strip's stream then continues after it.
+static int gather_multi(csph* H, cudaEvent_t Strip::*ready) {
+  const int n = (int)H->s.size();
+  Strip& s0 = H->s[0];
+  CK(cudaSetDevice(s0.dev));
+  for (int r = 0; r < n; ++r) {
+    CK(cudaStreamWaitEvent(s0.st, H->s[r].*ready, 0));
+    CK(cudaMemcpyPeerAsync(H->gather + 4 * r, s0.dev, H->s[r].gM, H->s[r].dev,
+                           4 * sizeof(unsigned long long), s0.st));
+  }
+  max_gather_kernel<<<1, 32, 0, s0.st>>>(s0.gM, H->gather, n);
+  H->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(s0.ev, s0.st));
+  for (int r = 1; r < n; ++r) {
+    Strip& s = H->s[r];
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamWaitEvent(s.st, s0.ev, 0));
+    CK(cudaMemcpyPeerAsync(s.gM, s.dev, s0.gM, s0.dev, 4 * sizeof(unsigned long long), s.st));
+    CK(cudaEventRecord(s.ev, s.st));
+  }
+  // strip 0's ctrl kernel clears s0.gM: only after every strip has taken its copy
+  CK(cudaSetDevice(s0.dev));
+  for (int r = 1; r < n; ++r) CK(cudaStreamWaitEvent(s0.st, H->s[r].ev, 0));
+  return CSPH_OK;
+}
+
+// Halo exchange of buffer q and the maxima combine, all on the strips' main streams
+// (staged path and set_state).  NCCL for DIST, peer copies for MULTI.
 static int exchange(csph* H, int q) {
-  const size_t rowbytes = (size_t)H->s[0].v.pitch * 8;
   if (H->mode == DIST) {
     int st = halo_nccl(H, q, H->s[0].st);
     if (st) return st;
@@ -1067,49 +1166,14 @@ static int exchange(csph* H, int q) {
       CK(cudaSetDevice(H->s[r].dev));
       CK(cudaEventRecord(H->s[r].ev, H->s[r].st));
     }
-    Strip& s0 = H->s[0];
-    CK(cudaSetDevice(s0.dev));
-    for (int r = 0; r < n; ++r) {
-      CK(cudaStreamWaitEvent(s0.st, H->s[r].ev, 0));
-      CK(cudaMemcpyPeerAsync(H->gather + 4 * r, s0.dev, H->s[r].gM, H->s[r].dev,
-                             4 * sizeof(unsigned long long), s0.st));
-    }
-    max_gather_kernel<<<1, 32, 0, s0.st>>>(s0.gM, H->gather, n);
-    H->launches += 1;
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(s0.ev, s0.st));
+    int st = gather_multi(H, &Strip::ev);
+    if (st) return st;
+    // every strip's state of buffer q is final (gather waited for all): pull the halos
     for (int r = 0; r < n; ++r) {
       Strip& s = H->s[r];
       CK(cudaSetDevice(s.dev));
-      CK(cudaStreamWaitEvent(s.st, s0.ev, 0));
-      if (r > 0)
-        CK(cudaMemcpyPeerAsync(s.gM, s.dev, s0.gM, s0.dev, 3 * sizeof(unsigned long long), s.st));
-      const StripView& v = s.v;
-      const size_t es = (size_t)v.prec;
-      const size_t bytes = (size_t)GY * v.pitch * es;
-      char* f[4] = {(char*)v.H[q], (char*)v.Qx[q], (char*)v.Qy[q], (char*)v.b[q]};
-      unsigned char* gq = s.gflag + 2 * (size_t)s.ntx * (size_t)q;
-      if (r > 0) {
-        const Strip& o = H->s[r - 1];
-        const char* g[4] = {(const char*)o.v.H[q], (const char*)o.v.Qx[q], (const char*)o.v.Qy[q],
-                            (const char*)o.v.b[q]};
-        for (int k = 0; k < 4; ++k)
-          CK(cudaMemcpyPeerAsync(f[k] + es * off(v.pitch, -GX, -GY), s.dev,
-                                 g[k] + es * off(o.v.pitch, -GX, o.v.ny - GY), o.dev, bytes, s.st));
-        // the neighbour's last tile row of flags (parity q) -> my glo
-        const unsigned char* of = o.tflag + (size_t)o.ntx * o.nty * q + (size_t)(o.nty - 1) * o.ntx;
-        CK(cudaMemcpyPeerAsync(gq, s.dev, of, o.dev, (size_t)s.ntx, s.st));
-      }
-      if (r < n - 1) {
-        const Strip& o = H->s[r + 1];
-        const char* g[4] = {(const char*)o.v.H[q], (const char*)o.v.Qx[q], (const char*)o.v.Qy[q],
-                            (const char*)o.v.b[q]};
-        for (int k = 0; k < 4; ++k)
-          CK(cudaMemcpyPeerAsync(f[k] + es * off(v.pitch, -GX, v.ny), s.dev,
-                                 g[k] + es * off(o.v.pitch, -GX, 0), o.dev, bytes, s.st));
-        const unsigned char* of = o.tflag + (size_t)o.ntx * o.nty * q;  // its first tile row
-        CK(cudaMemcpyPeerAsync(gq + s.ntx, s.dev, of, o.dev, (size_t)s.ntx, s.st));
-      }
+      if (r == 0) CK(cudaStreamWaitEvent(s.st, H->s[0].ev, 0));
+      if ((st = halo_peer(H, r, q, s.st))) return st;
     }
     // every strip must finish reading its neighbours before they run ahead
     for (int r = 0; r < n; ++r) {
@@ -1121,8 +1185,6 @@ static int exchange(csph* H, int q) {
       if (r > 0) CK(cudaStreamWaitEvent(H->s[r].st, H->s[r - 1].ev, 0));
       if (r < n - 1) CK(cudaStreamWaitEvent(H->s[r].st, H->s[r + 1].ev, 0));
     }
-    (void)rowbytes;
-    return CSPH_OK;
   }
   return CSPH_OK;
 }
@@ -1308,7 +1370,7 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
   }
   if (H->mode == DIST) {
     Strip& s = H->s[0];
-    NK(g_nccl.AllReduce(s.gM, s.gM, 3, ncclUint64, ncclMax, H->comm, s.st));
+    NK(g_nccl.AllReduce(s.gM, s.gM, 4, ncclUint64, ncclMax, H->comm, s.st));
   } else if (H->mode == MULTI) {
     if ((st = exchange(H, 0))) return st;  // also refreshes halos of buffer 0
   }
@@ -1399,6 +1461,11 @@ int csph_set_fields_rows(csph_t* H, int j_begin, int j_end, const double* n_mann
     v.beta = bt;
     v.src = sr;
     v.aj0 = aj;
+    // new source fields change which dry tiles are identities: every tile marches again
+    // (tstate >= 2 would skip tiles whose two buffers differ once sources stop)
+    CK(cudaMemsetAsync(s.tflag, HGS_ALL, 2 * s.tflag_cap, s.st));
+    CK(cudaMemsetAsync(s.tstate, 0, s.tflag_cap, s.st));
+    CK(cudaMemsetAsync(s.gflag, HGS_ALL, 4 * (size_t)s.ntx, s.st));
   }
   H->P.fric = H->p.n_manning > 0.0 || has_n;
   return CSPH_OK;
@@ -1435,8 +1502,6 @@ static Hgs hgs_of(const csph* H, const Strip& s) {
 // One step of a single-grid handle: the 3 launches (clear flags, step kernel(s), ctrl)
 // reading buffer host_parity.  Used directly and inside the CUDA-graph capture.
 static int single_step(csph* H, Strip& s) {
-  clear_flags_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
-  H->launches += 1;
   if (H->p.path == CSPH_PATH_STAGED) {
     launch_staged_step(s.v, s.ctrl, s.scr, H->P, s.gM, s.st, &H->launches);
     launch_mirror(s.v, s.ctrl, 1, s.st, &H->launches);
@@ -1487,6 +1552,95 @@ static int graph_pair(csph* H, Strip& s, long long* per_launch) {
   return CSPH_OK;
 }
 
+// The boundary tile rows of a strip, [0, lo) and [hi, ny), hold the GY rows each
+// neighbour needs; the halo exchange starts after them and overlaps the interior
+// [lo, hi).  Both are whole tile rows (the HGS tiling), and the last one must hold at
+// least GY rows: a short last tile (ny % ty in {1, 2}) is merged with the one before it,
+// else rows the neighbour receives would still be in flight in the interior launch.
+// false: no interior tile row, the strip is launched whole before the exchange.
+static bool edge_split(const Strip& s, int* lo, int* hi) {
+  const int ny = s.v.ny, ty = s.ty;
+  int l = ty, h = (s.nty - 1) * ty;
+  if (ny - h < GY) h -= ty;
+  if (s.nty < 3 || h <= l) return false;
+  *lo = l;
+  *hi = h;
+  return true;
+}
+
+// One step of a DIST or MULTI handle on the fused path: edge tile rows, then the halo
+// exchange of buffer q on the comm streams (NCCL send/recv or peer copies) overlapped
+// with the interior, then the combine of the Eq.7 maxima and the negative-depth flag, and
+// the ctrl kernel once the halo has landed.
+static int split_step(csph* H, int n, int q) {
+  const int ns = (int)H->s.size();
+  std::vector<int> lo(ns, 0), hi(ns, 0);
+  std::vector<char> sp(ns, 0);
+  for (int r = 0; r < ns; ++r) {  // 1. edge tile rows
+    Strip& s = H->s[r];
+    CK(cudaSetDevice(s.dev));
+    const Hgs hg = hgs_of(H, s);
+    if (H->profiling && r == 0) CK(cudaEventRecord(H->evs[2 * n], s.st));
+    sp[r] = edge_split(s, &lo[r], &hi[r]);
+    if (sp[r]) {
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, lo[r], s.ty, hg, s.st, &H->launches);
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, hi[r], s.v.ny, s.ty, hg, s.st, &H->launches);
+    } else {
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, s.ty, hg, s.st, &H->launches);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s.ev_edge, s.st));
+  }
+  int st;
+  for (int r = 0; r < ns; ++r) {  // 2. halo exchange on the comm streams
+    Strip& s = H->s[r];
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamWaitEvent(s.cst, s.ev_edge, 0));
+    if (H->mode == DIST) {
+      if ((st = halo_nccl(H, q, s.cst))) return st;
+    } else {
+      if (r > 0) CK(cudaStreamWaitEvent(s.cst, H->s[r - 1].ev_edge, 0));
+      if (r < ns - 1) CK(cudaStreamWaitEvent(s.cst, H->s[r + 1].ev_edge, 0));
+      if ((st = halo_peer(H, r, q, s.cst))) return st;
+      CK(cudaEventRecord(s.ev_comm, s.cst));
+    }
+  }
+  for (int r = 0; r < ns; ++r) {  // 3. interior tile rows
+    Strip& s = H->s[r];
+    CK(cudaSetDevice(s.dev));
+    if (sp[r])
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, lo[r], hi[r], s.ty, hgs_of(H, s), s.st,
+                        &H->launches);
+    if (H->profiling && r == 0) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s.ev_int, s.st));
+  }
+  if (H->mode == DIST) {  // 4. combine, then ctrl after the halo and the allreduce
+    Strip& s = H->s[0];
+    CK(cudaStreamWaitEvent(s.cst, s.ev_int, 0));
+    if ((st = allreduce_nccl(H, s.cst))) return st;
+    CK(cudaEventRecord(s.ev_comm, s.cst));
+    CK(cudaStreamWaitEvent(s.st, s.ev_comm, 0));
+  } else {
+    if ((st = gather_multi(H, &Strip::ev_int))) return st;
+    // ctrl (and the next step) after my halo landed and my neighbours finished reading
+    // my edge rows of buffer q (the step after next overwrites them)
+    for (int r = 0; r < ns; ++r) {
+      Strip& s = H->s[r];
+      CK(cudaSetDevice(s.dev));
+      for (int o = r - 1; o <= r + 1; ++o)
+        if (o >= 0 && o < ns) CK(cudaStreamWaitEvent(s.st, H->s[o].ev_comm, 0));
+    }
+  }
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 1);
+    H->launches += 1;
+    CK(cudaGetLastError());
+  }
+  return CSPH_OK;
+}
+
 int csph_step(csph_t* H, int nsteps) {
   if (!H) return fail(CSPH_EINVAL, "handle is NULL");
   if (nsteps < 0) return fail(CSPH_EINVAL, "nsteps < 0");
@@ -1500,40 +1654,14 @@ int csph_step(csph_t* H, int nsteps) {
       H->evs.push_back(e);
     }
   }
-  // (a single rank takes the same split-launch path -- its NCCL calls are no-ops -- so the
-  // launch sequence of the multi-GPU step is exercised on one GPU)
-  const bool overlap = H->mode == DIST && H->p.path == CSPH_PATH_FUSED && H->s[0].nty >= 2;
+  // DIST and MULTI (fused path): boundary tile rows first, their halo exchange overlapped
+  // with the interior (a single rank takes the same path; its NCCL calls are no-ops)
+  const bool split = H->mode != SINGLE && H->p.path == CSPH_PATH_FUSED;
   for (int n = 0; n < nsteps; ++n) {
     const int q = H->host_parity ^ 1;
-    if (overlap) {
-      // boundary rows first; their halo exchange (NCCL stream) overlaps the interior
-      // boundary tile rows first (aligned to the HGS tiling), then the interior
-      Strip& s = H->s[0];
-      const int ny = s.v.ny, ty = s.ty;
-      const Hgs hg = hgs_of(H, s);
-      const int lo = ty < ny ? ty : ny, hi = (s.nty - 1) * ty;
-      clear_flags_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
-      H->launches += 1;
-      if (H->profiling) CK(cudaEventRecord(H->evs[2 * n], s.st));
-      launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, lo, ty, hg, s.st, &H->launches);
-      // last tile row (nty >= 2, so hi >= lo: with 2 tile rows there is no interior)
-      launch_fused_step(s.v, s.ctrl, H->P, s.gM, hi, ny, ty, hg, s.st, &H->launches);
-      CK(cudaEventRecord(s.ev_edge, s.st));
-      CK(cudaStreamWaitEvent(s.cst, s.ev_edge, 0));
-      int st = halo_nccl(H, q, s.cst);
+    if (split) {
+      int st = split_step(H, n, q);
       if (st) return st;
-      if (hi > lo)
-        launch_fused_step(s.v, s.ctrl, H->P, s.gM, lo, hi, ty, hg, s.st, &H->launches);
-      if (H->profiling) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
-      CK(cudaGetLastError());
-      CK(cudaEventRecord(s.ev_int, s.st));
-      CK(cudaStreamWaitEvent(s.cst, s.ev_int, 0));
-      if ((st = allreduce_nccl(H, s.cst))) return st;
-      CK(cudaEventRecord(s.ev_comm, s.cst));
-      CK(cudaStreamWaitEvent(s.st, s.ev_comm, 0));
-      ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 1);
-      H->launches += 1;
-      CK(cudaGetLastError());
       H->host_parity = q;
       continue;
     }
@@ -1556,8 +1684,6 @@ int csph_step(csph_t* H, int nsteps) {
     for (size_t si = 0; si < H->s.size(); ++si) {
       Strip& s = H->s[si];
       CK(cudaSetDevice(s.dev));
-      clear_flags_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
-      H->launches += 1;
       if (H->profiling && si == 0) CK(cudaEventRecord(H->evs[2 * n], s.st));
       if (H->p.path == CSPH_PATH_STAGED)
         launch_staged_step(s.v, s.ctrl, s.scr, H->P, s.gM, s.st, &H->launches);

@@ -185,6 +185,12 @@ __global__ void __launch_bounds__(NT, MINB)
   // sediment flux), Q^L = 0, so H' = H - lam*0, Q' = +0, b' = b - (lam W)*0 + (tau W)*src.
   // A tile is therefore an identity when no cell of it and no cell of the facing 1-cell
   // bands of its 4 edge neighbours was wet after the previous step (band-mask flags). ----
+  // index of a static per-cell field (NEXT-3/4, GEN instance) at column c, row r, for a
+  // read whose result may feed nothing: threads past the last ghost column of the last tile
+  // and the phase A run one row beyond the march are clamped into the allocation
+  auto fidx = [&](int c, int r) -> size_t {
+    return off(pitch, min(c, nx + GX - 1), min(r, S.ny + GY - 1));
+  };
   const int tr = y0 / TY;
   const int ti = tr * hg.ntx + (int)blockIdx.x;
   // across an interior strip edge the facing tile row is the neighbouring strip's, whose
@@ -358,7 +364,8 @@ __global__ void __launch_bounds__(NT, MINB)
       if (FRIC) {
         T cgc = Q.cgam;
         if constexpr (GEN) {
-          if (S.cg) cgc = S.cg[off(pitch, col, L)];  // NEXT-3 field
+          // NEXT-3 field (see fidx: clamped where the result feeds nothing)
+          if (S.cg) cgc = S.cg[fidx(col, L)];
         }
         gg = (cgc * sqrt0_t(uu * uu + vv * vv)) * (rr * icbrt_t(Hs));
       }
@@ -417,12 +424,13 @@ __global__ void __launch_bounds__(NT, MINB)
       phx2h = T(0);
       ut3 = ut2; vt3 = vt2; ut2 = ut1; vt2 = vt1;
       J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = J0a1;
-      // K4 of the dry row L: H_half = H, u~ = v~ = 0, J0 = 0
+      // K4 of the dry row L: H_half = H, u~ = v~ = 0, J0 = 0.  Only H_half goes to the
+      // exchange row: this parity's u~, v~, J0 slots hold row L-2's values, which are +0
+      // already (rows L-4..L are dry), and a neighbour may still be reading them in the
+      // previous iteration's phase D (no barrier in between; racecheck)
       Hh1 = H0; ut1 = T(0); vt1 = T(0); J0x1 = T(0); J0y1 = T(0); J0a1 = T(0);
       vm1 = T(0);
       X2w[0 * SM::XW + t + 1] = H0;
-#pragma unroll
-      for (int q = 1; q < 5; ++q) X2w[q * SM::XW + t + 1] = T(0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) XG(sm.X4[q], 0) = T(0);
       if (col_out && j >= y0 && j < y1) {
@@ -554,7 +562,7 @@ __global__ void __launch_bounds__(NT, MINB)
           Hh = w0 ? hh : H0; ut = w0 ? uu : T(0); vt = w0 ? vv : T(0);
         }
         T jx = T(0), jy = T(0), ja = T(0);
-        if (TRANSP) grass_t<GEN>(Q, ut, vt, H0, aj_at(off(pitch, col, L), H0), jx, jy, ja);
+        if (TRANSP) grass_t<GEN>(Q, ut, vt, H0, aj_at(fidx(col, L), H0), jx, jy, ja);
         X2w[0 * SM::XW + t + 1] = Hh;
         X2w[1 * SM::XW + t + 1] = ut;
         X2w[2 * SM::XW + t + 1] = vt;
@@ -587,7 +595,9 @@ __global__ void __launch_bounds__(NT, MINB)
   }
 #undef RG
 #undef XG
-  if (neg) atomicOr(&C->flags, 1);
+  // negative depth (reading #27): a 4th max slot, combined across strips and ranks with the
+  // Eq.7 maxima, so every strip stops at the same step
+  if (neg) atomicMax(&gM[3], 1ull);
   // block max of the Eq.7 terms, one atomicMax per CTA and term
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -627,12 +637,16 @@ void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
               int row1, int TY, const Hgs& hg, cudaStream_t st) {
   using SM = Smem<T, NT, HASW, D>;
   constexpr int TX = NT - 8;
-  static bool configured = false;
+  // the dynamic shared-memory limit is a per-device attribute: set it once per device (a
+  // failure leaves the bit clear and surfaces as the launch error the caller checks)
+  static unsigned long long configured = 0;
   const size_t smem = sizeof(SM);
-  if (!configured) {
-    cudaFuncSetAttribute(fused_step_kernel<T, NT, HASW, D, PF, MINB, GEN>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!((configured >> (dev & 63)) & 1ull)) {
+    if (cudaFuncSetAttribute(fused_step_kernel<T, NT, HASW, D, PF, MINB, GEN>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
+      configured |= 1ull << (dev & 63);
   }
   dim3 grid((unsigned)((S.nx + TX - 1) / TX), (unsigned)((row1 - row0 + TY - 1) / TY));
   fused_step_kernel<T, NT, HASW, D, PF, MINB, GEN>

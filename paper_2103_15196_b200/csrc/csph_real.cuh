@@ -11,7 +11,7 @@ namespace ck {
 // Scalar constants of R converted once to T at kernel start.
 template <typename T>
 struct PT {
-  T g, eps, neg_tol, A_J, C_J, C_Sh, kappa, cPh, cgam, inv_h, inv_2h, src, d50;
+  T g, eps, neg_tol, A_J, C_J, C_Sh, kappa, cPh, cgam, inv_h, inv_2h, src, d50, hbm;
   int m_grass, fric, transport;
 };
 
@@ -22,6 +22,7 @@ __device__ __forceinline__ PT<T> make_pt(const Phys& P) {
   q.C_J = T(P.C_J); q.C_Sh = T(P.C_Sh); q.kappa = T(P.kappa); q.cPh = T(P.cPh);
   q.cgam = T(P.cgam); q.inv_h = T(P.inv_h); q.inv_2h = T(P.inv_2h); q.src = T(P.src);
   q.d50 = T(P.d50);
+  q.hbm = T(P.hbm);
   q.m_grass = P.m_grass; q.fric = P.fric; q.transport = P.transport;
   return q;
 }
@@ -105,8 +106,8 @@ __device__ __forceinline__ void grass_t(const PT<T>& P, T ut, T vt, T H, T A, T&
   T s2 = ut * ut + vt * vt;
   T sa = sqrt0_t(s2);
   T a = A * pow_m_t<GEN>(P.m_grass, s2, sa);
-  // Eq.5 gate and reading #31: no bedload through a film no deeper than the grain (H <= d50)
-  const bool gate = ((P.C_Sh == T(0)) | ((s2 * s2) * s2 > P.kappa * H)) & (H > P.d50);
+  // Eq.5 gate and reading #31: no bedload through a film (H <= h_bed_min, default d50)
+  const bool gate = ((P.C_Sh == T(0)) | ((s2 * s2) * s2 > P.kappa * H)) & (H > P.hbm);
   jx = gate ? a * ut : T(0); jy = gate ? a * vt : T(0); ja = gate ? a * sa : T(0);
 }
 
@@ -129,7 +130,7 @@ __device__ __forceinline__ void dt_terms_t(const PT<T>& P, T H, T Qx, T Qy, T W,
   T a = sqrt0_t(s2);
   t1 = s2;
   t2 = a + sqrt_gh_t<GEN>(P.g * H);
-  bool gate = ((P.C_Sh == T(0)) || ((s2 * s2) * s2 > P.kappa * H)) && (H > P.d50);
+  bool gate = ((P.C_Sh == T(0)) || ((s2 * s2) * s2 > P.kappa * H)) && (H > P.hbm);
   t3 = gate ? ((A * pow_m_t<GEN>(P.m_grass, s2, a)) * a) * W : T(0);
 }
 

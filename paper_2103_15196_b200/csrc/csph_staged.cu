@@ -194,7 +194,7 @@ __global__ void k8_update(StripView S, Ctrl* C, Scratch T, Range R, Phys P,
     apply_sources(S, tau, c, Hn, Qxn, Qyn);
     bool wet = Hn > P.eps;
     if (!wet) { Qxn = 0.0; Qyn = 0.0; }
-    if (Hn < -P.neg_tol) atomicOr(&C->flags, 1);
+    if (Hn < -P.neg_tol) atomicMax(&gM[3], 1ull);  // combined like the maxima
     S.H[q][c] = Hn; S.Qx[q][c] = Qxn; S.Qy[q][c] = Qyn; S.b[q][c] = bn;
     if (wet) {
       double t1, t2, t3;

@@ -25,6 +25,7 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["steps"] == 2 and d["warmup"] == 1
     assert d["value"] > 0 and d["unit"] == "Gcell-updates/s" and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
+    assert d["cpu_baseline"]["host"]["nproc"] >= 1 and "cpu_model" in d["cpu_baseline"]["host"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
 
 
@@ -44,8 +45,35 @@ def test_gpu_arm_json_line():
     ro = d["roofline"]
     assert ro["bound"] == "hbm" and ro["unit"] == "GB/s" and 0 < ro["frac"] < 1
     assert abs(ro["frac"] - ro["achieved"] / ro["peak"]) < 1e-9
-    assert d["gpu_launches"] >= 5 * 3  # clear flags + fused + ctrl per step
+    assert d["gpu_launches"] >= 5 * 2  # fused + ctrl per step
+    assert len(d["timed_runs_ms"]) == 3 and d["ms_per_step"] * 5 in d["timed_runs_ms"]
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_dist_path_under_torchrun():
+    """The multi-GPU code path of bench.py end to end with one rank under torchrun
+    (DESIGN.md 9): torch.distributed NCCL group, the all-gathered balanced bounds, the
+    NCCL-id broadcast, csph_create_dist_rows, the split launches + halo exchange + max
+    allreduce of every step, and the e2e leg through csph_set_state_rows/get_state_rows."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "bench.py"), "--dist", "--config", "C5", "--grid-n", "1024",
+           "--steps", "4", "--warmup", "3", "--repeats", "1", "--no-cpu-baseline",
+           "--e2e-steps", "4", "--tile-rows", "64"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.strip().startswith("{")][-1])
+    assert d["value"] > 0 and d["n_gpus"] == 1
+    assert d["config"]["partition"]["bounds"] == [0, 1024]
+    assert d["config"]["parallelism"].startswith("row strips")
+    # per step: ctrl + 2 edge launches + the interior launch (16 tile rows of 64)
+    assert d["gpu_launches"] == 4 * 4
+    assert d["e2e"]["value"] > 0

@@ -79,6 +79,33 @@ def test_fp32_parity_1e4(cs, name, n, ny, cj):
     assert q <= max(1e-5, 4 * qc), (q, qc)
 
 
+@pytest.mark.parametrize("name,n,ny,cj", [("C1", None, None, None), ("C2", 256, 256, None),
+                                          ("C3", 256, 200, None), ("C4", 192, 256, None),
+                                          ("C5", 300, 260, None), ("C5", 300, 260, 0.0)])
+def test_fp32_bitwise_vs_binary32_oracle(cs, name, n, ny, cj):
+    """The fp32 mode is R evaluated in IEEE binary32: every decision of R
+    (wet test, Shamov gate, film cut-off, donor, HLL case, minmod) taken in the precision
+    the mode computes in, as the oracle built with -DORC_FP32 takes it.  After 100 steps
+    the GPU state and dt log are bitwise those of the binary32 oracle -- including C5 with
+    the Eq.2 slope term, where binary32 and binary64 legitimately part (the gate flips)."""
+    c = synth.config(name, n, ny)
+    if cj is not None:
+        c.params = dict(c.params, C_J=cj)
+    f = synth.fill(c)
+    ref = oracle.Oracle(c.nx, c.ny, c.dx, oracle.Params(**c.params), precision=32)
+    assert ref.set_state(*f) == 0
+    st, dt_ref, lim_ref = ref.step(100)
+    assert st == 0 and len(dt_ref) == 100
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, precision=32))
+    g.set_state(*f)
+    g.step(100)
+    dt, lim = g.get_dt_log(100)
+    assert np.array_equal(dt, dt_ref) and np.array_equal(lim, lim_ref)
+    for a, r in zip(g.get_state(), ref.get_state()):
+        assert np.array_equal(a, r)
+    g.destroy()
+
+
 def test_fp32_strips_and_hgs_bitwise(cs):
     """fp32 results do not depend on the decomposition or on HGS skipping."""
     c = synth.config("C4", 180, 200)

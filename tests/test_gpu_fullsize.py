@@ -1,15 +1,19 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times
-(fused path, HGS on, default tiling).
+(fused path, HGS on, default tiling), at north_star's 100 steps.
 
 * C3 4096^2 (the third config, 16.7 M cells): the whole grid against the oracle over
-  3 steps -- every cell and the dt log bitwise.
+  100 steps -- every cell and the dt log bitwise (about 2.5 min of oracle time).
+* C4: SURVEY 8(d)'s oracle crop of the 8192^2 field, columns [3584, 4608) x rows
+  [0, 2048) (the dam, the breach and the channel) as its own walled domain, 100 steps,
+  whole crop and dt log bitwise.
 * C5 16384^2 (the bench workload, 268 M cells): the oracle cannot run the whole grid in
   test time, so (a) tau_0 is computed by the oracle from the Eq.7 maxima of the initial
   state, reduced strip by strip (max is exact and order-free); (b) after
-  one GPU step, sampled 48 x 48 patches (the 4 wall corners, wet/dry fronts, random
-  interior points) are recomputed by the oracle one by one: a patch plus its 3 ghost
-  layers taken from the real neighbours (walls mirrored by the oracle itself) determines
-  the patch's update exactly (stencil radius 3), stepped with tau_0;
+  k = 20 and k = 100 GPU steps, sampled 48 x 48 patches (wall corners, wet/dry fronts,
+  random interior points) are recomputed by the oracle: the patch's dependency cone, a
+  window of 48 + 6k cells with its 3 ghost layers taken from the real neighbours (walls
+  mirrored by the oracle itself), stepped k times with the GPU's own tau log -- cells
+  farther than 3k from the window edge are exact (stencil radius 3);
   (c) properties that hold at any size over 12 steps: HGS on == HGS off bitwise, exact
   volume bookkeeping of the walled domain, no negative depth."""
 import numpy as np
@@ -29,22 +33,39 @@ def cs():
     return csph
 
 
-def test_C3_full_grid_3_steps_bitwise(cs):
-    c = synth.config("C3")
-    assert (c.nx, c.ny) == (4096, 4096)
-    f = synth.fill(c)
+def _whole_vs_oracle(cs, c, f, steps):
     ref = oracle.Oracle(c.nx, c.ny, c.dx, oracle.Params(**c.params))
     assert ref.set_state(*f) == 0
-    st, dt_ref, lim_ref = ref.step(3)
-    assert st == 0
+    st, dt_ref, lim_ref = ref.step(steps)
+    assert st == 0 and len(dt_ref) == steps
     g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params))
     g.set_state(*f)
-    g.step(3)
-    dt, lim = g.get_dt_log(3)
+    g.step(steps)
+    dt, lim = g.get_dt_log(steps)
     assert np.array_equal(dt, dt_ref) and np.array_equal(lim, lim_ref)
     for a, r in zip(g.get_state(), ref.get_state()):
         assert np.array_equal(a, r)
     g.destroy()
+
+
+def test_C3_full_grid_100_steps_bitwise(cs):
+    c = synth.config("C3")
+    assert (c.nx, c.ny) == (4096, 4096)
+    _whole_vs_oracle(cs, c, synth.fill(c), 100)
+
+
+def test_C4_survey_crop_100_steps_bitwise(cs):
+    """the crop i in [3584, 4608), j in [0, 2048) of the 8192^2 fields,
+    run as its own walled domain (it holds the dam rows 1016-1023, the breach and the
+    channel: moving wet/dry fronts)."""
+    c8 = synth.config("C4")
+    assert (c8.nx, c8.ny) == (8192, 8192)
+    rows = synth.fill(c8, 0, 2048)
+    f = tuple(np.ascontiguousarray(a[:, 3584:4608]) for a in rows)
+    c = synth.Config("C4crop", 4, 1024, 2048, c8.dx, 0, dict(c8.params))
+    h = f[0]
+    assert (h[:1016] > 1e-6).any() and (h[1024:] > 1e-6).any()  # reservoir and channel
+    _whole_vs_oracle(cs, c, f, 100)
 
 
 def _window(a, i0, i1, j0, j1, fill):
@@ -72,7 +93,7 @@ def _patches(wet, n, rng, size):
     return ps
 
 
-def test_C5_full_size_sampled_vs_oracle(cs):
+def test_C5_full_size_cones_vs_oracle(cs):
     c = synth.config("C5")
     assert (c.nx, c.ny) == (16384, 16384)
     P = oracle.Params(**c.params)
@@ -89,27 +110,35 @@ def test_C5_full_size_sampled_vs_oracle(cs):
         del o
     st, tau0, lim0 = oracle.Oracle(8, 8, c.dx, P).tau_from_M(M)
     assert st == 0
-    # the GPU, bench configuration, one step
+    # the GPU, bench configuration
     g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params))
     g.set_state(*f)
-    g.step(1)
-    dt, lim = g.get_dt_log(1)
-    assert dt[0] == tau0 and lim[0] == lim0
-    # (b) sampled patches recomputed by the oracle
     size = 48
     W = 1.0 / (1.0 - psi)
     rng = np.random.default_rng(2103)
-    for (i0, j0) in _patches(h > P.eps_dry, 10, rng, size):
-        i1, j1 = i0 + size, j0 + size
-        o = oracle.Oracle(size, size, c.dx, P)
-        o.set_walls(i0 == 0, i1 == c.nx, j0 == 0, j1 == c.ny)
-        assert o.set_state_padded(*[_window(a, i0, i1, j0, j1, 0.0) for a in (h, hu, hv, b)],
-                                  _window(W, i0, i1, j0, j1, 1.0)) == 0
-        assert o.step_tau(tau0) == 0
-        ref = o.get_state()
-        got = g.get_state_rows(j0, j1)
-        for a, r in zip(got, ref):
-            assert np.array_equal(a[:, i0:i1], r), (i0, j0)
+    patches = _patches(h > P.eps_dry, 4, rng, size)
+    done = 0
+    for k in (20, 100):
+        g.step(k - done)
+        done = k
+        dt, lim = g.get_dt_log(k)
+        assert len(dt) == k and dt[0] == tau0 and lim[0] == lim0
+        m = 3 * k  # the dependency cone of the patch after k steps
+        for (pi, pj) in patches:
+            i0, i1 = max(0, pi - m), min(c.nx, pi + size + m)
+            j0, j1 = max(0, pj - m), min(c.ny, pj + size + m)
+            o = oracle.Oracle(i1 - i0, j1 - j0, c.dx, P)
+            o.set_walls(i0 == 0, i1 == c.nx, j0 == 0, j1 == c.ny)
+            assert o.set_state_padded(*[_window(a, i0, i1, j0, j1, 0.0) for a in (h, hu, hv, b)],
+                                      _window(W, i0, i1, j0, j1, 1.0)) == 0
+            for tau in dt:
+                assert o.step_tau(float(tau)) == 0
+            ref = o.get_state()
+            got = g.get_state_rows(pj, pj + size)
+            for a, r in zip(got, ref):
+                assert np.array_equal(a[:, pi:pi + size],
+                                      r[pj - j0:pj - j0 + size, pi - i0:pi - i0 + size]), (k, pi, pj)
+            del o
     g.destroy()
 
 

@@ -120,7 +120,14 @@ def test_dist_split_launches(cs, tile_rows):
     assert np.array_equal(g.get_dt_log(40)[0], dt0)
     for a, r in zip(g.get_state(), ref):
         assert np.array_equal(a, r)
-    assert g.last_launch_count() == 40 * (2 + (3 if c.ny > 2 * tile_rows else 2))
+    # per step: ctrl + the edge tile rows, the interior (when there is one); the last
+    # launch must hold >= 3 rows (a short last tile is merged with the one before it)
+    nty = -(-c.ny // tile_rows)
+    hi = (nty - 1) * tile_rows
+    if c.ny - hi < 3:
+        hi -= tile_rows
+    split = nty >= 3 and hi > tile_rows
+    assert g.last_launch_count() == 40 * (1 + (3 if split else 1))
     g.destroy()
 
 
@@ -151,4 +158,85 @@ def test_front_crosses_strip_edges_hgs(cs, nstrips):
     for a, r in zip(g.get_state(), ref):
         assert np.array_equal(a, r)
     assert ref[0][76:].max() > 0  # the front crossed the strip edges at rows 37/41 and 70
+    g.destroy()
+
+
+@pytest.mark.parametrize("tile_rows", [16, 32])
+def test_split_strips_short_last_tile_vs_oracle(cs, tile_rows):
+    """Overlapped multi-strip steps (edge tile rows -> halo on the comm stream || interior,
+    DESIGN.md 9) with strips whose last tile row has 1 or 2 rows (ny % ty in {1, 2}): the
+    halo rows sent at the edge event must all be final.  Four strips of
+    3 * ty + 1, 3 * ty + 2, 4 * ty + 1 rows and the rest, HGS on, compared element by
+    element with the CPU oracle (and the dt log bitwise)."""
+    import oracle
+    c = synth.config("C4", 160, 14 * tile_rows + 7)
+    f = synth.fill(c)
+    b1 = 3 * tile_rows + 1
+    b2 = b1 + 3 * tile_rows + 2
+    b3 = b2 + 4 * tile_rows + 1
+    bounds = [0, b1, b2, b3, c.ny]
+    steps = 60
+    ref = oracle.Oracle(c.nx, c.ny, c.dx, oracle.Params(**c.params))
+    assert ref.set_state(*f) == 0
+    st, dt0, lim0 = ref.step(steps)
+    assert st == 0
+    g = cs.csph_create_multi_rows(c.nx, c.ny, c.dx, cs.params_from(c.params, tile_rows=tile_rows),
+                                  [0] * 4, bounds)
+    g.set_state(*f)
+    g.step(steps)
+    dt, lim = g.get_dt_log(steps)
+    assert np.array_equal(dt, dt0) and np.array_equal(lim, lim0)
+    for a, r in zip(g.get_state(), ref.get_state()):
+        assert np.array_equal(a, r)
+    g.destroy()
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_negative_depth_stops_every_strip(cs, path):
+    """CSPH_ENEGDEPTH (reading #27) on the device: with K = 0.95 (beyond the
+    unsplit scheme's positivity bound, reading #13) a random moving state drives a depth
+    below -neg_tol at step 4.  Like the oracle, the GPU returns ENEGDEPTH after exactly that
+    step with its state kept (bitwise the oracle's), and later calls neither advance nor
+    clear the error.  The flag is combined across strips with the Eq.7 maxima:
+    on 3 strips every strip stops after the same step."""
+    import oracle
+    nx, ny = 48, 40
+    f = synth.random_state(nx, ny, seed=35, wet_frac=0.6, vel=4.0)
+    prm = dict(K=0.95)
+    ref = oracle.Oracle(nx, ny, 1.0, oracle.Params(**prm))
+    ref.set_state(*f)
+    st, dt0, _ = ref.step(20)
+    assert st == oracle.ENEGDEPTH and len(dt0) == 4
+    for g in (cs.csph_create(nx, ny, 1.0, cs.params_from(prm, path=path)),
+              cs.csph_create_multi_rows(nx, ny, 1.0, cs.params_from(prm, path=path), [0] * 3,
+                                        [0, 13, 27, ny])):
+        g.set_state(*f)
+        with pytest.raises(cs.CsphError) as e:
+            g.step(20)
+        assert e.value.code == cs.CSPH_ENEGDEPTH
+        assert g.get_time()[1] == 4
+        assert np.array_equal(g.get_dt_log(20)[0], dt0)
+        for a, r in zip(g.get_state(), ref.get_state()):
+            assert np.array_equal(a, r)
+        assert g.step(3, check=False) == cs.CSPH_ENEGDEPTH
+        assert g.get_time()[1] == 4
+        g.destroy()
+
+
+def test_nonfinite_maxima(cs):
+    """CSPH_ENONFINITE: finite inputs whose Eq.7 term overflows (|v| = 1e200,
+    s2 = inf) stop the first step, as in the oracle; nothing advances."""
+    import oracle
+    nx, ny = 8, 6
+    h = np.ones((ny, nx)); hu = np.zeros((ny, nx)); hu[2, 3] = 1e200
+    z = np.zeros((ny, nx))
+    ref = oracle.Oracle(nx, ny, 1.0, oracle.Params())
+    ref.set_state(h, hu, z, z)
+    assert ref.step(1)[0] == oracle.ENONFINITE
+    g = cs.csph_create(nx, ny, 1.0, cs.params_from({}))
+    g.set_state(h, hu, z, z)
+    assert g.step(2, check=False) == cs.CSPH_ENONFINITE
+    assert g.get_time()[1] == 0
+    for a, r in zip(g.get_state(), (h, hu, z, z)):
+        assert np.array_equal(a, r)
     g.destroy()

@@ -29,65 +29,65 @@ PIN_TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_bruteforce.py",
 # (name, original text, mutated text)
 MUTATIONS = [
     # ---- the five time-level slips that survived round 1's pins
-    ("K5 centre eta uses H_n", "double ec = o->Hh[c] + b[c];", "double ec = H[c] + b[c];"),
-    ("K7 reconstructs H_half", "const double* q[4] = {o->eta, H, un, utn};",
-     "const double* q[4] = {o->eta, o->Hh, un, utn};"),
-    ("gate reads H_half", "orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh) && orc_bed_mobile(H[c], o->hbm)",
-     "orc_shamov_gate(o->kappa, s2, o->Hh[c], p->C_Sh) && orc_bed_mobile(H[c], o->hbm)"),
-    ("film cut-off reads H_half", "orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh) && orc_bed_mobile(H[c], o->hbm)",
-     "orc_shamov_gate(o->kappa, s2, H[c], p->C_Sh) && orc_bed_mobile(o->Hh[c], o->hbm)"),
-    ("dry H_half = 0", "if (!o->w[c]) { o->Hh[c] = H[c];", "if (!o->w[c]) { o->Hh[c] = 0.0;"),
+    ("K5 centre eta uses H_n", "real ec = o->Hh[c] + b[c];", "real ec = H[c] + b[c];"),
+    ("K7 reconstructs H_half", "const real* q[4] = {o->eta, H, un, utn};",
+     "const real* q[4] = {o->eta, o->Hh, un, utn};"),
+    ("gate reads H_half", "r_shamov_gate(o->kappa, s2, H[c], o->C_Sh) && r_bed_mobile(H[c], o->hbm)",
+     "r_shamov_gate(o->kappa, s2, o->Hh[c], o->C_Sh) && r_bed_mobile(H[c], o->hbm)"),
+    ("film cut-off reads H_half", "r_shamov_gate(o->kappa, s2, H[c], o->C_Sh) && r_bed_mobile(H[c], o->hbm)",
+     "r_shamov_gate(o->kappa, s2, H[c], o->C_Sh) && r_bed_mobile(o->Hh[c], o->hbm)"),
+    ("dry H_half = 0", "if (!o->w[c]) { o->Hh[c] = H[c];", "if (!o->w[c]) { o->Hh[c] = RL(0);"),
     # ---- K1 / K2 / friction
     ("K1 wet test >=", "o->w[c] = H[c] > eps;", "o->w[c] = H[c] >= eps;"),
     ("K1 v from Qx", "o->v[c] = Qy[c] * o->r[c];", "o->v[c] = Qx[c] * o->r[c];"),
     ("K2 force sign", "o->phix[c] = -(PE + PW);", "o->phix[c] = (PE + PW);"),
-    ("K2 west face swapped", "double PW = face_force(o->cP, o->eta[wv], b[wv], o->eta[c], b[c]);",
-     "double PW = face_force(o->cP, o->eta[c], b[c], o->eta[wv], b[wv]);"),
+    ("K2 west face swapped", "real PW = face_force(o->cP, o->eta[wv], b[wv], o->eta[c], b[c]);",
+     "real PW = face_force(o->cP, o->eta[c], b[c], o->eta[wv], b[wv]);"),
     ("face force b* = min", "double bs = sel_max(bL, bR);", "double bs = sel_min(bL, bR);"),
-    ("face force mean factor", "return (cP * (0.5 * (HsL + HsR))) * (HsR - HsL);",
+    ("face force mean factor", "return (cP * (RL(0.5) * (HsL + HsR))) * (HsR - HsL);",
      "return (cP * (HsL + HsR)) * (HsR - HsL);"),
-    ("friction H^(-1/3) dropped", "o->gam[c] = (o->cgam * sp) * (o->r[c] * orc_icbrt(H[c]));",
+    ("friction H^(-1/3) dropped", "o->gam[c] = (o->cgam * sp) * (o->r[c] * r_icbrt(H[c]));",
      "o->gam[c] = (o->cgam * sp) * o->r[c];"),
     ("icbrt 4 Newton steps", "for (int k = 0; k < 5; ++k) {", "for (int k = 0; k < 2; ++k) {"),
     # ---- K4 / K6
-    ("K4 theta = tau", "o->Hh[c] = H[c] * (1.0 - theta * div);", "o->Hh[c] = H[c] * (1.0 - tau * div);"),
+    ("K4 theta = tau", "o->Hh[c] = H[c] * (RL(1) - theta * div);", "o->Hh[c] = H[c] * (RL(1) - tau * div);"),
     ("K4 div sign v", "(o->v[c + sy] - o->v[c - sy])", "(o->v[c - sy] - o->v[c + sy])"),
     ("K4 u~ uses Phi_half", "o->ut[c] = ((Qx[c] + theta * o->phix[c]) * f) * o->r[c];",
      "o->ut[c] = ((Qx[c] + theta * o->phix2[c]) * f) * o->r[c];"),
-    ("K4 friction factor tau", "double f = 1.0 / (1.0 + theta * o->gam[c]);",
-     "double f = 1.0 / (1.0 + tau * o->gam[c]);"),
+    ("K4 friction factor tau", "real f = RL(1) / (RL(1) + theta * o->gam[c]);",
+     "real f = RL(1) / (RL(1) + tau * o->gam[c]);"),
     ("K6 uses Phi^n", "o->QLx[c] = (Qx[c] + tau * o->phix2[c]) * f;", "o->QLx[c] = (Qx[c] + tau * o->phix[c]) * f;"),
     ("K6 theta", "o->QLy[c] = (Qy[c] + tau * o->phiy2[c]) * f;", "o->QLy[c] = (Qy[c] + theta * o->phiy2[c]) * f;"),
     # ---- K7
-    ("minmod picks max", "if (a > 0.0 && b > 0.0) return sel_min(a, b);", "if (a > 0.0 && b > 0.0) return sel_max(a, b);"),
-    ("face state - sign", "qm[k] = q[k][L] + 0.5 * sL[k];", "qm[k] = q[k][L] - 0.5 * sL[k];"),
-    ("slope R wrong cells", "sR[k] = orc_minmod(q[k][R] - q[k][L], q[k][RR] - q[k][R]);",
-     "sR[k] = orc_minmod(q[k][L] - q[k][LL], q[k][RR] - q[k][R]);"),
-    ("HLL S_R dry factor 2", "SR = un_m + 2.0 * c_m;", "SR = un_m + c_m;"),
+    ("minmod picks max", "if (a > RL(0) && b > RL(0)) return sel_min(a, b);", "if (a > RL(0) && b > RL(0)) return sel_max(a, b);"),
+    ("face state - sign", "qm[k] = q[k][L] + RL(0.5) * sL[k];", "qm[k] = q[k][L] - RL(0.5) * sL[k];"),
+    ("slope R wrong cells", "sR[k] = r_minmod(q[k][R] - q[k][L], q[k][RR] - q[k][R]);",
+     "sR[k] = r_minmod(q[k][L] - q[k][LL], q[k][RR] - q[k][R]);"),
+    ("HLL S_R dry factor 2", "SR = un_m + RL(2) * c_m;", "SR = un_m + c_m;"),
     ("HLL S_L both wet", "SL = sel_min(un_m - c_m, un_p - c_p);", "SL = sel_min(un_m - c_m, un_p + c_p);"),
     ("HLL dissipation sign", "out[k] = ((SR * FL[k] - SL * FR[k]) + SLSR * (UR[k] - UL[k])) * inv;",
      "out[k] = ((SR * FL[k] - SL * FR[k]) - SLSR * (UR[k] - UL[k])) * inv;"),
     ("hydrostatic b* = min", "double bs = sel_max(b_m, b_p);", "double bs = sel_min(b_m, b_p);"),
-    ("donor reversed", "if (us > 0.0) { Jn = J0n[L]; Ja = o->J0a[L]; }", "if (us < 0.0) { Jn = J0n[L]; Ja = o->J0a[L]; }"),
+    ("donor reversed", "if (us > RL(0)) { Jn = J0n[L]; Ja = o->J0a[L]; }", "if (us < RL(0)) { Jn = J0n[L]; Ja = o->J0a[L]; }"),
     ("slope term sign", "return J0n - (C_J * J0abs) * db_dn;", "return J0n + (C_J * J0abs) * db_dn;"),
     ("grass |J0| drops sqrt", "*jabs = c * a;", "*jabs = c;"),
     ("sediment gradient L/R", "(b[R] - b[L]) * o->inv_h", "(b[L] - b[R]) * o->inv_h"),
     # ---- K8 / Eq.7
-    ("K8 W dropped", "double bn = (b[c] - (lam * W[c]) * dJ) + (tau * W[c]) * src;",
-     "double bn = (b[c] - lam * dJ) + (tau * W[c]) * src;"),
-    ("K8 y-flux of Qx from normal", "double dQx = (o->FQx[e] - o->FQx[c]) + (o->GQx[n] - o->GQx[c]);",
-     "double dQx = (o->FQx[e] - o->FQx[c]) + (o->GQy[n] - o->GQy[c]);"),
-    ("K8 no dry zeroing", "if (!(Hn > eps)) { Qxn = 0.0; Qyn = 0.0; }", "if (!(Hn > 0.0)) { Qxn = 0.0; Qyn = 0.0; }"),
+    ("K8 W dropped", "real bn = (b[c] - (lam * W[c]) * dJ) + (tau * W[c]) * src;",
+     "real bn = (b[c] - lam * dJ) + (tau * W[c]) * src;"),
+    ("K8 y-flux of Qx from normal", "real dQx = (o->FQx[e] - o->FQx[c]) + (o->GQx[n] - o->GQx[c]);",
+     "real dQx = (o->FQx[e] - o->FQx[c]) + (o->GQy[n] - o->GQy[c]);"),
+    ("K8 no dry zeroing", "if (!(Hn > eps)) { Qxn = RL(0); Qyn = RL(0); }", "if (!(Hn > RL(0))) { Qxn = RL(0); Qyn = RL(0); }"),
     ("Eq.7 t1 factor", "double t1 = h / (2.0 * sqrt(M[0]));", "double t1 = h / sqrt(M[0]);"),
     ("Eq.7 M3 without W", "t3 = ((cell_aj(o, c, Hc) * pw) * a) * o->W[c];", "t3 = (cell_aj(o, c, Hc) * pw) * a;"),
-    ("Eq.7 M2 drops |v|", "double t2 = a + sqrt(p->g * Hc);", "double t2 = sqrt(p->g * Hc);"),
-    ("W = 1 - psi", "o->W[d] = 1.0 / (1.0 - (psi ? psi[s] : 0.0));", "o->W[d] = 1.0 - (psi ? psi[s] : 0.0);"),
+    ("Eq.7 M2 drops |v|", "real t2 = a + SQRT(o->g * Hc);", "real t2 = SQRT(o->g * Hc);"),
+    ("W = 1 - psi", "o->W[d] = RL(1.0 / (1.0 - (psi ? psi[s] : 0.0)));", "o->W[d] = RL(1.0 - (psi ? psi[s] : 0.0));"),
     ("wall ghost Qx not negated", "o->Qx[d] = negx ? -o->Qx[s] : o->Qx[s];", "o->Qx[d] = o->Qx[s];"),
     # ---- NEXT-4 closures
-    ("Grass odd m drops |v|", "if (m % 2) pw = pw * a;", "if (m % 2) pw = pw * 1.0;"),
-    ("Eq.4 sqrt(gH) -> gH", "(((s_rel - 1.0) * sqrt(g * H)) * d50)", "(((s_rel - 1.0) * (g * H)) * d50)"),
-    ("Eq.4 A_J at H_half", "orc_grass_m(cell_aj(o, c, H[c]),", "orc_grass_m(cell_aj(o, c, o->Hh[c]),"),
-    ("sources: absorption explicit", "double a = 1.0 / (1.0 + tau * o->beta[c]);", "double a = 1.0 - tau * o->beta[c];"),
+    ("Grass odd m drops |v|", "if (m % 2) pw = pw * a;", "if (m % 2) pw = pw * RL(1);"),
+    ("Eq.4 sqrt(gH) -> gH", "(((s_rel - RL(1)) * SQRT(g * H)) * d50)", "(((s_rel - RL(1)) * (g * H)) * d50)"),
+    ("Eq.4 A_J at H_half", "r_grass_m(cell_aj(o, c, H[c]),", "r_grass_m(cell_aj(o, c, o->Hh[c]),"),
+    ("sources: absorption explicit", "real a = RL(1) / (RL(1) + tau * o->beta[c]);", "real a = RL(1) - tau * o->beta[c];"),
 ]
 
 
