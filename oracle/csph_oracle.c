@@ -27,9 +27,11 @@
 #ifdef ORC_FP32
 typedef float real;
 #define SQRT sqrtf
+#define FMA fmaf
 #else
 typedef double real;
 #define SQRT sqrt
+#define FMA fma
 #endif
 #define RL(x) ((real)(x))  /* a constant of R in the working precision */
 
@@ -41,7 +43,7 @@ struct orc {
   orc_params p;
   /* host-side constants of R, computed in double, then rounded once to
    * the working precision */
-  real inv_h, inv_2h, cP, cgam, kappa;
+  real inv_h, inv_2h, cPh, cgam, kappa;
   real hbm;  /* reading #31 cut-off depth: h_bed_min, or d50 when h_bed_min < 0 */
   real eps, neg_tol, g, A_J, C_J, C_Sh, d50, s_rel, src;
   int wall[4];
@@ -152,14 +154,15 @@ static int r_bed_mobile(real H, real h_bed_min) {
 /* Face pressure term of K2/K5 (Eq.6 row 2, -gH grad(H+b), reading #1;
  * DESIGN.md 3.3) in hydrostatic-reconstruction form:
  *   b* = max(b_L, b_R) (cell beds), H*_s = max(0, eta_s - b*),
- *   P  = (c_P * (0.5*(H*_L + H*_R))) * (H*_R - H*_L).
+ *   P  = (c_P/2 * (H*_L + H*_R)) * (H*_R - H*_L),  c_P/2 = g/(4h) a host constant
+ * (= c_P * (0.5*(H*_L + H*_R)) exactly unless the sum is subnormal).
  * The wet flags are not needed: a dry cell whose bed is above the water has
  * H* = 0 on both sides of the face (a wall), a lower dry cell drives the flow. */
-static real face_force(real cP, real etaL, real bL, real etaR, real bR) {
+static real face_force(real cPh, real etaL, real bL, real etaR, real bR) {
   real bs = sel_max(bL, bR);
   real HsL = sel_max(RL(0), etaL - bs);
   real HsR = sel_max(RL(0), etaR - bs);
-  return (cP * (RL(0.5) * (HsL + HsR))) * (HsR - HsL);
+  return (cPh * (HsL + HsR)) * (HsR - HsL);
 }
 
 /* K7: hydrostatic step + HLL on F = (Hu, Hu^2, Huv) (Eq.6) */
@@ -283,7 +286,7 @@ orc_t* orc_create(int nx, int ny, double dx, const orc_params* p) {
   o->h = dx; o->p = *p;
   o->inv_h = RL(1.0 / dx);
   o->inv_2h = RL(1.0 / (2.0 * dx));
-  o->cP = RL(p->g / (2.0 * dx));
+  o->cPh = RL(0.5 * (p->g / (2.0 * dx)));  /* c_P/2 = g/(4h) */
   o->cgam = RL(p->g * (p->n_manning * p->n_manning));
   {
     double c2 = p->C_Sh * p->C_Sh;
@@ -580,10 +583,10 @@ int orc_step_tau(orc_t* o, double tau_d) {
       size_t c = IDX(o, i, j);
       if (!o->w[c]) { o->phix[c] = RL(0); o->phiy[c] = RL(0); o->gam[c] = RL(0); continue; }
       size_t e = c + sx, wv = c - sx, nn = c + sy, s = c - sy;
-      real PE = face_force(o->cP, o->eta[c], b[c], o->eta[e], b[e]);
-      real PW = face_force(o->cP, o->eta[wv], b[wv], o->eta[c], b[c]);
-      real PN = face_force(o->cP, o->eta[c], b[c], o->eta[nn], b[nn]);
-      real PS = face_force(o->cP, o->eta[s], b[s], o->eta[c], b[c]);
+      real PE = face_force(o->cPh, o->eta[c], b[c], o->eta[e], b[e]);
+      real PW = face_force(o->cPh, o->eta[wv], b[wv], o->eta[c], b[c]);
+      real PN = face_force(o->cPh, o->eta[c], b[c], o->eta[nn], b[nn]);
+      real PS = face_force(o->cPh, o->eta[s], b[s], o->eta[c], b[c]);
       o->phix[c] = -(PE + PW);
       o->phiy[c] = -(PN + PS);
       if (o->fields_fric) {
@@ -617,10 +620,10 @@ int orc_step_tau(orc_t* o, double tau_d) {
       if (!o->w[c]) { o->phix2[c] = RL(0); o->phiy2[c] = RL(0); continue; }
       size_t e = c + sx, wv = c - sx, nn = c + sy, s = c - sy;
       real ec = o->Hh[c] + b[c];
-      real PE = face_force(o->cP, ec, b[c], o->Hh[e] + b[e], b[e]);
-      real PW = face_force(o->cP, o->Hh[wv] + b[wv], b[wv], ec, b[c]);
-      real PN = face_force(o->cP, ec, b[c], o->Hh[nn] + b[nn], b[nn]);
-      real PS = face_force(o->cP, o->Hh[s] + b[s], b[s], ec, b[c]);
+      real PE = face_force(o->cPh, ec, b[c], o->Hh[e] + b[e], b[e]);
+      real PW = face_force(o->cPh, o->Hh[wv] + b[wv], b[wv], ec, b[c]);
+      real PN = face_force(o->cPh, ec, b[c], o->Hh[nn] + b[nn], b[nn]);
+      real PS = face_force(o->cPh, o->Hh[s] + b[s], b[s], ec, b[c]);
       o->phix2[c] = -(PE + PW);
       o->phiy2[c] = -(PN + PS);
     }
@@ -675,9 +678,11 @@ int orc_step_tau(orc_t* o, double tau_d) {
           sR[k] = r_minmod(q[k][R] - q[k][L], q[k][RR] - q[k][R]);
         }
         real qm[4], qp[4];
+        /* face states q- = q_L + sigma_L/2, q+ = q_R - sigma_R/2 with one rounding each
+         * (fma: exact product; = q + 0.5*sigma unless 0.5*sigma is subnormal) */
         for (int k = 0; k < 4; ++k) {
-          qm[k] = q[k][L] + RL(0.5) * sL[k];
-          qp[k] = q[k][R] - RL(0.5) * sR[k];
+          qm[k] = FMA(RL(0.5), sL[k], q[k][L]);
+          qp[k] = FMA(RL(-0.5), sR[k], q[k][R]);
         }
         real F[3];
         r_hll_face(o->g, qm[0], qm[1], qm[2], qm[3], qp[0], qp[1], qp[2], qp[3],

@@ -107,6 +107,9 @@ enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
 // K7 hydrostatic step + HLL without branches: every case of
 // hll_face() is evaluated with the same operations and the result selected, so
 // the value is bitwise identical.  Callers have already excluded both-dry cells.
+#ifndef CSPH_HLL_FAST
+#define CSPH_HLL_FAST 0
+#endif
 template <typename T>
 __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T eta_p, T H_p,
                                        T un_p, T ut_p, bool off, T& F0, T& F1, T& F2) {
@@ -121,6 +124,28 @@ __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T et
   // the three wave-speed cases of R, all evaluated, then selected
   const T aL = un_m - cm, aR = un_p - cp, bL2 = un_m + cm, bR2 = un_p + cp;
   const bool both = (wm & wp) != 0u;
+  const T fl1 = mm * un_m, fl2 = mm * ut_m, fr1 = mp * un_p, fr2 = mp * ut_p;
+  const T d0 = Hp - Hm, d1 = mp - mm, d2 = Hp * ut_p - Hm * ut_m;
+  if (CSPH_HLL_FAST && __all_sync(0xffffffffu, both & !off)) {
+    // warp-uniform common case (both reconstructed sides wet, a face of a wet cell): R's
+    // both-wet speeds without the dry-side selects; then, unless some lane is supercritical,
+    // the HLL average without the upwind selects.  Same operations, same values.
+    const T SL = smin_t(aL, aR), SR = smax_t(bL2, bR2);
+    const T inv = rcp_t(SR - SL);
+    const T SLSR = SL * SR;
+    const T h0 = ((SR * mm - SL * mp) + SLSR * d0) * inv;
+    const T h1 = ((SR * fl1 - SL * fr1) + SLSR * d1) * inv;
+    const T h2 = ((SR * fl2 - SL * fr2) + SLSR * d2) * inv;
+    const bool up = SL >= T(0), dn = SR <= T(0);
+    if (__any_sync(0xffffffffu, up | dn)) {
+      F0 = up ? mm : (dn ? mp : h0);
+      F1 = up ? fl1 : (dn ? fr1 : h1);
+      F2 = up ? fl2 : (dn ? fr2 : h2);
+    } else {
+      F0 = h0; F1 = h1; F2 = h2;
+    }
+    return;
+  }
   const T SL = both ? smin_t(aL, aR) : (dp ? aL : fma(T(-2), cp, un_p));
   const T SR = both ? smax_t(bL2, bR2) : (dp ? fma(T(2), cm, un_m) : bR2);
   // both reconstructed sides dry, or a both-dry face of cells (off): the face carries 0
@@ -128,10 +153,9 @@ __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T et
   const T den = none ? T(1) : (SR - SL);
   const T inv = rcp_t(den);
   const T SLSR = SL * SR;
-  const T fl1 = mm * un_m, fl2 = mm * ut_m, fr1 = mp * un_p, fr2 = mp * ut_p;
-  const T h0 = ((SR * mm - SL * mp) + SLSR * (Hp - Hm)) * inv;
-  const T h1 = ((SR * fl1 - SL * fr1) + SLSR * (mp - mm)) * inv;
-  const T h2 = ((SR * fl2 - SL * fr2) + SLSR * (Hp * ut_p - Hm * ut_m)) * inv;
+  const T h0 = ((SR * mm - SL * mp) + SLSR * d0) * inv;
+  const T h1 = ((SR * fl1 - SL * fr1) + SLSR * d1) * inv;
+  const T h2 = ((SR * fl2 - SL * fr2) + SLSR * d2) * inv;
   const bool up = SL >= T(0), dn = SR <= T(0);
   F0 = none ? T(0) : (up ? mm : (dn ? mp : h0));
   F1 = none ? T(0) : (up ? fl1 : (dn ? fr1 : h1));

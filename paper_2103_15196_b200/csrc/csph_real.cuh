@@ -82,7 +82,7 @@ __device__ __forceinline__ float icbrt_t(float x) {
 __device__ __forceinline__ unsigned long long dbits_t(double x) { return dbits(x); }
 __device__ __forceinline__ unsigned long long dbits_t(float x) { return dbits((double)x); }
 
-// K2/K5 face force (hydrostatic form), c_P/2 folded in (see face_force_h)
+// K2/K5 face force (hydrostatic form): (c_P/2 (H*_L + H*_R)) (H*_R - H*_L)
 template <typename T>
 __device__ __forceinline__ T face_force_t(T cPh, T etaL, T bL, T etaR, T bR) {
   T bs = smax_t(bL, bR);

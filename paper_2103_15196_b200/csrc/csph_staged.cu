@@ -50,10 +50,10 @@ __global__ void k2_forces(StripView S, const Ctrl* __restrict__ C, Scratch T, Ra
   if (!T.w[c]) { T.phix[c] = 0.0; T.phiy[c] = 0.0; T.gam[c] = 0.0; return; }
   const double* b = S.b[p];
   size_t e = c + 1, wv = c - 1, n = c + S.pitch, s = c - S.pitch;
-  double PE = face_force(P.cP, T.eta[c], b[c], T.eta[e], b[e]);
-  double PW = face_force(P.cP, T.eta[wv], b[wv], T.eta[c], b[c]);
-  double PN = face_force(P.cP, T.eta[c], b[c], T.eta[n], b[n]);
-  double PS = face_force(P.cP, T.eta[s], b[s], T.eta[c], b[c]);
+  double PE = face_force(P.cPh, T.eta[c], b[c], T.eta[e], b[e]);
+  double PW = face_force(P.cPh, T.eta[wv], b[wv], T.eta[c], b[c]);
+  double PN = face_force(P.cPh, T.eta[c], b[c], T.eta[n], b[n]);
+  double PS = face_force(P.cPh, T.eta[s], b[s], T.eta[c], b[c]);
   T.phix[c] = -(PE + PW);
   T.phiy[c] = -(PN + PS);
   if (S.cg) {  // NEXT-3 Manning field
@@ -100,10 +100,10 @@ __global__ void k5_forces_half(StripView S, const Ctrl* __restrict__ C, Scratch 
   const double* Hh = T.Hh;
   size_t e = c + 1, wv = c - 1, n = c + S.pitch, s = c - S.pitch;
   double ec = Hh[c] + b[c];
-  double PE = face_force(P.cP, ec, b[c], Hh[e] + b[e], b[e]);
-  double PW = face_force(P.cP, Hh[wv] + b[wv], b[wv], ec, b[c]);
-  double PN = face_force(P.cP, ec, b[c], Hh[n] + b[n], b[n]);
-  double PS = face_force(P.cP, Hh[s] + b[s], b[s], ec, b[c]);
+  double PE = face_force(P.cPh, ec, b[c], Hh[e] + b[e], b[e]);
+  double PW = face_force(P.cPh, Hh[wv] + b[wv], b[wv], ec, b[c]);
+  double PN = face_force(P.cPh, ec, b[c], Hh[n] + b[n], b[n]);
+  double PS = face_force(P.cPh, Hh[s] + b[s], b[s], ec, b[c]);
   T.phix2[c] = -(PE + PW);
   T.phiy2[c] = -(PN + PS);
 }
@@ -158,8 +158,8 @@ __global__ void k7_fluxes(StripView S, const Ctrl* __restrict__ C, Scratch T, Ra
   for (int k = 0; k < 4; ++k) {
     double sL = minmod(q[k][Lc] - q[k][LL], q[k][Rc] - q[k][Lc]);
     double sR = minmod(q[k][Rc] - q[k][Lc], q[k][RR] - q[k][Rc]);
-    qm[k] = q[k][Lc] + 0.5 * sL;
-    qp[k] = q[k][Rc] - 0.5 * sR;
+    qm[k] = fma(0.5, sL, q[k][Lc]);   // face states with one rounding
+    qp[k] = fma(-0.5, sR, q[k][Rc]);
   }
   double F0, F1, F2;
   hll_face(P.g, qm[0], qm[1], qm[2], qm[3], qp[0], qp[1], qp[2], qp[3], F0, F1, F2);

@@ -205,3 +205,34 @@ def test_C5_full_size_long_run(cs):
     g.destroy()
     assert abs(vol - vol0) <= 1e-10 * vol0
     assert abs(sed - sed0) <= 1e-10 * abs(sed0)
+
+
+def test_C5_literal_eq5_blow_up(cs):
+    """Reading #31 / DESIGN.md 3.15 reproduced at full size: with the literal Eq.5
+    (`h_bed_min = 0`, films of any depth carry bedload) the bench workload's bed at the
+    downstream wall end of the channel runs away within ~1000 steps -- the step ends in an
+    error, or tau collapses, or the bed moves by metres in one 100-step chunk.  The default
+    cut-off (h_bed_min = d50) runs the same 1200 steps cleanly (test_C5_full_size_long_run)."""
+    c = synth.config("C5")
+    f = synth.fill(c)
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, h_bed_min=0.0))
+    g.set_state(*f)
+    b0 = f[3][c.ny - 64:, :].copy()
+    del f
+    blew, why = False, ""
+    for chunk in range(12):
+        st = g.step(100, check=False)
+        if st != 0:
+            blew, why = True, f"status {st} in steps {100 * chunk}..{100 * chunk + 100}"
+            break
+        dt, _ = g.get_dt_log(100)
+        if dt.min() < 1e-3:
+            blew, why = True, f"tau {dt.min():.3g} s by step {100 * chunk + 100}"
+            break
+        b = g.get_state_rows(c.ny - 64, c.ny)[3]
+        if not np.all(np.isfinite(b)) or np.max(np.abs(b - b0)) > 50.0:
+            blew, why = True, f"|db| {np.nanmax(np.abs(b - b0)):.3g} m by step {100 * chunk + 100}"
+            break
+    g.destroy()
+    assert blew, "the literal Eq.5 run stayed bounded for 1200 steps"
+    print("literal Eq.5:", why)

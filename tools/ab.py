@@ -1,35 +1,49 @@
-"""A/B kernel timing of libcsph variants (dev aid): python tools/ab.py variants/libcsph_a.so ...
+"""A/B kernel timing of libcsph variants (dev aid, GPU):
 
-Each library runs in its own process (CSPH_LIB_DEV) on all-wet and C5 (N = $N, default 8192);
-prints the fused kernel's CUDA-event time per step and Gcell/s."""
-import os, subprocess, sys
+    python tools/ab.py variants/libcsph_a.so variants/libcsph_b.so ...
+
+Each library runs in its own process (the child points the binding's SO_PATH at it before
+the first call -- a tool-side override, the product binding has no switch) on the bench
+workload C5 (N = $N, default 16384) and an all-wet field (N/2), and prints the fused
+kernel's CUDA-event time per step (best of 3 x 10 steps) and Gcell/s.  Variants are
+interleaved over $ROUNDS rounds (default 2) so that clock drift hits all of them alike."""
+import os
+import subprocess
+import sys
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 code = r'''
 import os, sys
 sys.path.insert(0, %r)
 import numpy as np, torch, synth
 from paper_2103_15196_b200 import csph
-n = int(os.environ.get("N", "8192"))
+csph.SO_PATH = sys.argv[1]
+n = int(os.environ.get("N", "16384"))
 phys = dict(n_manning=0.03, A_J=0.001, C_J=2.0, C_Sh=4.0, d50=1e-3)
-x = np.linspace(0, 20 * np.pi, n)
+m = n // 2
+x = np.linspace(0, 20 * np.pi, m)
 X, Y = np.meshgrid(x, x)
-wet = (1.0 + 0.2 * np.sin(X) * np.cos(Y), 0.8 * np.ones((n, n)), 0.3 * np.ones((n, n)),
-       0.05 * np.cos(X + Y), np.full((n, n), 0.4))
+wet = (1.0 + 0.2 * np.sin(X) * np.cos(Y), 0.8 * np.ones((m, m)), 0.3 * np.ones((m, m)),
+       0.05 * np.cos(X + Y), np.full((m, m), 0.4))
 c = synth.config("C5", n)
 out = []
-for name, f, p in [("wet", wet, phys), ("C5", synth.fill(c), c.params)]:
-    g = csph.csph_create(n, n, 1.0, csph.params_from(p))
+for name, nn, f, p in [("C5", n, synth.fill(c), c.params), ("wet", m, wet, phys)]:
+    g = csph.csph_create(nn, nn, 1.0, csph.params_from(p))
     g.set_state(*f)
+    del f
     g.step(3); torch.cuda.synchronize()
     best = 1e9
     for rep in range(3):
         g.profile(True); g.step(10); torch.cuda.synchronize()
         ms, k = g.get_profile(); best = min(best, ms / k)
-    out.append("%%s %%.3f ms %%.2f Gcell/s" %% (name, best, n * n / best / 1e6))
+    out.append("%%s %%.3f ms %%.2f Gcell/s" %% (name, best, nn * nn / best / 1e6))
     g.destroy()
 print(" | ".join(out))
 ''' % ROOT
-for lib in sys.argv[1:]:
-    env = dict(os.environ, CSPH_LIB_DEV=os.path.abspath(lib))
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
-    print(os.path.basename(lib), r.stdout.strip(), r.stderr.strip()[-400:], flush=True)
+libs = sys.argv[1:]
+for rnd in range(int(os.environ.get("ROUNDS", "2"))):
+    for lib in libs:
+        r = subprocess.run([sys.executable, "-c", code, os.path.abspath(lib)], capture_output=True,
+                           text=True)
+        print(f"r{rnd} {os.path.basename(lib):28s}", r.stdout.strip(), r.stderr.strip()[-300:],
+              flush=True)

@@ -43,9 +43,9 @@ MUTATIONS = [
     ("K2 force sign", "o->phix[c] = -(PE + PW);", "o->phix[c] = (PE + PW);"),
     ("K2 west face swapped", "real PW = face_force(o->cP, o->eta[wv], b[wv], o->eta[c], b[c]);",
      "real PW = face_force(o->cP, o->eta[c], b[c], o->eta[wv], b[wv]);"),
-    ("face force b* = min", "double bs = sel_max(bL, bR);", "double bs = sel_min(bL, bR);"),
-    ("face force mean factor", "return (cP * (RL(0.5) * (HsL + HsR))) * (HsR - HsL);",
-     "return (cP * (HsL + HsR)) * (HsR - HsL);"),
+    ("face force b* = min", "real bs = sel_max(bL, bR);", "real bs = sel_min(bL, bR);"),
+    ("face force mean factor", "return (cPh * (HsL + HsR)) * (HsR - HsL);",
+     "return (cPh * (HsL + HsR + HsR)) * (HsR - HsL);"),
     ("friction H^(-1/3) dropped", "o->gam[c] = (o->cgam * sp) * (o->r[c] * r_icbrt(H[c]));",
      "o->gam[c] = (o->cgam * sp) * o->r[c];"),
     ("icbrt 4 Newton steps", "for (int k = 0; k < 5; ++k) {", "for (int k = 0; k < 2; ++k) {"),
@@ -60,14 +60,14 @@ MUTATIONS = [
     ("K6 theta", "o->QLy[c] = (Qy[c] + tau * o->phiy2[c]) * f;", "o->QLy[c] = (Qy[c] + theta * o->phiy2[c]) * f;"),
     # ---- K7
     ("minmod picks max", "if (a > RL(0) && b > RL(0)) return sel_min(a, b);", "if (a > RL(0) && b > RL(0)) return sel_max(a, b);"),
-    ("face state - sign", "qm[k] = q[k][L] + RL(0.5) * sL[k];", "qm[k] = q[k][L] - RL(0.5) * sL[k];"),
+    ("face state - sign", "qm[k] = FMA(RL(0.5), sL[k], q[k][L]);", "qm[k] = FMA(RL(-0.5), sL[k], q[k][L]);"),
     ("slope R wrong cells", "sR[k] = r_minmod(q[k][R] - q[k][L], q[k][RR] - q[k][R]);",
      "sR[k] = r_minmod(q[k][L] - q[k][LL], q[k][RR] - q[k][R]);"),
     ("HLL S_R dry factor 2", "SR = un_m + RL(2) * c_m;", "SR = un_m + c_m;"),
     ("HLL S_L both wet", "SL = sel_min(un_m - c_m, un_p - c_p);", "SL = sel_min(un_m - c_m, un_p + c_p);"),
     ("HLL dissipation sign", "out[k] = ((SR * FL[k] - SL * FR[k]) + SLSR * (UR[k] - UL[k])) * inv;",
      "out[k] = ((SR * FL[k] - SL * FR[k]) - SLSR * (UR[k] - UL[k])) * inv;"),
-    ("hydrostatic b* = min", "double bs = sel_max(b_m, b_p);", "double bs = sel_min(b_m, b_p);"),
+    ("hydrostatic b* = min", "real bs = sel_max(b_m, b_p);", "real bs = sel_min(b_m, b_p);"),
     ("donor reversed", "if (us > RL(0)) { Jn = J0n[L]; Ja = o->J0a[L]; }", "if (us < RL(0)) { Jn = J0n[L]; Ja = o->J0a[L]; }"),
     ("slope term sign", "return J0n - (C_J * J0abs) * db_dn;", "return J0n + (C_J * J0abs) * db_dn;"),
     ("grass |J0| drops sqrt", "*jabs = c * a;", "*jabs = c;"),
