@@ -52,6 +52,7 @@ class _Params(ctypes.Structure):
         ("C_J", ctypes.c_double), ("C_Sh", ctypes.c_double), ("d50", ctypes.c_double),
         ("q_plus", ctypes.c_double), ("q_minus", ctypes.c_double),
         ("aj_mode", ctypes.c_int), ("s_rel", ctypes.c_double), ("h_bed_min", ctypes.c_double),
+        ("m_real", ctypes.c_double),
     ]
 
 
@@ -73,12 +74,13 @@ class Params:
     aj_mode: int = 0
     s_rel: float = 2.65
     h_bed_min: float = -1.0  # reading #31 cut-off depth; < 0: d50
+    m_real: float = -1.0     # NEXT-4 real Grass exponent (pinned pow); < 0: m_grass
 
     def to_c(self) -> _Params:
         return _Params(self.g, self.K, self.eps_dry, self.dt_max, self.neg_tol,
                        self.n_manning, self.A_J, self.m_grass, self.C_J, self.C_Sh,
                        self.d50, self.q_plus, self.q_minus, self.aj_mode, self.s_rel,
-                       self.h_bed_min)
+                       self.h_bed_min, self.m_real)
 
 
 _libs = {}
@@ -112,6 +114,8 @@ def lib(precision: int = 64):
         L.orc_aj_eq4.argtypes = [ctypes.c_double] * 5
         L.orc_slope_flux.restype = ctypes.c_double
         L.orc_slope_flux.argtypes = [ctypes.c_double] * 4
+        L.orc_pow_pinned.restype = ctypes.c_double
+        L.orc_pow_pinned.argtypes = [ctypes.c_double] * 2
         L.orc_icbrt.restype = ctypes.c_double
         L.orc_icbrt.argtypes = [ctypes.c_double]
         L.orc_gamma.restype = ctypes.c_double
@@ -272,6 +276,11 @@ def slope_flux(J0n, J0abs, C_J, db_dn):
 
 def icbrt(x):
     return lib().orc_icbrt(x)
+
+
+def pow_pinned(x, q):
+    """The pinned x^q of DESIGN.md 3.12 (NEXT-4 real Grass exponent)."""
+    return lib().orc_pow_pinned(x, q)
 
 
 def gamma(params: Params, H, u, v):

@@ -112,15 +112,76 @@ static real r_icbrt(real x) {
 }
 #endif
 
+/* Pinned x^q for x >= 0, q >= 0 (NEXT-4 real Grass exponent): IEEE + - x /
+ * and integer bit operations only, the same sequence on CPU and GPU, so both sides agree
+ * bitwise; not correctly rounded (pinned vs 50-digit mpmath, <= 1e-13 relative).
+ *   x^0 = 1, 0^q = 0 (q > 0);  x = f 2^e with f in [sqrt(1/2), sqrt(2));
+ *   ln f = 2 atanh(z) = 2 z (1 + z^2/3 + ... + z^22/23), z = (f-1)/(f+1), |z| <= 0.1716;
+ *   y = q e + (q ln f) / ln 2 = q log2 x;  y < -1021 -> 0, y > 1023 -> +inf;
+ *   n = nearest integer to y (the 1.5 2^52 trick), r = y - n in [-1/2, 1/2] (exact);
+ *   2^r = exp(r ln 2) by its Taylor series to degree 14;  x^q = 2^r 2^n. */
+static double pow_pinned(double x, double q) {
+  static const double A[12] = {0x1.0000000000000p+0, 0x1.5555555555555p-2, 0x1.999999999999ap-3,
+                               0x1.2492492492492p-3, 0x1.c71c71c71c71cp-4, 0x1.745d1745d1746p-4,
+                               0x1.3b13b13b13b14p-4, 0x1.1111111111111p-4, 0x1.e1e1e1e1e1e1ep-5,
+                               0x1.af286bca1af28p-5, 0x1.8618618618618p-5, 0x1.642c8590b2164p-5};
+  static const double E[15] = {0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1,
+                               0x1.5555555555555p-3, 0x1.5555555555555p-5, 0x1.1111111111111p-7,
+                               0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13, 0x1.a01a01a01a01ap-16,
+                               0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
+                               0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33, 0x1.93974a8c07c9dp-37};
+  if (q == 0.0) return 1.0;
+  if (!(x > 0.0)) return 0.0;
+  uint64_t bits;
+  memcpy(&bits, &x, 8);
+  int e = (int)((bits >> 52) & 0x7FF);
+  if (e == 0) {  /* subnormal: scale by 2^64 (exact) */
+    double xs = x * 0x1p64;
+    memcpy(&bits, &xs, 8);
+    e = (int)((bits >> 52) & 0x7FF) - 64;
+  }
+  e -= 1023;
+  uint64_t fb = (bits & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
+  double f;
+  memcpy(&f, &fb, 8);
+  if (f > 0x1.6a09e667f3bcdp+0) { f = 0.5 * f; e += 1; }
+  double z = (f - 1.0) / (f + 1.0);
+  double w = z * z;
+  double p = A[11];
+  for (int k = 10; k >= 0; --k) p = p * w + A[k];
+  double lnf = (2.0 * z) * p;
+  double y = q * (double)e + (q * lnf) * 0x1.71547652b82fep+0;
+  if (y < -1021.0) return 0.0;
+  if (y > 1023.0) return INFINITY;
+  double n = (y + 0x1.8p52) - 0x1.8p52;
+  double r = y - n;
+  double t = r * 0x1.62e42fefa39efp-1;
+  double s = E[14];
+  for (int k = 13; k >= 0; --k) s = s * t + E[k];
+  uint64_t sb = (uint64_t)((int64_t)n + 1023) << 52;
+  double sc;
+  memcpy(&sc, &sb, 8);
+  return s * sc;
+}
+
+double orc_pow_pinned(double x, double q) { return pow_pinned(x, q); }
+
 /* Eq.3 with integer m (m = 2 on the hot path, NEXT-4 any 0..8): p = |v|^m by
  * repeated multiplication in s2 = |v|^2, then J0 = (A p) v and |J0| = (A p) |v|.  For
- * m = 2: p = 1 * s2 = s2 exactly, i.e. J0 = A_J v |v|^2, |J0| = A_J |v|^3. */
-static void r_grass_m(real A, int m, real vx, real vy, real* jx, real* jy, real* jabs) {
-  real s2 = vx * vx + vy * vy;
-  real a = SQRT(s2);
+ * m = 2: p = 1 * s2 = s2 exactly, i.e. J0 = A_J v |v|^2, |J0| = A_J |v|^3.  A real
+ * exponent mr >= 0 (NEXT-4, m_real) takes p = pow_pinned(s2, mr/2) instead. */
+static real grass_pow(int m, double mr, real s2, real a) {
+  if (mr >= 0.0) return RL(pow_pinned((double)s2, 0.5 * mr));
   real pw = RL(1);
   for (int k = 0; k < m / 2; ++k) pw = pw * s2;
   if (m % 2) pw = pw * a;
+  return pw;
+}
+
+static void r_grass_mr(real A, int m, double mr, real vx, real vy, real* jx, real* jy, real* jabs) {
+  real s2 = vx * vx + vy * vy;
+  real a = SQRT(s2);
+  real pw = grass_pow(m, mr, s2, a);
   real c = A * pw;
   *jx = c * vx;
   *jy = c * vy;
@@ -219,7 +280,7 @@ void orc_grass(double A_J, double vx, double vy, double* jx, double* jy, double*
 
 void orc_grass_m(double A, int m, double vx, double vy, double* jx, double* jy, double* jabs) {
   real x, y, a;
-  r_grass_m(RL(A), m, RL(vx), RL(vy), &x, &y, &a);
+  r_grass_mr(RL(A), m, -1.0, RL(vx), RL(vy), &x, &y, &a);
   *jx = x; *jy = y; *jabs = a;
 }
 
@@ -275,6 +336,7 @@ static int valid_params(const orc_params* p) {
   if (p->C_Sh > 0.0 && !(p->d50 > 0.0)) return 0;
   if (!isfinite(p->q_plus) || !isfinite(p->q_minus)) return 0;
   if (!isfinite(p->h_bed_min)) return 0;
+  if (!(p->m_real < 0.0) && !(p->m_real >= 0.0 && p->m_real <= 8.0)) return 0;
   return 1;
 }
 
@@ -391,9 +453,7 @@ static void reduce_M(orc_t* o, const real* H, const real* Qx, const real* Qy, do
       real t2 = a + SQRT(o->g * Hc);
       real t3 = RL(0);
       if (r_shamov_gate(o->kappa, s2, Hc, o->C_Sh) && r_bed_mobile(Hc, o->hbm)) {
-        real pw = RL(1);  /* |v|^m as in r_grass_m; m = 2: pw = s2 */
-        for (int k = 0; k < p->m_grass / 2; ++k) pw = pw * s2;
-        if (p->m_grass % 2) pw = pw * a;
+        real pw = grass_pow(p->m_grass, p->m_real, s2, a);  /* |v|^m; m = 2: pw = s2 */
         t3 = ((cell_aj(o, c, Hc) * pw) * a) * o->W[c];
       }
       /* max that lets NaN win */
@@ -644,7 +704,7 @@ int orc_step_tau(orc_t* o, double tau_d) {
     for (int i = -G + 1; i < nx + G - 1; ++i) {
       size_t c = IDX(o, i, j);
       real jx, jy, ja;
-      r_grass_m(cell_aj(o, c, H[c]), p->m_grass, o->ut[c], o->vt[c], &jx, &jy, &ja);
+      r_grass_mr(cell_aj(o, c, H[c]), p->m_grass, p->m_real, o->ut[c], o->vt[c], &jx, &jy, &ja);
       real s2 = o->ut[c] * o->ut[c] + o->vt[c] * o->vt[c];
       if (r_shamov_gate(o->kappa, s2, H[c], o->C_Sh) && r_bed_mobile(H[c], o->hbm)) {
         o->J0x[c] = jx; o->J0y[c] = jy; o->J0a[c] = ja;

@@ -52,6 +52,7 @@ typedef struct {
   int    aj_mode;  /* NEXT-4: 0 constant A_J; 1 Eq.4 A_J = 0.05 n_M^3/((s-1) sqrt(gH) d50) */
   double s_rel;    /* Eq.4 relative density rho_s/rho (> 1 in mode 1) */
   double h_bed_min;/* reading #31: no bedload where H <= h_bed_min; < 0 means d50 */
+  double m_real;   /* NEXT-4: real Grass exponent in [0, 8] by the pinned pow; < 0: m_grass */
 } orc_params;
 
 typedef struct orc orc_t;
@@ -97,6 +98,7 @@ void   orc_grass_m(double A, int m, double vx, double vy, double* jx, double* jy
 double orc_aj_eq4(double g, double n_manning, double s_rel, double H, double d50);
 double orc_slope_flux(double J0n, double J0abs, double C_J, double db_dn);
 double orc_icbrt(double x);                   /* pinned x^(-1/3) recipe */
+double orc_pow_pinned(double x, double q);    /* pinned x^q, x >= 0, q >= 0 */
 double orc_gamma(const orc_params* p, double H, double u, double v); /* Manning gamma */
 double orc_minmod(double a, double b);
 /* Hydrostatic step + HLL on the advective flux of Eq.6 for one face, from the

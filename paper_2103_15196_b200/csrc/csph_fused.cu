@@ -108,7 +108,7 @@ enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
 // hll_face() is evaluated with the same operations and the result selected, so
 // the value is bitwise identical.  Callers have already excluded both-dry cells.
 #ifndef CSPH_HLL_FAST
-#define CSPH_HLL_FAST 0
+#define CSPH_HLL_FAST 1
 #endif
 template <typename T>
 __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T eta_p, T H_p,
@@ -690,7 +690,7 @@ void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
   }
   // GEN: NEXT-3/4 features present or a physics term switched off; otherwise the
   // hot-path specialisation
-  const bool gen = !P.fric || !P.transport || P.m_grass != 2 || P.aj_mode || S.cg || S.beta || S.aj0 || S.bc_xlo != 1 ||
+  const bool gen = !P.fric || !P.transport || P.m_grass != 2 || P.m_real >= 0.0 || P.aj_mode || S.cg || S.beta || S.aj0 || S.bc_xlo != 1 ||
                    S.bc_xhi != 1 || S.wall_lo == 2 || S.wall_hi == 2 ||
                    !(P.g * P.eps >= 0x1p-890);  // dt_terms: sqrt(g H) without the zero guard
   if (S.W) {

@@ -13,6 +13,7 @@ template <typename T>
 struct PT {
   T g, eps, neg_tol, A_J, C_J, C_Sh, kappa, cPh, cgam, inv_h, inv_2h, src, d50, hbm;
   int m_grass, fric, transport;
+  double m_real;
 };
 
 template <typename T>
@@ -24,6 +25,7 @@ __device__ __forceinline__ PT<T> make_pt(const Phys& P) {
   q.d50 = T(P.d50);
   q.hbm = T(P.hbm);
   q.m_grass = P.m_grass; q.fric = P.fric; q.transport = P.transport;
+  q.m_real = P.m_real;
   return q;
 }
 
@@ -92,8 +94,12 @@ __device__ __forceinline__ T face_force_t(T cPh, T etaL, T bL, T etaR, T bR) {
 }
 
 template <bool GEN, typename T>
-__device__ __forceinline__ T pow_m_t(int m, T s2, T a) {
-  if (!GEN || m == 2) return s2;
+__device__ __forceinline__ T pow_m_t(int m, double mr, T s2, T a) {
+  if (!GEN) return s2;
+  if constexpr (sizeof(T) == 8) {
+    if (mr >= 0.0) return pow_pinned(s2, 0.5 * mr);  // NEXT-4 real exponent (fp64 only)
+  }
+  if (m == 2) return s2;
   T pw = T(1);
   for (int k = 0; k < m / 2; ++k) pw = pw * s2;
   if (m & 1) pw = pw * a;
@@ -105,7 +111,7 @@ __device__ __forceinline__ void grass_t(const PT<T>& P, T ut, T vt, T H, T A, T&
                                         T& ja) {
   T s2 = ut * ut + vt * vt;
   T sa = sqrt0_t(s2);
-  T a = A * pow_m_t<GEN>(P.m_grass, s2, sa);
+  T a = A * pow_m_t<GEN>(P.m_grass, P.m_real, s2, sa);
   // Eq.5 gate and reading #31: no bedload through a film (H <= h_bed_min, default d50)
   const bool gate = ((P.C_Sh == T(0)) | ((s2 * s2) * s2 > P.kappa * H)) & (H > P.hbm);
   jx = gate ? a * ut : T(0); jy = gate ? a * vt : T(0); ja = gate ? a * sa : T(0);
@@ -131,7 +137,7 @@ __device__ __forceinline__ void dt_terms_t(const PT<T>& P, T H, T Qx, T Qy, T W,
   t1 = s2;
   t2 = a + sqrt_gh_t<GEN>(P.g * H);
   bool gate = ((P.C_Sh == T(0)) || ((s2 * s2) * s2 > P.kappa * H)) && (H > P.hbm);
-  t3 = gate ? ((A * pow_m_t<GEN>(P.m_grass, s2, a)) * a) * W : T(0);
+  t3 = gate ? ((A * pow_m_t<GEN>(P.m_grass, P.m_real, s2, a)) * a) * W : T(0);
 }
 
 // Wall-only ghost writer (the hot-path specialisation), generic in T.

@@ -141,7 +141,10 @@ class BruteR:
 
     # ------------------------------------------------------------ closures
     def _grass_pow(self, s2):
-        """|v|^m of Eq.3, exact."""
+        """|v|^m of Eq.3, exact (the real exponent m_real when it is >= 0)."""
+        if self.p.get("m_real", -1) >= 0:
+            return mp.power(s2, self.p["m_real"] / 2) if s2 > 0 else (
+                _m(1) if self.p["m_real"] == 0 else _m(0))
         m = self.p["m_grass"]
         return mp.power(mp.sqrt(s2), m) if m % 2 else mp.power(s2, m // 2)
 

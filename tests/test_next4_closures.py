@@ -48,6 +48,47 @@ def test_grass_general_exponent():
     assert oracle.grass_m(0.002, 0, 3.0, 4.0) == (0.006, 0.008, 0.01)
 
 
+def test_pinned_pow_vs_mpmath():
+    """The pinned x^q of DESIGN.md 3.12 (NEXT-4 real Grass exponent, "m is a constant
+    coefficient"): within 1e-13 (relative) of 40-digit mpmath over the range Eq.3 meets
+    (s2 = |v|^2 in [1e-30, 1e4], q = m/2 in [0, 4]); exact special cases x^0 = 1, 0^q = 0,
+    and powers of two to integer powers."""
+    mp.mp.dps = 40
+    rng = np.random.default_rng(3103)
+    worst = 0.0
+    for _ in range(4000):
+        x = float(10.0 ** rng.uniform(-30, 4))
+        q = float(rng.uniform(0.0, 4.0))
+        y = oracle.pow_pinned(x, q)
+        worst = max(worst, float(abs(mp.mpf(y) / mp.mpf(x) ** mp.mpf(q) - 1)))
+    assert worst < 1e-13, worst
+    assert oracle.pow_pinned(0.7, 0.0) == 1.0 and oracle.pow_pinned(0.0, 0.0) == 1.0
+    assert oracle.pow_pinned(0.0, 1.25) == 0.0
+    for e in range(-20, 21, 3):
+        assert rel(oracle.pow_pinned(2.0 ** e, 1.5), 2.0 ** (1.5 * e)) < 1e-15
+
+
+def test_grass_real_exponent_closed_form():
+    """Eq.3 with m = 2.5: J0 = A v |v|^2.5; v = (3, 4), |v| = 5 -> |v|^2.5 = 25 sqrt 5, and the
+    Eq.7 bed term A |v|^3.5 / (1 - psi) of a single moving cell (40-digit closed forms)."""
+    mp.mp.dps = 40
+    A = 0.002
+    o = oracle.Oracle(3, 3, 1.0, oracle.Params(K=0.5, A_J=A, m_real=2.5))
+    h = np.zeros((3, 3)); h[1, 1] = 1.0
+    hu = np.zeros((3, 3)); hu[1, 1] = 3.0
+    hv = np.zeros((3, 3)); hv[1, 1] = 4.0
+    assert o.set_state(h, hu, hv, np.zeros((3, 3)), 0.4) == 0
+    M = o.reduce_M()
+    exact = mp.mpf(A) * mp.mpf(5) ** mp.mpf("3.5") / (1 - mp.mpf("0.4"))
+    assert rel(M[2], float(exact)) < 1e-13
+    # the integer path and the real path agree to the pow's accuracy at an integer m
+    o3 = oracle.Oracle(3, 3, 1.0, oracle.Params(K=0.5, A_J=A, m_grass=3))
+    o3r = oracle.Oracle(3, 3, 1.0, oracle.Params(K=0.5, A_J=A, m_real=3.0))
+    for oo in (o3, o3r):
+        oo.set_state(h, hu, hv, np.zeros((3, 3)), 0.4)
+    assert rel(o3r.reduce_M()[2], o3.reduce_M()[2]) < 1e-14
+
+
 def test_eq4_channel_exner_walls():
     """W2 (walled uniform current) with Eq.4's A_J: the bed changes only at the
     walls, by -/+ tau W A_J(H) u~^3 / h (closed form), where the Manning n_M that
@@ -85,7 +126,7 @@ def test_grass_m3_dt_term():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("path", [0, 1])
-@pytest.mark.parametrize("case", ["eq4_field", "eq4_scalar", "m3", "m0"])
+@pytest.mark.parametrize("case", ["eq4_field", "eq4_scalar", "m3", "m0", "m2.5", "m1.7_eq4"])
 def test_gpu_closure_parity(path, case):
     from paper_2103_15196_b200 import build, csph
     build.build()
@@ -93,11 +134,13 @@ def test_gpu_closure_parity(path, case):
     h, hu, hv, b, psi = synth.fill(c)
     p = dict(c.params)
     nfield = None
-    if case.startswith("eq4"):
+    if case.startswith("eq4") or case.endswith("eq4"):
         p.update(aj_mode=1, s_rel=2.65, A_J=0.0)
         if case == "eq4_field":
             nfield = 0.02 + 0.02 * np.random.default_rng(2).random((c.ny, c.nx))
-    else:
+    if case.startswith("m2.5") or case.startswith("m1.7"):
+        p.update(m_real=float(case[1:4]))  # real exponent, pinned pow
+    elif case in ("m3", "m0"):
         p.update(m_grass=3 if case == "m3" else 0)
     ref = oracle.Oracle(c.nx, c.ny, 1.0, oracle.Params(**p))
     ref.set_state(h, hu, hv, b, psi)

@@ -31,7 +31,7 @@ MARGIN = 1e-9
 def _params(**kw):
     p = dict(g=G, K=0.25, eps_dry=1e-6, dt_max=math.inf, neg_tol=1e-12, n_manning=0.03,
              A_J=0.02, m_grass=2, C_J=2.0, C_Sh=4.0, d50=1e-3, q_plus=0.0, q_minus=0.0,
-             aj_mode=0, s_rel=2.65, h_bed_min=-1.0)
+             aj_mode=0, s_rel=2.65, h_bed_min=-1.0, m_real=-1.0)
     p.update(kw)
     return p
 
@@ -57,6 +57,8 @@ def _random_case(seed, films=False, bc=None, fields=False, closures=False):
     prm = _params(eps_dry=eps, K=float(rs.uniform(0.12, 0.3)))
     if closures:  # NEXT-4: Eq.4 A_J at the local depth and an odd Grass exponent
         prm.update(aj_mode=1, m_grass=int(rs.choice([1, 3, 4])), d50=2e-4)
+        if rs.uniform() < 0.5:  # a real exponent through the pinned pow
+            prm.update(m_real=float(rs.uniform(1.2, 3.8)))
     if bc is None:
         bc = (1, 1, 1, 1)
     fl = {}

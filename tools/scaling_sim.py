@@ -1,7 +1,17 @@
 """Predicted strong scaling of C5 16384^2 on one GPU (dev aid): each rank's strip
 of rows [j0, j1) is run alone as a walled domain and its step time measured; the N-GPU step
-time is bounded below by the slowest strip (halo exchange and the allreduce are overlapped /
-small).  Compares the paper's even Ny_dev split with the wet-count-balanced one."""
+time is the slowest strip plus the communication the step cannot hide, modelled as:
+
+  * halo: 3 rows x 4 fields x the padded row (2 sides) over NVLink 5 at HALO_GBS (default
+    300 GB/s effective for ~1.6 MB NCCL send/recv) + HALO_US latency (default 15 us); it runs
+    on the comm stream while the interior tile rows compute, so only the part exceeding the
+    interior launch is exposed;
+  * the Eq.7 max-allreduce of 32 B: ALLRED_US (default 20 us, NCCL on 8 GPUs of one NVSwitch
+    node) -- fully exposed: the ctrl kernel needs tau before the next step;
+  * the split into 3 launches (edge, edge, interior) + ctrl instead of 2: LAUNCH_US per extra
+    launch gap (default 3 us).
+
+Compares the paper's even Ny_dev split with the wet-count-balanced one."""
 import os, sys
 os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")  # see bench.py
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -33,6 +43,20 @@ def strip_ms(j0, j1):
     return e0.elapsed_time(e1) / steps
 
 
+HALO_GBS = float(os.environ.get("HALO_GBS", "300"))
+HALO_US = float(os.environ.get("HALO_US", "15"))
+ALLRED_US = float(os.environ.get("ALLRED_US", "20"))
+LAUNCH_US = float(os.environ.get("LAUNCH_US", "3"))
+pitch = ((n + 4 + 3 + 4) + 31) // 32 * 32
+
+
+def comm_ms(rows, t_strip):
+    """Exposed communication per step of a strip of `rows` rows (see the module doc)."""
+    halo = 2 * 3 * 4 * pitch * 8 / (HALO_GBS * 1e9) * 1e3 + HALO_US * 1e-3
+    interior = t_strip * max(0.0, 1.0 - 2 * 128 / rows)  # the interior launch's share
+    return max(0.0, halo - interior) + ALLRED_US * 1e-3 + 2 * LAUNCH_US * 1e-3
+
+
 t1 = strip_ms(0, c.ny)
 print(f"N=1: {t1:.3f} ms/step, {c.cells / t1 / 1e6:.1f} Gcell/s", flush=True)
 for N in NS:
@@ -40,7 +64,10 @@ for N in NS:
         b = ([csph.csph_strip_rows(c.ny, N, r)[0] for r in range(N)] + [c.ny]) if kind == "even" \
             else csph.csph_balance_rows(c.ny, N, w)
         ts = [strip_ms(b[r], b[r + 1]) for r in range(N)]
-        tN = max(ts)
+        tc = [t + comm_ms(b[r + 1] - b[r], t) for r, t in enumerate(ts)]
+        tN, tNc = max(ts), max(tc)
         print(f"N={N} {kind:8s}: strips {[b[r + 1] - b[r] for r in range(N)]} ms "
               f"{[round(x, 3) for x in ts]} -> {c.cells / tN / 1e6:.1f} Gcell/s, "
-              f"efficiency {t1 / (N * tN):.2f}", flush=True)
+              f"efficiency {t1 / (N * tN):.2f} (compute only); with modelled comm "
+              f"{tNc:.3f} ms -> {c.cells / tNc / 1e6:.1f} Gcell/s, efficiency "
+              f"{t1 / (N * tNc):.2f}", flush=True)
