@@ -172,6 +172,26 @@ int         csph_strip_rows(int ny, int nranks, int rank, int* j0, int* j1);
  * on a NULL pointer, a negative/NaN weight, or ny < 3 * nranks. */
 int         csph_balance_rows(int ny, int nranks, const double* w, int* bounds);
 
+/* Per-row cost weights of the CURRENT state for csph_balance_rows: for every row j
+ * this handle owns (all rows of a single grid or MULTI handle; a DIST rank's own strip),
+ * w[j] = (wet cells of row j, H > eps_dry) + 0.03 nx -- the fused kernel's cost of a full row
+ * vs a dry one.  w is a host array of ny doubles indexed by the global row; entries of rows the
+ * handle does not own are left untouched (a DIST harness all-gathers them).  Syncs with the
+ * device.  CSPH_EINVAL on NULL, CSPH_ENOSTATE before set_state. */
+int         csph_row_weights(csph_t*, double* w);
+
+/* Re-partition a DIST or MULTI handle into the strips [bounds[r], bounds[r+1]) between two
+ * steps (collective: every rank calls it with the same bounds, e.g. from csph_balance_rows on
+ * all-gathered csph_row_weights).  The current state, W = 1/(1-psi) and the NEXT-3 fields
+ * migrate between strips (NCCL send/recv of full padded rows for DIST, a rank's rows to itself
+ * by a device copy; peer copies for MULTI); the control block (time, step count, tau of the
+ * next step, status), the dt log and the tile height rule carry over; HGS tile flags restart
+ * with every tile active (the first step marches all tiles).  Results are bitwise those of an
+ * unpartitioned run.  CSPH_EINVAL on a SINGLE handle or bad bounds (as csph_create_dist_rows),
+ * CSPH_ENOSTATE before set_state, CSPH_ENOMEM / CSPH_ECUDA / CSPH_ENCCL on failure (the
+ * handle is then unusable). */
+int         csph_rebalance_rows(csph_t*, const int* bounds);
+
 void        csph_destroy(csph_t*);
 const char* csph_strerror(int code);
 const char* csph_last_error(void);

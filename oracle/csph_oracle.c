@@ -90,7 +90,7 @@ static real r_icbrt(real x) {
   real y;
   memcpy(&y, &yb, 4);
   const real third = RL(1) / RL(3);
-  for (int k = 0; k < 3; ++k) y = y + y * ((RL(1) - x * ((y * y) * y)) * third);
+  for (int k = 0; k < 3; ++k) y = FMA(y, FMA(-x, (y * y) * y, RL(1)) * third, y);
   return y;
 }
 #else
@@ -105,8 +105,8 @@ static real r_icbrt(real x) {
   const real third = 1.0 / 3.0;
   for (int k = 0; k < 5; ++k) {
     real y3 = (y * y) * y;
-    real e = (1.0 - x * y3) * third;
-    y = y + y * e;
+    real e = FMA(-x, y3, 1.0) * third;
+    y = FMA(y, e, y);
   }
   return y;
 }
@@ -195,7 +195,7 @@ static real r_aj_eq4(real g, real n_manning, real s_rel, real H, real d50) {
 
 /* Eq.2, vector reading #4: J_n = J0_n - C_J |J0| db/dn */
 static real r_slope_flux(real J0n, real J0abs, real C_J, real db_dn) {
-  return J0n - (C_J * J0abs) * db_dn;
+  return FMA(-(C_J * J0abs), db_dn, J0n);
 }
 
 /* Eq.5 Shamov gate, reading #6: |v| > v_k  <=>  s2^3 > kappa*H */
@@ -667,10 +667,10 @@ int orc_step_tau(orc_t* o, double tau_d) {
       size_t c = IDX(o, i, j);
       if (!o->w[c]) { o->Hh[c] = H[c]; o->ut[c] = RL(0); o->vt[c] = RL(0); continue; }
       real div = ((o->u[c + sx] - o->u[c - sx]) + (o->v[c + sy] - o->v[c - sy])) * o->inv_2h;
-      o->Hh[c] = H[c] * (RL(1) - theta * div);
-      real f = RL(1) / (RL(1) + theta * o->gam[c]);
-      o->ut[c] = ((Qx[c] + theta * o->phix[c]) * f) * o->r[c];
-      o->vt[c] = ((Qy[c] + theta * o->phiy[c]) * f) * o->r[c];
+      o->Hh[c] = H[c] * FMA(-theta, div, RL(1));
+      real f = RL(1) / FMA(theta, o->gam[c], RL(1));
+      o->ut[c] = (FMA(theta, o->phix[c], Qx[c]) * f) * o->r[c];
+      o->vt[c] = (FMA(theta, o->phiy[c], Qy[c]) * f) * o->r[c];
     }
 
   /* Step 4 -- K5: forces at t_{n+1/2} from eta_half, step-n mask */
@@ -693,9 +693,9 @@ int orc_step_tau(orc_t* o, double tau_d) {
     for (int i = 0; i < nx; ++i) {
       size_t c = IDX(o, i, j);
       if (!o->w[c]) { o->QLx[c] = RL(0); o->QLy[c] = RL(0); continue; }
-      real f = RL(1) / (RL(1) + tau * o->gam[c]);
-      o->QLx[c] = (Qx[c] + tau * o->phix2[c]) * f;
-      o->QLy[c] = (Qy[c] + tau * o->phiy2[c]) * f;
+      real f = RL(1) / FMA(tau, o->gam[c], RL(1));
+      o->QLx[c] = FMA(tau, o->phix2[c], Qx[c]) * f;
+      o->QLy[c] = FMA(tau, o->phiy2[c], Qy[c]) * f;
     }
 
   /* Step 7a: per-cell Grass flux J0 (Eq.3) gated by Shamov (Eq.5) from
@@ -773,9 +773,9 @@ int orc_step_tau(orc_t* o, double tau_d) {
       real dQx = (o->FQx[e] - o->FQx[c]) + (o->GQx[n] - o->GQx[c]);
       real dQy = (o->FQy[e] - o->FQy[c]) + (o->GQy[n] - o->GQy[c]);
       real dJ = (o->FJ[e] - o->FJ[c]) + (o->GJ[n] - o->GJ[c]);
-      real Hn = H[c] - lam * dH;
-      real Qxn = o->QLx[c] - lam * dQx;
-      real Qyn = o->QLy[c] - lam * dQy;
+      real Hn = FMA(-lam, dH, H[c]);
+      real Qxn = FMA(-lam, dQx, o->QLx[c]);
+      real Qyn = FMA(-lam, dQy, o->QLy[c]);
       if (o->fields_src) {
         /* sigma = s - beta H (reading #21): source explicit, absorption implicit,
          * H' = ((H - lam dF) + tau s) / (1 + tau beta); momenta scaled alike */
@@ -784,7 +784,7 @@ int orc_step_tau(orc_t* o, double tau_d) {
         Qxn = Qxn * a;
         Qyn = Qyn * a;
       }
-      real bn = (b[c] - (lam * W[c]) * dJ) + (tau * W[c]) * src;
+      real bn = FMA(-(lam * W[c]), dJ, b[c]) + (tau * W[c]) * src;
       if (!(Hn > eps)) { Qxn = RL(0); Qyn = RL(0); }
       if (Hn < -o->neg_tol) neg = 1;
       o->Hn[c] = Hn; o->Qxn[c] = Qxn; o->Qyn[c] = Qyn; o->bn[c] = bn;

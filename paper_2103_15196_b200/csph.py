@@ -28,7 +28,7 @@ EXPORTS = [
     "csph_create_multi", "csph_create_multi_rows", "csph_create_dist_rows", "csph_balance_rows",
     "csph_last_launch_count", "csph_profile", "csph_get_profile",
     "csph_selftest_math", "csph_get_tile_stats", "csph_reset_tile_stats",
-    "csph_set_fields", "csph_set_fields_rows",
+    "csph_set_fields", "csph_set_fields_rows", "csph_row_weights", "csph_rebalance_rows",
 ]
 
 
@@ -111,6 +111,8 @@ def lib():
         L.csph_reset_tile_stats.argtypes = [_vp]
         L.csph_last_launch_count.argtypes = [_vp]
         L.csph_last_launch_count.restype = ctypes.c_longlong
+        L.csph_row_weights.argtypes = [_vp, _D]
+        L.csph_rebalance_rows.argtypes = [_vp, _I]
         _lib = L
     return _lib
 
@@ -276,6 +278,20 @@ class Csph:
 
     def last_launch_count(self) -> int:
         return lib().csph_last_launch_count(self.h)
+
+    def row_weights(self, w=None):
+        """Per-row cost weights of the current state (csph_row_weights) into w (ny doubles)."""
+        if w is None:
+            w = np.zeros(self.ny)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        assert w.shape == (self.ny,)
+        _check(lib().csph_row_weights(self.h, _p(w)), "csph_row_weights")
+        return w
+
+    def rebalance_rows(self, bounds):
+        """Move to new strip bounds (collective for DIST; csph_rebalance_rows)."""
+        b = (ctypes.c_int * len(bounds))(*bounds)
+        return _check(lib().csph_rebalance_rows(self.h, b), "csph_rebalance_rows")
 
 
 def _params(params: csph_params | dict | None) -> csph_params:

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/csph.h"
@@ -144,6 +145,7 @@ struct csph {
   Phys P{};
   Mode mode = SINGLE;
   int rank = 0, nranks = 1;
+  std::vector<int> bounds;  // DIST: the strip bounds of every rank [nranks + 1]
   ncclComm_t comm = nullptr;
   std::vector<Strip> s;
   bool have_state = false;
@@ -425,6 +427,17 @@ __global__ void selftest_math_kernel(long long n, unsigned long long seed, int l
     double x = __longlong_as_double((long long)((e << 52) | (z & 0xFFFFFFFFFFFFFull)));
     if (rcp_nb(x) != 1.0 / x) nb++;
     if (sqrt_nb(x) != sqrt(x)) nb++;
+    {  // structured significands: all ones, near all ones, near zero, one bit cleared
+      const unsigned long long ONES = 0xFFFFFFFFFFFFFull;
+      const unsigned long long k = (unsigned long long)i;
+      const unsigned long long ms[3] = {ONES - (k & 255), k & 255, ONES ^ (1ull << (k % 52))};
+      for (int q = 0; q < 3; ++q) {
+        const double y = __longlong_as_double((long long)((e << 52) | ms[q]));
+        if (rcp_nb(y) != 1.0 / y) nb++;
+        if (sqrt_nb(y) != sqrt(y)) nb++;
+        if (sqrt0nb(y) != sqrt(y)) nb++;
+      }
+    }
     double t = x * 0x1p-1000;  // tiny and subnormal arguments of sqrt0nb
     if (sqrt0nb(t) != sqrt(t)) nb++;
     if (sqrt0nb(x) != sqrt(x)) nb++;
@@ -647,10 +660,10 @@ static void strip_free(Strip& s) {
 namespace {
 // Wet flags of the 120-column x kTyMin-row blocks of the current state (buffer 0).
 template <typename T>
-__global__ void wet_blocks_kernel(StripView S, double eps, unsigned char* out) {
+__global__ void wet_blocks_kernel(StripView S, double eps, unsigned char* out, int buf) {
   const int bx = blockIdx.x, by = blockIdx.y, t = threadIdx.x;
   const int col = bx * FUSED_TX + t;
-  const T* H = reinterpret_cast<const T*>(S.H[0]);
+  const T* H = reinterpret_cast<const T*>(S.H[buf]);
   bool wet = false;
   if (t < FUSED_TX && col < S.nx) {
     const int j1 = min(S.ny, (by + 1) * kTyMin);
@@ -658,6 +671,25 @@ __global__ void wet_blocks_kernel(StripView S, double eps, unsigned char* out) {
   }
   wet = __syncthreads_or(wet);
   if (t == 0) out[by * gridDim.x + bx] = wet ? 1 : 0;
+}
+
+// Wet cells per owned row of buffer `buf` (one block per row): the cost model of the row-strip
+// partition.
+template <typename T>
+__global__ void row_wet_kernel(StripView S, double eps, int buf, int* out) {
+  const int j = blockIdx.x;
+  const T* H = reinterpret_cast<const T*>(S.H[buf]);
+  int n = 0;
+  for (int i = threadIdx.x; i < S.nx; i += blockDim.x) n += (double)H[off(S.pitch, i, j)] > eps;
+  n = __reduce_add_sync(0xffffffffu, n);
+  __shared__ int part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w];
+    out[j] = s;
+  }
 }
 
 }  // namespace
@@ -912,6 +944,7 @@ csph_t* csph_create_dist_rows(int nx, int ny, double dx, const csph_params* p, i
   H->mode = DIST;
   H->rank = rank;
   H->nranks = nranks;
+  H->bounds.assign(bounds, bounds + nranks + 1);
   H->s.resize(1);
   if (strip_init(H, H->s[0], local_device, j0, j1 - j0, p->path == CSPH_PATH_STAGED)) {
     std::string keep = g_err;
@@ -1308,13 +1341,13 @@ static int upload_rows(csph* H, Strip& s, int j_begin, int j_end, const double* 
 // wet tiles make 2.5 waves of 3 resident CTAs per SM -- while keeping the launch of the
 // skipped ones cheap (at most 40 K tiles in all).  Measured on one B200: C3 4096^2 -> 32 rows
 // (+22 % over 128), C4 8192^2 -> 64 (+9 %), C5 16384^2 -> 128.
-static int choose_tile_rows(csph* H, Strip& s) {
+static int choose_tile_rows(csph* H, Strip& s, int buf = 0) {
   const int nby = (s.v.ny + kTyMin - 1) / kTyMin;
   dim3 grd((unsigned)s.ntx, (unsigned)nby);
   if (s.v.prec == 4)
-    wet_blocks_kernel<float><<<grd, 128, 0, s.st>>>(s.v, H->P.eps, s.wetblk);
+    wet_blocks_kernel<float><<<grd, 128, 0, s.st>>>(s.v, H->P.eps, s.wetblk, buf);
   else
-    wet_blocks_kernel<double><<<grd, 128, 0, s.st>>>(s.v, H->P.eps, s.wetblk);
+    wet_blocks_kernel<double><<<grd, 128, 0, s.st>>>(s.v, H->P.eps, s.wetblk, buf);
   H->launches += 1;
   CK(cudaGetLastError());
   std::vector<unsigned char> w((size_t)s.ntx * nby);
@@ -1861,6 +1894,214 @@ int csph_get_maxima(csph_t* H, double M[3]) {
   CK(cudaSetDevice(s.dev));
   CK(cudaStreamSynchronize(s.st));
   CK(cudaMemcpy(M, s.Mlast, 3 * 8, cudaMemcpyDeviceToHost));
+  return CSPH_OK;
+}
+
+// ---- load balance during a run ----
+
+int csph_row_weights(csph_t* H, double* w) {
+  if (!H || !w) return fail(CSPH_EINVAL, "bad argument");
+  if (!H->have_state) return fail(CSPH_ENOSTATE, "no state");
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    int* d = nullptr;
+    CK(cudaMallocAsync((void**)&d, (size_t)s.v.ny * sizeof(int), s.st));
+    if (s.v.prec == 4)
+      row_wet_kernel<float><<<s.v.ny, 256, 0, s.st>>>(s.v, H->P.eps, H->host_parity, d);
+    else
+      row_wet_kernel<double><<<s.v.ny, 256, 0, s.st>>>(s.v, H->P.eps, H->host_parity, d);
+    CK(cudaGetLastError());
+    std::vector<int> cnt(s.v.ny);
+    CK(cudaMemcpyAsync(cnt.data(), d, cnt.size() * sizeof(int), cudaMemcpyDeviceToHost, s.st));
+    CK(cudaFreeAsync(d, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    for (int j = 0; j < s.v.ny; ++j) w[s.gj0 + j] = (double)cnt[j] + 0.03 * (double)H->nx;
+  }
+  return CSPH_OK;
+}
+
+namespace {
+// One field of the row migration: for every pair (old strip o, new strip r) the rows of o's
+// owned range that r needs (its owned rows and, at interior edges, its 3 ghost rows),
+// full padded width.  Peer copies between the strips of one process (MULTI) or NCCL
+// send/recv between ranks (DIST; a rank's rows to itself by a device copy).
+struct MigField {
+  std::vector<char*> oldp;  // per old strip (DIST: only entry 0, this rank)
+  std::vector<char*> newp;  // per new strip
+  size_t es;                // element size
+};
+
+int migrate_field(csph* H, const std::vector<Strip>& olds, const std::vector<Strip>& news,
+                  const std::vector<int>& ob, const std::vector<int>& nb, const MigField& f) {
+  const int ny = H->ny;
+  const size_t rowb = (size_t)news[0].v.pitch * f.es;
+  const int nr = (int)nb.size() - 1;
+  auto need = [&](int r, int* a, int* b) {  // rows [a, b) new strip r needs (global)
+    *a = r > 0 ? nb[r] - GY : 0;
+    *b = r < nr - 1 ? nb[r + 1] + GY : ny;
+    if (*a < 0) *a = 0;
+    if (*b > ny) *b = ny;
+  };
+  if (H->mode == MULTI) {
+    for (int r = 0; r < nr; ++r) {
+      const Strip& ns = news[r];
+      CK(cudaSetDevice(ns.dev));
+      int a, b;
+      need(r, &a, &b);
+      for (int o = 0; o + 1 < (int)ob.size(); ++o) {
+        const int lo = a > ob[o] ? a : ob[o], hi = b < ob[o + 1] ? b : ob[o + 1];
+        if (hi <= lo) continue;
+        CK(cudaMemcpyPeerAsync(f.newp[r] + f.es * off(ns.v.pitch, -GX, lo - nb[r]), ns.dev,
+                               f.oldp[o] + f.es * off(olds[o].v.pitch, -GX, lo - ob[o]),
+                               olds[o].dev, (size_t)(hi - lo) * rowb, ns.st));
+      }
+    }
+    return CSPH_OK;
+  }
+  // DIST: this rank sends the parts of its old rows every new strip needs, and receives the
+  // parts of its new rows from their old owners
+  const int me = H->rank;
+  const Strip& ns = news[0];
+  int a, b;
+  need(me, &a, &b);
+  NK(g_nccl.GroupStart());
+  for (int o = 0; o < nr; ++o) {  // receive from old owner o
+    if (o == me) continue;
+    const int lo = a > ob[o] ? a : ob[o], hi = b < ob[o + 1] ? b : ob[o + 1];
+    if (hi <= lo) continue;
+    NK(g_nccl.Recv(f.newp[0] + f.es * off(ns.v.pitch, -GX, lo - nb[me]), (size_t)(hi - lo) * rowb,
+                   ncclChar, o, H->comm, ns.st));
+  }
+  for (int d = 0; d < nr; ++d) {  // send to new owner d
+    if (d == me) continue;
+    int da, db;
+    need(d, &da, &db);
+    const int lo = da > ob[me] ? da : ob[me], hi = db < ob[me + 1] ? db : ob[me + 1];
+    if (hi <= lo) continue;
+    NK(g_nccl.Send(f.oldp[0] + f.es * off(olds[0].v.pitch, -GX, lo - ob[me]),
+                   (size_t)(hi - lo) * rowb, ncclChar, d, H->comm, ns.st));
+  }
+  NK(g_nccl.GroupEnd());
+  const int lo = a > ob[me] ? a : ob[me], hi = b < ob[me + 1] ? b : ob[me + 1];
+  if (hi > lo)
+    CK(cudaMemcpyAsync(f.newp[0] + f.es * off(ns.v.pitch, -GX, lo - nb[me]),
+                       f.oldp[0] + f.es * off(olds[0].v.pitch, -GX, lo - ob[me]),
+                       (size_t)(hi - lo) * rowb, cudaMemcpyDeviceToDevice, ns.st));
+  return CSPH_OK;
+}
+}  // namespace
+
+int csph_rebalance_rows(csph_t* H, const int* bounds) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  if (H->mode == SINGLE) return fail(CSPH_EINVAL, "rebalance needs a DIST or MULTI handle");
+  if (!H->have_state) return fail(CSPH_ENOSTATE, "no state");
+  const int nr = H->nranks;
+  if (check_bounds(H->ny, nr, bounds)) return CSPH_EINVAL;
+  std::vector<int> nb(bounds, bounds + nr + 1), ob(nr + 1);
+  // the current bounds (every rank knows them: identical on all ranks)
+  if (H->mode == MULTI) {
+    for (int r = 0; r < nr; ++r) ob[r] = H->s[r].gj0;
+  } else {
+    ob = H->bounds;
+  }
+  ob[nr] = H->ny;
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.st));
+    CK(cudaStreamSynchronize(s.cst));
+  }
+  graphs_reset(H);
+  const int p = H->host_parity;
+  std::vector<Strip> news(H->mode == MULTI ? nr : 1);
+  const bool staged = H->p.path == CSPH_PATH_STAGED;
+  int st;
+  for (size_t k = 0; k < news.size(); ++k) {
+    const int r = H->mode == MULTI ? (int)k : H->rank;
+    const int dev = H->s[k].dev;
+    if ((st = strip_init(H, news[k], dev, nb[r], nb[r + 1] - nb[r], staged))) {
+      for (auto& s : news) strip_free(s);
+      return st;
+    }
+  }
+  std::vector<Strip>& olds = H->s;
+  const size_t es = (size_t)olds[0].v.prec;
+  auto run = [&](std::function<char*(Strip&)> get, size_t esz) -> int {
+    MigField f;
+    f.es = esz;
+    for (auto& s : olds) f.oldp.push_back(get(s));
+    for (auto& s : news) f.newp.push_back(get(s));
+    return migrate_field(H, olds, news, ob, nb, f);
+  };
+  // static fields first: allocate them on the new strips where the old ones have them
+  const bool hasW = olds[0].v.W != nullptr;
+  for (auto& s : news) {
+    CK(cudaSetDevice(s.dev));
+    const size_t n = (size_t)(s.v.ny + 2 * GY) * s.v.pitch;
+    s.v.Wc = olds[0].v.Wc;
+    if (hasW) {
+      if ((st = dalloc(s, (void**)&s.Wbuf, n * 8))) return st;
+      CK(cudaMemsetAsync(s.Wbuf, 0, n * 8, s.st));
+      if (es == 4) {
+        if ((st = dalloc(s, (void**)&s.Wbuf32, n * 4))) return st;
+        CK(cudaMemsetAsync(s.Wbuf32, 0, n * 4, s.st));
+        s.v.W = (const double*)s.Wbuf32;
+      } else {
+        s.v.W = s.Wbuf;
+      }
+    }
+    double** fl[4] = {&s.cgbuf, &s.betabuf, &s.srcbuf, &s.ajbuf};
+    const double* have[4] = {olds[0].cgbuf, olds[0].betabuf, olds[0].srcbuf, olds[0].ajbuf};
+    for (int q = 0; q < 4; ++q)
+      if (have[q]) {
+        if ((st = dalloc(s, (void**)fl[q], n * 8))) return st;
+        CK(cudaMemsetAsync(*fl[q], 0, n * 8, s.st));
+      }
+    s.v.cg = s.cgbuf; s.v.beta = s.betabuf; s.v.src = s.srcbuf; s.v.aj0 = s.ajbuf;
+  }
+  if (hasW) {
+    if (es == 4) { if ((st = run([](Strip& s) { return (char*)s.Wbuf32; }, 4))) return st; }
+    else if ((st = run([](Strip& s) { return (char*)s.Wbuf; }, 8))) return st;
+  }
+  if (olds[0].cgbuf && (st = run([](Strip& s) { return (char*)s.cgbuf; }, 8))) return st;
+  if (olds[0].betabuf && (st = run([](Strip& s) { return (char*)s.betabuf; }, 8))) return st;
+  if (olds[0].srcbuf && (st = run([](Strip& s) { return (char*)s.srcbuf; }, 8))) return st;
+  if (olds[0].ajbuf && (st = run([](Strip& s) { return (char*)s.ajbuf; }, 8))) return st;
+  // the current state (buffer p)
+  if ((st = run([p](Strip& s) { return (char*)s.v.H[p]; }, es))) return st;
+  if ((st = run([p](Strip& s) { return (char*)s.v.Qx[p]; }, es))) return st;
+  if ((st = run([p](Strip& s) { return (char*)s.v.Qy[p]; }, es))) return st;
+  if ((st = run([p](Strip& s) { return (char*)s.v.b[p]; }, es))) return st;
+  // control block, dt log and last maxima carry over (identical on every strip / rank)
+  for (size_t k = 0; k < news.size(); ++k) {
+    Strip& s = news[k];
+    const Strip& o = olds[H->mode == MULTI ? 0 : k];
+    CK(cudaSetDevice(s.dev));
+    CK(cudaMemcpyPeerAsync(s.ctrl, s.dev, o.ctrl, o.dev, sizeof(Ctrl), s.st));
+    CK(cudaMemcpyPeerAsync(s.dtlog, s.dev, o.dtlog, o.dev, LOGCAP * sizeof(double), s.st));
+    CK(cudaMemcpyPeerAsync(s.limlog, s.dev, o.limlog, o.dev, LOGCAP * sizeof(int), s.st));
+    CK(cudaMemcpyPeerAsync(s.Mlast, s.dev, o.Mlast, o.dev, 4 * sizeof(double), s.st));
+    // wall ghosts of the state buffer and of the static fields (interior edges: migrated)
+    launch_mirror(s.v, s.ctrl, 0, s.st, &H->launches);
+    for (double* F : {s.cgbuf, s.betabuf, s.srcbuf, s.ajbuf}) {
+      if (!F) continue;
+      int n1 = (s.v.ny + 2 * GY) * 6, n2 = (s.v.nx + 6) * 6;
+      mirror_field_kernel<<<(n1 + 255) / 256, 256, 0, s.st>>>(s.v, F);
+      mirror_field_y_kernel<<<(n2 + 255) / 256, 256, 0, s.st>>>(s.v, F);
+    }
+    CK(cudaGetLastError());
+    if (s.auto_ty && H->p.path == CSPH_PATH_FUSED && (st = choose_tile_rows(H, s, p))) return st;
+    CK(cudaStreamSynchronize(s.st));
+  }
+  // a caller stream (csph_set_stream, single-strip handles) carries over
+  if (H->s.size() == 1 && !H->s[0].own_stream) {
+    CK(cudaSetDevice(news[0].dev));
+    CK(cudaStreamDestroy(news[0].st));
+    news[0].st = H->s[0].st;
+    news[0].own_stream = false;
+  }
+  for (auto& s : H->s) strip_free(s);
+  H->s = std::move(news);
+  if (H->mode == DIST) H->bounds = nb;
   return CSPH_OK;
 }
 

@@ -243,9 +243,9 @@ __global__ void __launch_bounds__(NT, MINB)
             const T H3 = gin[0][o], b3 = gin[3][o];
             const T W3 = HASW ? gin[4][o] : T(S.Wc);
             const T z = T(0) + (T(0) - T(0));
-            T Hn = H3 - lam * z;
-            T Qn = T(0) - lam * z, Qm = Qn;
-            const T bn = (b3 - (lam * W3) * z) + (tau * W3) * Q.src;
+            T Hn = fma(-lam, z, H3);
+            T Qn = fma(-lam, z, T(0)), Qm = Qn;
+            const T bn = fma(-(lam * W3), z, b3) + (tau * W3) * Q.src;
             if constexpr (GEN) apply_sources(S, tau, o, Hn, Qn, Qm);
             if (Hn > Q.eps) cwet = true;  // momenta stay +0 (they were +0 * a)
             if constexpr (GEN)
@@ -464,10 +464,10 @@ __global__ void __launch_bounds__(NT, MINB)
         const T dQx = dF3[1] + (Gn[1] - Gs[1]);
         const T dQy = dF3[2] + (Gn[2] - Gs[2]);
         const T dJ = dF3[3] + (Gn[3] - Gs[3]);
-        T Hn = H3 - lam * dH;
-        T Qxn = QLx3 - lam * dQx;
-        T Qyn = QLy3 - lam * dQy;
-        const T bn = (b3 - (lam * W3) * dJ) + (tau * W3) * Q.src;
+        T Hn = fma(-lam, dH, H3);
+        T Qxn = fma(-lam, dQx, QLx3);
+        T Qyn = fma(-lam, dQy, QLy3);
+        const T bn = fma(-(lam * W3), dJ, b3) + (tau * W3) * Q.src;
         if constexpr (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
         store_update(Hn, Qxn, Qyn, bn, W3, j);
       }
@@ -511,9 +511,9 @@ __global__ void __launch_bounds__(NT, MINB)
       T QLx2 = T(0), QLy2 = T(0);
       if (ANYW(w2)) {
         const T phy2h = -(PhN2 + PhS);
-        const T f1 = FRIC ? rcp_t(T(1) + tau * gam2) : T(1);
-        const T qx = (RG(F_QX, km2, 0) + tau * phx2h) * f1;
-        const T qy = (RG(F_QY, km2, 0) + tau * phy2h) * f1;
+        const T f1 = FRIC ? rcp_t(fma(tau, gam2, T(1))) : T(1);
+        const T qx = fma(tau, phx2h, RG(F_QX, km2, 0)) * f1;
+        const T qy = fma(tau, phy2h, RG(F_QY, km2, 0)) * f1;
         QLx2 = w2 ? qx : T(0); QLy2 = w2 ? qy : T(0);
       }
       PhS = PhN2;
@@ -579,10 +579,10 @@ __global__ void __launch_bounds__(NT, MINB)
         if (ANYW(w0)) {
           const T* Uc = sm.U[k & 1];
           T div = ((XG(Uc, 1) - XG(Uc, -1)) + (av0 - vm1)) * Q.inv_2h;
-          const T hh = H0 * (T(1) - theta * div);
-          const T f = FRIC ? rcp_t(T(1) + theta * gam0) : T(1);  // gam0 = 0 when dry
-          const T uu = ((RG(F_QX, k, 0) + theta * phix0) * f) * r0;
-          const T vv = ((RG(F_QY, k, 0) + theta * aphiy1) * f) * r0;
+          const T hh = H0 * fma(-theta, div, T(1));
+          const T f = FRIC ? rcp_t(fma(theta, gam0, T(1))) : T(1);  // gam0 = 0 when dry
+          const T uu = (fma(theta, phix0, RG(F_QX, k, 0)) * f) * r0;
+          const T vv = (fma(theta, aphiy1, RG(F_QY, k, 0)) * f) * r0;
           Hh = w0 ? hh : H0; ut = w0 ? uu : T(0); vt = w0 ? vv : T(0);
         }
         T jx = T(0), jy = T(0), ja = T(0);
@@ -603,10 +603,10 @@ __global__ void __launch_bounds__(NT, MINB)
         const T dQx = dF3[1] + (Gn[1] - Gs[1]);
         const T dQy = dF3[2] + (Gn[2] - Gs[2]);
         const T dJ = dF3[3] + (Gn[3] - Gs[3]);
-        T Hn = H3 - lam * dH;
-        T Qxn = QLx3 - lam * dQx;
-        T Qyn = QLy3 - lam * dQy;
-        const T bn = (b3 - (lam * W3) * dJ) + (tau * W3) * Q.src;
+        T Hn = fma(-lam, dH, H3);
+        T Qxn = fma(-lam, dQx, QLx3);
+        T Qyn = fma(-lam, dQy, QLy3);
+        const T bn = fma(-(lam * W3), dJ, b3) + (tau * W3) * Q.src;
         if constexpr (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
         store_update(Hn, Qxn, Qyn, bn, W3, j);
       }

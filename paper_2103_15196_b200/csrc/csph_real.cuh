@@ -78,7 +78,7 @@ __device__ __forceinline__ float icbrt_t(float x) {
   float y = __int_as_float(0x54A2FA8C - __float_as_int(x) / 3);
   const float third = 1.0f / 3.0f;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) y = y + y * ((1.0f - x * ((y * y) * y)) * third);
+  for (int k = 0; k < 3; ++k) y = fmaf(y, fmaf(-x, (y * y) * y, 1.0f) * third, y);
   return y;
 }
 __device__ __forceinline__ unsigned long long dbits_t(double x) { return dbits(x); }
@@ -124,7 +124,7 @@ __device__ __forceinline__ T sed_face_t(const PT<T>& P, T unL, T unR, T JnL, T J
   const bool up = us > T(0), dn = us < T(0);
   const T Jn = up ? JnL : (dn ? JnR : T(0.5) * (JnL + JnR));
   const T Ja = up ? JaL : (dn ? JaR : T(0.5) * (JaL + JaR));
-  return Jn - (P.C_J * Ja) * ((bR - bL) * P.inv_h);
+  return fma(-(P.C_J * Ja), (bR - bL) * P.inv_h, Jn);
 }
 
 template <bool GEN, typename T>

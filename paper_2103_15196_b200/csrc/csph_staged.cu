@@ -81,10 +81,10 @@ __global__ void k4_predictor(StripView S, const Ctrl* __restrict__ C, Scratch T,
   if (!T.w[c]) { T.Hh[c] = H; T.ut[c] = 0.0; T.vt[c] = 0.0; return; }
   const double theta = 0.5 * C->tau;
   double div = ((T.u[c + 1] - T.u[c - 1]) + (T.v[c + S.pitch] - T.v[c - S.pitch])) * P.inv_2h;
-  T.Hh[c] = H * (1.0 - theta * div);
-  double f = 1.0 / (1.0 + theta * T.gam[c]);
-  T.ut[c] = ((S.Qx[p][c] + theta * T.phix[c]) * f) * T.r[c];
-  T.vt[c] = ((S.Qy[p][c] + theta * T.phiy[c]) * f) * T.r[c];
+  T.Hh[c] = H * fma(-theta, div, 1.0);
+  double f = 1.0 / fma(theta, T.gam[c], 1.0);
+  T.ut[c] = (fma(theta, T.phix[c], S.Qx[p][c]) * f) * T.r[c];
+  T.vt[c] = (fma(theta, T.phiy[c], S.Qy[p][c]) * f) * T.r[c];
 }
 
 // K5: forces at t_{n+1/2}
@@ -126,9 +126,9 @@ __global__ void k6_corrector(StripView S, const Ctrl* __restrict__ C, Scratch T,
   size_t c = off(S.pitch, i, j);
   if (!T.w[c]) { T.QLx[c] = 0.0; T.QLy[c] = 0.0; return; }
   const double tau = C->tau;
-  double f = 1.0 / (1.0 + tau * T.gam[c]);
-  T.QLx[c] = (S.Qx[p][c] + tau * T.phix2[c]) * f;
-  T.QLy[c] = (S.Qy[p][c] + tau * T.phiy2[c]) * f;
+  double f = 1.0 / fma(tau, T.gam[c], 1.0);
+  T.QLx[c] = fma(tau, T.phix2[c], S.Qx[p][c]) * f;
+  T.QLy[c] = fma(tau, T.phiy2[c], S.Qy[p][c]) * f;
 }
 
 // K7: one face per thread. axis 0: face between (i-1,j),(i,j).
@@ -187,10 +187,10 @@ __global__ void k8_update(StripView S, Ctrl* C, Scratch T, Range R, Phys P,
     double dQx = (T.FQx[e] - T.FQx[c]) + (T.GQx[n] - T.GQx[c]);
     double dQy = (T.FQy[e] - T.FQy[c]) + (T.GQy[n] - T.GQy[c]);
     double dJ = (T.FJ[e] - T.FJ[c]) + (T.GJ[n] - T.GJ[c]);
-    double Hn = S.H[p][c] - lam * dH;
-    double Qxn = T.QLx[c] - lam * dQx;
-    double Qyn = T.QLy[c] - lam * dQy;
-    double bn = (S.b[p][c] - (lam * W) * dJ) + (tau * W) * P.src;
+    double Hn = fma(-lam, dH, S.H[p][c]);
+    double Qxn = fma(-lam, dQx, T.QLx[c]);
+    double Qyn = fma(-lam, dQy, T.QLy[c]);
+    double bn = fma(-(lam * W), dJ, S.b[p][c]) + (tau * W) * P.src;
     apply_sources(S, tau, c, Hn, Qxn, Qyn);
     bool wet = Hn > P.eps;
     if (!wet) { Qxn = 0.0; Qyn = 0.0; }

@@ -240,3 +240,73 @@ def test_nonfinite_maxima(cs):
     for a, r in zip(g.get_state(), (h, hu, z, z)):
         assert np.array_equal(a, r)
     g.destroy()
+
+
+@pytest.mark.parametrize("fields", [False, True])
+def test_rebalance_multi_bitwise(cs, fields):
+    """Re-partitioning during a run (csph_row_weights -> csph_balance_rows ->
+    csph_rebalance_rows): 3 strips start on an even split, are re-balanced on the
+    wet cells of the current state after 40 steps (state, psi field and NEXT-3 fields migrate;
+    time, tau and dt log carry over), and step on -- bitwise the single grid, dt log included.
+    With `fields`: n_M / beta / source fields, open edges, 16-row tiles."""
+    c = synth.config("C5", 200, 183)
+    f = synth.fill(c)
+    prm = dict(c.params)
+    kw = {}
+    fl = None
+    if fields:
+        rng = np.random.default_rng(4)
+        fl = dict(n_manning=0.02 + 0.02 * rng.random((c.ny, c.nx)),
+                  beta=np.full((c.ny, c.nx), 1e-4), src=np.where(rng.random((c.ny, c.nx)) < 0.01, 1e-3, 0.0))
+        prm.update(open_bc=5)
+        kw = dict(tile_rows=16)
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(prm, **kw))
+    g.set_state(*f)
+    if fl:
+        g.set_fields(**fl)
+    g.step(100)
+    dt0, ref = g.get_dt_log(100)[0], g.get_state()
+    g.destroy()
+    m = cs.csph_create_multi(c.nx, c.ny, c.dx, cs.params_from(prm, **kw), [0, 0, 0])
+    m.set_state(*f)
+    if fl:
+        m.set_fields(**fl)
+    m.step(40)
+    w = m.row_weights()
+    wet = (m.get_state()[0] > 1e-6).sum(axis=1) + 0.03 * c.nx
+    assert np.array_equal(w, wet)
+    bounds = cs.csph_balance_rows(c.ny, 3, w)
+    assert bounds != [0, 61, 122, 183]
+    m.rebalance_rows(bounds)
+    assert m.get_time()[1] == 40
+    m.step(60)
+    assert np.array_equal(m.get_dt_log(100)[0], dt0)
+    for a, r in zip(m.get_state(), ref):
+        assert np.array_equal(a, r)
+    # and back to an uneven split with a short last tile
+    m.rebalance_rows([0, 3, 100, 183])
+    m.destroy()
+
+
+def test_rebalance_dist_single_rank(cs):
+    """csph_rebalance_rows on a 1-rank NCCL handle (the DIST migration code path: a rank's rows
+    to itself), mid-run, graphs on: bitwise the uninterrupted run."""
+    c = synth.config("C3", 150, 130)
+    f = synth.fill(c)
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params))
+    g.set_state(*f)
+    g.step(50)
+    dt0, ref = g.get_dt_log(50)[0], g.get_state()
+    g.destroy()
+    d = cs.csph_create_dist_rows(c.nx, c.ny, c.dx, cs.params_from(c.params, tile_rows=32), 0, 1,
+                                 [0, c.ny], 0, cs.csph_make_nccl_id())
+    d.set_state(*f)
+    d.step(20)
+    d.rebalance_rows([0, c.ny])
+    d.step(30)
+    assert np.array_equal(d.get_dt_log(50)[0], dt0)
+    for a, r in zip(d.get_state(), ref):
+        assert np.array_equal(a, r)
+    with pytest.raises(cs.CsphError):
+        d.rebalance_rows([0, 2, c.ny])  # wrong rank count
+    d.destroy()

@@ -41,8 +41,8 @@ MUTATIONS = [
     ("K1 wet test >=", "o->w[c] = H[c] > eps;", "o->w[c] = H[c] >= eps;"),
     ("K1 v from Qx", "o->v[c] = Qy[c] * o->r[c];", "o->v[c] = Qx[c] * o->r[c];"),
     ("K2 force sign", "o->phix[c] = -(PE + PW);", "o->phix[c] = (PE + PW);"),
-    ("K2 west face swapped", "real PW = face_force(o->cP, o->eta[wv], b[wv], o->eta[c], b[c]);",
-     "real PW = face_force(o->cP, o->eta[c], b[c], o->eta[wv], b[wv]);"),
+    ("K2 west face swapped", "real PW = face_force(o->cPh, o->eta[wv], b[wv], o->eta[c], b[c]);",
+     "real PW = face_force(o->cPh, o->eta[c], b[c], o->eta[wv], b[wv]);"),
     ("face force b* = min", "real bs = sel_max(bL, bR);", "real bs = sel_min(bL, bR);"),
     ("face force mean factor", "return (cPh * (HsL + HsR)) * (HsR - HsL);",
      "return (cPh * (HsL + HsR + HsR)) * (HsR - HsL);"),
@@ -50,14 +50,14 @@ MUTATIONS = [
      "o->gam[c] = (o->cgam * sp) * o->r[c];"),
     ("icbrt 4 Newton steps", "for (int k = 0; k < 5; ++k) {", "for (int k = 0; k < 2; ++k) {"),
     # ---- K4 / K6
-    ("K4 theta = tau", "o->Hh[c] = H[c] * (RL(1) - theta * div);", "o->Hh[c] = H[c] * (RL(1) - tau * div);"),
+    ("K4 theta = tau", "o->Hh[c] = H[c] * FMA(-theta, div, RL(1));", "o->Hh[c] = H[c] * FMA(-tau, div, RL(1));"),
     ("K4 div sign v", "(o->v[c + sy] - o->v[c - sy])", "(o->v[c - sy] - o->v[c + sy])"),
-    ("K4 u~ uses Phi_half", "o->ut[c] = ((Qx[c] + theta * o->phix[c]) * f) * o->r[c];",
-     "o->ut[c] = ((Qx[c] + theta * o->phix2[c]) * f) * o->r[c];"),
-    ("K4 friction factor tau", "real f = RL(1) / (RL(1) + theta * o->gam[c]);",
-     "real f = RL(1) / (RL(1) + tau * o->gam[c]);"),
-    ("K6 uses Phi^n", "o->QLx[c] = (Qx[c] + tau * o->phix2[c]) * f;", "o->QLx[c] = (Qx[c] + tau * o->phix[c]) * f;"),
-    ("K6 theta", "o->QLy[c] = (Qy[c] + tau * o->phiy2[c]) * f;", "o->QLy[c] = (Qy[c] + theta * o->phiy2[c]) * f;"),
+    ("K4 u~ uses Phi_half", "o->ut[c] = (FMA(theta, o->phix[c], Qx[c]) * f) * o->r[c];",
+     "o->ut[c] = (FMA(theta, o->phix2[c], Qx[c]) * f) * o->r[c];"),
+    ("K4 friction factor tau", "real f = RL(1) / FMA(theta, o->gam[c], RL(1));",
+     "real f = RL(1) / FMA(tau, o->gam[c], RL(1));"),
+    ("K6 uses Phi^n", "o->QLx[c] = FMA(tau, o->phix2[c], Qx[c]) * f;", "o->QLx[c] = FMA(tau, o->phix[c], Qx[c]) * f;"),
+    ("K6 theta", "o->QLy[c] = FMA(tau, o->phiy2[c], Qy[c]) * f;", "o->QLy[c] = FMA(theta, o->phiy2[c], Qy[c]) * f;"),
     # ---- K7
     ("minmod picks max", "if (a > RL(0) && b > RL(0)) return sel_min(a, b);", "if (a > RL(0) && b > RL(0)) return sel_max(a, b);"),
     ("face state - sign", "qm[k] = FMA(RL(0.5), sL[k], q[k][L]);", "qm[k] = FMA(RL(-0.5), sL[k], q[k][L]);"),
@@ -69,12 +69,12 @@ MUTATIONS = [
      "out[k] = ((SR * FL[k] - SL * FR[k]) - SLSR * (UR[k] - UL[k])) * inv;"),
     ("hydrostatic b* = min", "real bs = sel_max(b_m, b_p);", "real bs = sel_min(b_m, b_p);"),
     ("donor reversed", "if (us > RL(0)) { Jn = J0n[L]; Ja = o->J0a[L]; }", "if (us < RL(0)) { Jn = J0n[L]; Ja = o->J0a[L]; }"),
-    ("slope term sign", "return J0n - (C_J * J0abs) * db_dn;", "return J0n + (C_J * J0abs) * db_dn;"),
+    ("slope term sign", "return FMA(-(C_J * J0abs), db_dn, J0n);", "return FMA((C_J * J0abs), db_dn, J0n);"),
     ("grass |J0| drops sqrt", "*jabs = c * a;", "*jabs = c;"),
     ("sediment gradient L/R", "(b[R] - b[L]) * o->inv_h", "(b[L] - b[R]) * o->inv_h"),
     # ---- K8 / Eq.7
-    ("K8 W dropped", "real bn = (b[c] - (lam * W[c]) * dJ) + (tau * W[c]) * src;",
-     "real bn = (b[c] - lam * dJ) + (tau * W[c]) * src;"),
+    ("K8 W dropped", "real bn = FMA(-(lam * W[c]), dJ, b[c]) + (tau * W[c]) * src;",
+     "real bn = FMA(-lam, dJ, b[c]) + (tau * W[c]) * src;"),
     ("K8 y-flux of Qx from normal", "real dQx = (o->FQx[e] - o->FQx[c]) + (o->GQx[n] - o->GQx[c]);",
      "real dQx = (o->FQx[e] - o->FQx[c]) + (o->GQy[n] - o->GQy[c]);"),
     ("K8 no dry zeroing", "if (!(Hn > eps)) { Qxn = RL(0); Qyn = RL(0); }", "if (!(Hn > RL(0))) { Qxn = RL(0); Qyn = RL(0); }"),
@@ -86,7 +86,7 @@ MUTATIONS = [
     # ---- NEXT-4 closures
     ("Grass odd m drops |v|", "if (m % 2) pw = pw * a;", "if (m % 2) pw = pw * RL(1);"),
     ("Eq.4 sqrt(gH) -> gH", "(((s_rel - RL(1)) * SQRT(g * H)) * d50)", "(((s_rel - RL(1)) * (g * H)) * d50)"),
-    ("Eq.4 A_J at H_half", "r_grass_m(cell_aj(o, c, H[c]),", "r_grass_m(cell_aj(o, c, o->Hh[c]),"),
+    ("Eq.4 A_J at H_half", "r_grass_mr(cell_aj(o, c, H[c]),", "r_grass_mr(cell_aj(o, c, o->Hh[c]),"),
     ("sources: absorption explicit", "real a = RL(1) / (RL(1) + tau * o->beta[c]);", "real a = RL(1) - tau * o->beta[c];"),
 ]
 
