@@ -6,7 +6,7 @@
 //  * Input rows (H, Qx, Qy, b [, W]) are staged into a D-slot shared-memory ring by 1D TMA
 //    bulk copies (cp.async.bulk ... mbarrier::complete_tx), PF rows ahead of use.
 //  * Every stage of R is computed once per cell: x-neighbour values are exchanged through
-//    shared memory (three barriers per row), y-neighbour values are carried in registers.
+//    shared memory (two barriers per row), y-neighbour values are carried in registers.
 //    The update of row L-3 is produced when row L is loaded (stencil radius 3).
 //  * Epilogue: stores of (H, Qx, Qy, b) for row L-3, wall-mirror ghosts, the next step's
 //    Eq.7 maxima (warp shuffle + block max + one atomicMax per CTA) and the negative-depth flag.
@@ -32,6 +32,12 @@ constexpr int kUnroll = CSPH_UNROLL;  // y-march unroll of the fp64 hot speciali
 #endif
 constexpr int kMinB32 = CSPH_MINB32;  // resident CTAs per SM of the fp32 instance
 
+#ifndef CSPH_YFAST
+#define CSPH_YFAST true
+#endif
+#ifndef CSPH_XFAST
+#define CSPH_XFAST true
+#endif
 #ifndef CSPH_GUARD
 #define CSPH_GUARD 0
 #endif
@@ -110,7 +116,7 @@ enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
 #ifndef CSPH_HLL_FAST
 #define CSPH_HLL_FAST 1
 #endif
-template <typename T>
+template <bool FASTP = true, typename T>
 __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T eta_p, T H_p,
                                        T un_p, T ut_p, bool off, T& F0, T& F1, T& F2) {
   const T bs = smax_t(eta_m - H_m, eta_p - H_p);
@@ -126,7 +132,7 @@ __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T et
   const bool both = (wm & wp) != 0u;
   const T fl1 = mm * un_m, fl2 = mm * ut_m, fr1 = mp * un_p, fr2 = mp * ut_p;
   const T d0 = Hp - Hm, d1 = mp - mm, d2 = Hp * ut_p - Hm * ut_m;
-  if (CSPH_HLL_FAST && __all_sync(0xffffffffu, both & !off)) {
+  if (CSPH_HLL_FAST && FASTP && __all_sync(0xffffffffu, both & !off)) {
     // warp-uniform common case (both reconstructed sides wet, a face of a wet cell): R's
     // both-wet speeds without the dry-side selects; then, unless some lane is supercritical,
     // the HLL average without the upwind selects.  Same operations, same values.
@@ -326,7 +332,7 @@ __global__ void __launch_bounds__(NT, MINB)
   T vm1 = 0;                 // v(L-1)
   T gam1 = 0, gam2 = 0;      // gamma(L-1), gamma(L-2)
   T PS = 0;                  // K2 y-face force (L-1|L)
-  T Hh1 = 0, ut1 = 0, vt1 = 0, J0x1 = 0, J0y1 = 0, J0a1 = 0;  // K4 outputs of row L-1
+  T J0y1 = 0;                // K4 output of row L-1 (the others are read from sm.X2)
   T Hh2 = 0;                 // H_half(L-2)
   T PhS = 0;                 // K5 y-face force (L-3|L-2)
   T phx2h = 0;               // Phi_half_x(L-2)
@@ -342,6 +348,7 @@ __global__ void __launch_bounds__(NT, MINB)
   unsigned long long m0 = 0, m1 = 0, m2 = 0;
   bool neg = false;
   unsigned hist = 0;  // wet flags of rows L..L-4 of this column (bit 0 = row L)
+  unsigned wmask = 0;  // HGS band mask of this thread's output cells (see store_update)
 
   const bool col_out = (t >= 4) && (t < 4 + TX) && (col < nx);
   const bool colg = feeds_xghost(S, col);
@@ -350,7 +357,6 @@ __global__ void __launch_bounds__(NT, MINB)
   // wall ghosts and the next step's Eq.7 terms.
   // HGS band mask of this thread's output cells (wet anywhere / in the first or last row
   // of the tile); the first / last column add HGS_LEFT / HGS_RIGHT at the end
-  unsigned wmask = 0;
   auto store_update = [&](T Hn, T Qxn, T Qyn, T bn, T W3, int j) {
     const bool wet = Hn > Q.eps;
     wmask |= wet ? (HGS_ANY | (j == y0 ? HGS_TOP : 0u) | (j == y1 - 1 ? HGS_BOT : 0u)) : 0u;
@@ -444,15 +450,15 @@ __global__ void __launch_bounds__(NT, MINB)
       // identity, so only the carried window and the row L-3 update run.
       const T H0 = RG(F_H, k, 0);
       gam2 = gam1; gam1 = T(0);
-      Hh2 = Hh1;
+      Hh2 = X2(0, 0);  // row L-1's K4 outputs (exchange row; the previous iteration wrote it)
       phx2h = T(0);
-      ut3 = ut2; vt3 = vt2; ut2 = ut1; vt2 = vt1;
-      J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = J0a1;
+      ut3 = ut2; vt3 = vt2; ut2 = X2(1, 0); vt2 = X2(2, 0);
+      J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = X2(4, 0);
       // K4 of the dry row L: H_half = H, u~ = v~ = 0, J0 = 0.  Only H_half goes to the
       // exchange row: this parity's u~, v~, J0 slots hold row L-2's values, which are +0
       // already (rows L-4..L are dry), and a neighbour may still be reading them in the
       // previous iteration's phase D (no barrier in between; racecheck)
-      Hh1 = H0; ut1 = T(0); vt1 = T(0); J0x1 = T(0); J0y1 = T(0); J0a1 = T(0);
+      J0y1 = T(0);
       vm1 = T(0);
       X2w[0 * SM::XW + t + 1] = H0;
 #pragma unroll
@@ -484,9 +490,12 @@ __global__ void __launch_bounds__(NT, MINB)
     const T eta1 = H1 + b1;
     __syncthreads();  // ---------------------------------------------------- barrier 1
     {
+      // row L-1's K4 outputs: the exchange row written in the previous phase D
+      const T Hh1 = X2(0, 0), ut1 = X2(1, 0), vt1 = X2(2, 0), J0a1 = X2(4, 0);
       // ====== phase C: Phi_x (row L), Delta F_x (row L-2), K5 + sigma_x (row L-1),
-      //        K6 (row L-2), y-face (L-3|L-2) ======
+      //        K6 (row L-2), y-face (L-3|L-2), K8 (row L-3) ======
       const T phix0 = aw0 ? -(aPE0 + XG(sm.PE, -1)) : T(0);
+
       // Delta F_x of row L-2 from the own face (t|t+1) and the west face (t-1|t)
       T dF2[4];
 #pragma unroll
@@ -529,7 +538,7 @@ __global__ void __launch_bounds__(NT, MINB)
       sy2[3] = minmod_t(ut2 - ut3, ut1 - ut2);
       if (ANYW(w3 || w2)) {
         const bool any = w3 || w2;
-        hll_bf(Q.g, fma(T(0.5), sy3[0], eta3), fma(T(0.5), sy3[1], H3), fma(T(0.5), sy3[2], vt3),
+        hll_bf<CSPH_YFAST>(Q.g, fma(T(0.5), sy3[0], eta3), fma(T(0.5), sy3[1], H3), fma(T(0.5), sy3[2], vt3),
                  fma(T(0.5), sy3[3], ut3), fma(T(-0.5), sy2[0], eta2), fma(T(-0.5), sy2[1], H2),
                  fma(T(-0.5), sy2[2], vt2), fma(T(-0.5), sy2[3], ut2), !any,
                  Gn[0], Gn[2], Gn[1]);  // normal momentum of a y-face -> Qy, tangential -> Qx
@@ -540,24 +549,47 @@ __global__ void __launch_bounds__(NT, MINB)
       J0y3 = J0y2; J0a3 = J0a2; J0y2 = J0y1; J0a2 = J0a1;
 #pragma unroll
       for (int q = 0; q < 4; ++q) sy3[q] = sy2[q];
+      // ---- K8 update of row L-3 (its last input, the y-face (L-3|L-2), is ready) ----
+      if (col_out && j >= y0 && j < y1) {
+        const T W3 = HASW ? RG(F_W, km3, 0) : T(S.Wc);
+        const T dH = dF3[0] + (Gn[0] - Gs[0]);
+        const T dQx = dF3[1] + (Gn[1] - Gs[1]);
+        const T dQy = dF3[2] + (Gn[2] - Gs[2]);
+        const T dJ = dF3[3] + (Gn[3] - Gs[3]);
+        T Hn = fma(-lam, dH, H3);
+        T Qxn = fma(-lam, dQx, QLx3);
+        T Qyn = fma(-lam, dQy, QLy3);
+        const T bn = fma(-(lam * W3), dJ, b3) + (tau * W3) * Q.src;
+        if constexpr (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
+        store_update(Hn, Qxn, Qyn, bn, W3, j);
+      }
+      QLx3 = QLx2; QLy3 = QLy2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { dF3[q] = dF2[q]; Gs[q] = Gn[q]; }
       XG(sm.X3[0], 0) = PhE1;
 #pragma unroll
       for (int q = 0; q < 4; ++q) XG(sm.X3[1 + q], 0) = sx1[q];
       next_hist();
       const bool dry_next = __syncthreads_and(hist == 0u);  // ---------------- barrier 2
       // ====== phase D: Phi_half_x + x-face flux (row L-1), phase A (row L+1), K4 + J0
-      //        (row L), K8 (row L-3) ======
-      phx2h = w1 ? -(PhE1 + XG(sm.X3[0], -1)) : T(0);
+      //        (row L) ======
+      phx2h = w1 ? -(XG(sm.X3[0], 0) + XG(sm.X3[0], -1)) : T(0);
       T Fn[4] = {T(0), T(0), T(0), T(0)};
       {
+        // own-side values of row L-1 re-read (exchange rows, ring) instead of carried
+        const T H1 = RG(F_H, km1, 0), b1 = RG(F_B, km1, 0);
+        const T eta1 = H1 + b1;
+        const T ut1 = X2(1, 0), vt1 = X2(2, 0), J0x1 = X2(3, 0), J0a1 = X2(4, 0);
         const T HR = RG(F_H, km1, 1);
         const bool any = (gt_u(H1, Q.eps) | gt_u(HR, Q.eps)) != 0u;
         if (ANYW(any)) {
           const T bR = RG(F_B, km1, 1);
           const T eR = HR + bR;
           const T uR = X2(1, 1), vR = X2(2, 1);
-          hll_bf(Q.g, fma(T(0.5), sx1[0], eta1), fma(T(0.5), sx1[1], H1), fma(T(0.5), sx1[2], ut1),
-                   fma(T(0.5), sx1[3], vt1), fma(T(-0.5), XG(sm.X3[1], 1), eR), fma(T(-0.5), XG(sm.X3[2], 1), HR),
+          // own slopes sigma_x of row L-1: the exchange row written in phase C
+          hll_bf<CSPH_XFAST>(Q.g, fma(T(0.5), XG(sm.X3[1], 0), eta1), fma(T(0.5), XG(sm.X3[2], 0), H1),
+                   fma(T(0.5), XG(sm.X3[3], 0), ut1), fma(T(0.5), XG(sm.X3[4], 0), vt1),
+                   fma(T(-0.5), XG(sm.X3[1], 1), eR), fma(T(-0.5), XG(sm.X3[2], 1), HR),
                    fma(T(-0.5), XG(sm.X3[3], 1), uR), fma(T(-0.5), XG(sm.X3[4], 1), vR), !any,
                    Fn[0], Fn[1], Fn[2]);  // normal momentum of an x-face -> Qx, tangential -> Qy
           Fn[3] = (any && TRANSP) ? sed_face_t(Q, ut1, uR, J0x1, X2(3, 1), J0a1, X2(4, 1), b1, bR)
@@ -592,27 +624,10 @@ __global__ void __launch_bounds__(NT, MINB)
         X2w[2 * SM::XW + t + 1] = vt;
         X2w[3 * SM::XW + t + 1] = jx;
         X2w[4 * SM::XW + t + 1] = ja;
-        Hh1 = Hh; ut1 = ut; vt1 = vt; J0x1 = jx; J0y1 = jy; J0a1 = ja;
+        J0y1 = jy;
         vm1 = v0;
         gam2 = gam1; gam1 = gam0;
       }
-      // ---- K8 update of row L-3 ----
-      if (col_out && j >= y0 && j < y1) {
-        const T W3 = HASW ? RG(F_W, km3, 0) : T(S.Wc);
-        const T dH = dF3[0] + (Gn[0] - Gs[0]);
-        const T dQx = dF3[1] + (Gn[1] - Gs[1]);
-        const T dQy = dF3[2] + (Gn[2] - Gs[2]);
-        const T dJ = dF3[3] + (Gn[3] - Gs[3]);
-        T Hn = fma(-lam, dH, H3);
-        T Qxn = fma(-lam, dQx, QLx3);
-        T Qyn = fma(-lam, dQy, QLy3);
-        const T bn = fma(-(lam * W3), dJ, b3) + (tau * W3) * Q.src;
-        if constexpr (GEN) apply_sources(S, tau, off(pitch, col, j), Hn, Qxn, Qyn);
-        store_update(Hn, Qxn, Qyn, bn, W3, j);
-      }
-      QLx3 = QLx2; QLy3 = QLy2;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) { dF3[q] = dF2[q]; Gs[q] = Gn[q]; }
       cta_dry = dry_next;
     }
 #undef X2
