@@ -130,7 +130,7 @@ int         csph_set_fields_rows(csph_t*, int j_begin, int j_end, const double* 
  * on the device.  No host synchronisation inside the call except one status
  * readback at its end.  A single-grid handle replays pairs of steps from CUDA
  * graphs (captured on first use, rebuilt after set_state / set_fields;
- * environment CSPH_NO_GRAPHS=1 disables them).  On CSPH_ENEGDEPTH/ENONFINITE/EDRY the steps up to the
+ * params.graphs = 0 disables them).  On CSPH_ENEGDEPTH/ENONFINITE/EDRY the steps up to the
  * failing one are done (see csph_get_time) and later calls return the same code. */
 int         csph_step(csph_t*, int nsteps);
 

@@ -120,6 +120,8 @@ struct Strip {
   int nsm = 148;
   unsigned char* tstate = nullptr;   // HGS identity-copy counters [ntiles]
   unsigned long long* hstats = nullptr;  // HGS tile counters: marched, copied, skipped
+  unsigned short* tcost = nullptr;   // per tile: full-cost rows of its last march [ntiles]
+  int* torder = nullptr;             // launch order of the tiles [ntiles]
   int ntx = 0, nty = 0;
   double* Wbuf = nullptr;            // device psi -> W field (when psi varies)
   float* Wbuf32 = nullptr;           // fp32 mode W field
@@ -610,6 +612,9 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
     }
     if ((st = dalloc(s, (void**)&s.hstats, 4 * sizeof(unsigned long long)))) return st;
     CK(cudaMemset(s.hstats, 0, 4 * sizeof(unsigned long long)));
+    if ((st = dalloc(s, (void**)&s.tcost, nt * sizeof(unsigned short)))) return st;
+    CK(cudaMemset(s.tcost, 0, nt * sizeof(unsigned short)));
+    if ((st = dalloc(s, (void**)&s.torder, nt * sizeof(int)))) return st;
   }
   CK(cudaMemset(s.gM, 0, 4 * sizeof(unsigned long long)));
   CK(cudaMemset(s.Mlast, 0, 4 * sizeof(double)));
@@ -1390,6 +1395,7 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
     CK(cudaMemsetAsync(s.tstate, 0, s.tflag_cap, s.st));
     CK(cudaMemsetAsync(s.gflag, HGS_ALL, 4 * (size_t)s.ntx, s.st));
     CK(cudaMemsetAsync(s.hstats, 0, 4 * sizeof(unsigned long long), s.st));
+    CK(cudaMemsetAsync(s.tcost, 0, s.tflag_cap * sizeof(unsigned short), s.st));
     // walls: ghosts of buffer 0 (W is read only on owned cells: no ghosts needed)
     launch_mirror(s.v, s.ctrl, 0, s.st, &H->launches);
     CK(cudaGetLastError());
@@ -1532,6 +1538,8 @@ static Hgs hgs_of(const csph* H, const Strip& s) {
   h.nty = s.nty;
   h.enable = H->p.hgs != 0 && H->p.path == CSPH_PATH_FUSED;
   h.stats = s.hstats;
+  h.order = nullptr;
+  h.cost = s.tcost;
   return h;
 }
 
@@ -1542,8 +1550,12 @@ static int single_step(csph* H, Strip& s) {
     launch_staged_step(s.v, s.ctrl, s.scr, H->P, s.gM, s.st, &H->launches);
     launch_mirror(s.v, s.ctrl, 1, s.st, &H->launches);
   } else {
-    launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, s.ty, hgs_of(H, s), s.st,
-                      &H->launches);
+    Hgs hg = hgs_of(H, s);
+    if (hg.enable) {  // costliest tiles first (last step's costs)
+      launch_order_tiles(s.tcost, s.ntx, 0, s.nty, s.torder, s.st, &H->launches);
+      hg.order = s.torder;
+    }
+    launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, s.ty, hg, s.st, &H->launches);
   }
   CK(cudaGetLastError());
   ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 1);
@@ -1657,9 +1669,15 @@ static int split_step(csph* H, int n, int q) {
   for (int r = 0; r < ns; ++r) {  // 3. interior tile rows
     Strip& s = H->s[r];
     CK(cudaSetDevice(s.dev));
-    if (sp[r])
-      launch_fused_step(s.v, s.ctrl, H->P, s.gM, lo[r], hi[r], s.ty, hgs_of(H, s), s.st,
-                        &H->launches);
+    if (sp[r]) {
+      Hgs hg = hgs_of(H, s);
+      if (hg.enable) {  // the interior tile rows, costliest first
+        launch_order_tiles(s.tcost, s.ntx, lo[r] / s.ty, hi[r] / s.ty, s.torder, s.st,
+                           &H->launches);
+        hg.order = s.torder;
+      }
+      launch_fused_step(s.v, s.ctrl, H->P, s.gM, lo[r], hi[r], s.ty, hg, s.st, &H->launches);
+    }
     if (H->profiling && r == 0) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
     CK(cudaGetLastError());
     CK(cudaEventRecord(s.ev_int, s.st));
@@ -1744,12 +1762,17 @@ int csph_step(csph_t* H, int nsteps) {
     for (size_t si = 0; si < H->s.size(); ++si) {
       Strip& s = H->s[si];
       CK(cudaSetDevice(s.dev));
+      Hgs hg = hgs_of(H, s);
+      if (H->p.path != CSPH_PATH_STAGED && hg.enable) {  // costliest tiles first
+        launch_order_tiles(s.tcost, s.ntx, 0, s.nty, s.torder, s.st, &H->launches);
+        hg.order = s.torder;
+      }
       if (H->profiling && si == 0) CK(cudaEventRecord(H->evs[2 * n], s.st));
       if (H->p.path == CSPH_PATH_STAGED)
         launch_staged_step(s.v, s.ctrl, s.scr, H->P, s.gM, s.st, &H->launches);
       else
-        launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, s.ty, hgs_of(H, s),
-                          s.st, &H->launches);  // writes the wall ghosts in its epilogue
+        launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, s.ty, hg, s.st,
+                          &H->launches);  // writes the wall ghosts in its epilogue
       if (H->profiling && si == 0) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
       if (H->p.path == CSPH_PATH_STAGED) launch_mirror(s.v, s.ctrl, 1, s.st, &H->launches);
       CK(cudaGetLastError());

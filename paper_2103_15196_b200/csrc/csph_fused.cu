@@ -205,9 +205,13 @@ __global__ void __launch_bounds__(NT, MINB)
 
   const int t = threadIdx.x;
   const int nx = S.nx, pitch = S.pitch;
-  const int x0 = blockIdx.x * TX;
+  // the tile of this CTA: the launch's order list (costliest first), else natural order
+  const int gx = (S.nx + TX - 1) / TX;
+  const int lin = hg.order ? hg.order[blockIdx.x] : (int)blockIdx.x;
+  const int bx = lin % gx, by = lin / gx;
+  const int x0 = bx * TX;
   const int col = x0 - 4 + t;
-  const int y0 = row0 + blockIdx.y * TY;
+  const int y0 = row0 + by * TY;
   const int y1 = min(y0 + TY, row1);
   if (y0 >= y1) return;
   // ---- HGS.  Under R a dry cell whose 4
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(NT, MINB)
     return off(pitch, min(c, nx + GX - 1), min(r, S.ny + GY - 1));
   };
   const int tr = y0 / TY;
-  const int ti = tr * hg.ntx + (int)blockIdx.x;
+  const int ti = tr * hg.ntx + bx;
   // across an interior strip edge the facing tile row is the neighbouring strip's, whose
   // flags arrive with the halo rows (hg.glo / hg.ghi); without them such a tile marches
   if (hg.enable && (S.wall_lo || y0 > 0 || hg.glo) && (S.wall_hi || y1 < S.ny || hg.ghi)) {
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(NT, MINB)
       if (r >= hg.nty) return hg.ghi ? hg.ghi[q] : 0u;
       return hg.fprev[r * hg.ntx + q];
     };
-    const int q0 = (int)blockIdx.x;
+    const int q0 = bx;
     const bool dry = !(fl(tr, q0) & HGS_ANY) && !(fl(tr - 1, q0) & HGS_BOT) &&
                      !(fl(tr + 1, q0) & HGS_TOP) && !(fl(tr, q0 - 1) & HGS_RIGHT) &&
                      !(fl(tr, q0 + 1) & HGS_LEFT);
@@ -262,6 +266,7 @@ __global__ void __launch_bounds__(NT, MINB)
         }
         const bool any = __syncthreads_or(cwet);
         if (t == 0) {
+          if (hg.cost) hg.cost[ti] = 0;
           hg.tstate[ti] = any ? 0 : (unsigned char)(stt + 1);
           hg.fnext[ti] = any ? HGS_ALL : 0;  // conservative: every band
           atomicAdd(&hg.stats[1], 1ull);
@@ -286,6 +291,7 @@ __global__ void __launch_bounds__(NT, MINB)
       if (t == 0) {
         atomicAdd(&hg.stats[2], 1ull);
         hg.fnext[ti] = 0;
+        if (hg.cost) hg.cost[ti] = 0;
       }
       return;  // both buffers already hold the identity (tstate >= 2, no source)
     }
@@ -422,6 +428,7 @@ __global__ void __launch_bounds__(NT, MINB)
   hist = RG(F_H, 0, 0) > Q.eps ? 1u : 0u;
   bool cta_dry = __syncthreads_and(hist == 0u);
   if (!cta_dry) phaseA(0);
+  int nfull = 0;  // iterations at full cost (this tile's cost for the next step's order)
 
   constexpr int kUR = (!GEN && sizeof(T) == 8) ? kUnroll : 1;
 #pragma unroll kUR
@@ -485,6 +492,7 @@ __global__ void __launch_bounds__(NT, MINB)
       if (!cta_dry && k + 1 < niter) phaseA(k + 1);
       continue;
     }
+    ++nfull;
     const T H1 = RG(F_H, km1, 0), b1 = RG(F_B, km1, 0);
     const bool w1 = H1 > Q.eps;
     const T eta1 = H1 + b1;
@@ -662,6 +670,7 @@ __global__ void __launch_bounds__(NT, MINB)
     hg.fnext[ti] = (unsigned char)m;
     hg.tstate[ti] = 0;
   }
+  if (t == 0 && hg.cost) hg.cost[ti] = (unsigned short)min(nfull, 65535);
   if (t == 0 && hg.stats) atomicAdd(&hg.stats[0], 1ull);
   if (t < 3) {
     unsigned long long m = 0;
@@ -687,7 +696,8 @@ void launch_t(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
       configured |= 1ull << (dev & 63);
   }
-  dim3 grid((unsigned)((S.nx + TX - 1) / TX), (unsigned)((row1 - row0 + TY - 1) / TY));
+  // one-dimensional: CTA i marches tile hg.order[i] (or i), tile (bx, by) = (i % gx, i / gx)
+  dim3 grid((unsigned)((S.nx + TX - 1) / TX) * (unsigned)((row1 - row0 + TY - 1) / TY));
   fused_step_kernel<T, NT, HASW, D, PF, MINB, GEN>
       <<<grid, NT, smem, st>>>(S, C, P, gM, row0, row1, TY, hg);
 }
@@ -717,7 +727,90 @@ void launch_v(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM
   }
 }
 
+// Counting sort of a launch's tiles by descending cost: one CTA.  Each
+// thread loads its keys for a chunk of kOrdChunk tiles at once (one memory latency per
+// chunk, not one per key) and keeps them for the scatter; the shared-memory atomics are
+// warp-aggregated (most tiles share the key of cost 0).
+constexpr int kOrdBuckets = 256;
+constexpr int kOrdThreads = 1024;
+constexpr int kOrdPer = 24;  // keys per thread per chunk
+constexpr int kOrdChunk = kOrdThreads * kOrdPer;
+__global__ void __launch_bounds__(kOrdThreads, 1) order_tiles_kernel(
+    const unsigned short* __restrict__ cost, int ntx, int tr0, int tr1, int* __restrict__ order) {
+  __shared__ int cnt[kOrdBuckets];
+  __shared__ int wsum[kOrdBuckets / 32];
+  const int n = ntx * (tr1 - tr0);
+  const int t = threadIdx.x, lane = t & 31;
+  const unsigned short* c = cost + (size_t)tr0 * ntx;
+  auto key_of = [&](int i) { return kOrdBuckets - 1 - min((int)__ldg(c + i), kOrdBuckets - 1); };
+  // warp-aggregated atomicAdd of 1 per lane on cnt[key]; returns this lane's old value
+  auto agg_add = [&](unsigned act, int key) {
+    // a warp whose keys are all equal (common: runs of dry tiles) skips the match
+    const unsigned m = __all_sync(act, key == __shfl_sync(act, key, __ffs(act) - 1))
+                           ? act : __match_any_sync(act, key);
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&cnt[key], __popc(m));
+    return __shfl_sync(m, base, leader) + __popc(m & ((1u << lane) - 1u));
+  };
+  for (int b = t; b < kOrdBuckets; b += kOrdThreads) cnt[b] = 0;
+  __syncthreads();
+  int key[kOrdPer];
+  for (int c0 = 0; c0 < n; c0 += kOrdChunk) {  // pass 1: histogram (bucket 0 = costliest)
+#pragma unroll
+    for (int q = 0; q < kOrdPer; ++q) {
+      const int i = c0 + q * kOrdThreads + t;
+      key[q] = i < n ? key_of(i) : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < kOrdPer; ++q) {
+      const unsigned act = __ballot_sync(0xffffffffu, key[q] >= 0);
+      if (key[q] >= 0) agg_add(act, key[q]);
+    }
+  }
+  __syncthreads();
+  int x = 0, incl = 0;  // exclusive scan of the 256 counts: 8 warps, then the warp totals
+  if (t < kOrdBuckets) {
+    x = cnt[t];
+    incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[t >> 5] = incl;
+  }
+  __syncthreads();
+  if (t < kOrdBuckets) {
+    int base = 0;
+    for (int w = 0; w < (t >> 5); ++w) base += wsum[w];
+    cnt[t] = base + incl - x;
+  }
+  __syncthreads();
+  for (int c0 = 0; c0 < n; c0 += kOrdChunk) {  // pass 2: scatter (keys still held when n fits)
+    if (n > kOrdChunk) {
+#pragma unroll
+      for (int q = 0; q < kOrdPer; ++q) {
+        const int i = c0 + q * kOrdThreads + t;
+        key[q] = i < n ? key_of(i) : -1;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kOrdPer; ++q) {
+      const unsigned act = __ballot_sync(0xffffffffu, key[q] >= 0);
+      if (key[q] >= 0) order[agg_add(act, key[q])] = c0 + q * kOrdThreads + t;
+    }
+  }
+}
+
 }  // namespace
+
+void launch_order_tiles(const unsigned short* cost, int ntx, int tr0, int tr1, int* order,
+                        cudaStream_t st, long long* nlaunch) {
+  if (tr1 <= tr0) return;
+  order_tiles_kernel<<<1, kOrdThreads, 0, st>>>(cost, ntx, tr0, tr1, order);
+  *nlaunch += 1;
+}
 
 void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM,
                        int row0, int row1, int tile_rows, const Hgs& hg, cudaStream_t st,

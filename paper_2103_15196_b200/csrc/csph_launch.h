@@ -35,6 +35,12 @@ struct Hgs {
   int ntx, nty;
   int enable;
   unsigned long long* stats;  // [0] tiles marched, [1] copied (identity), [2] skipped
+  // Launch order: CTA i of the launch takes tile order[i] (linear index
+  // within the launch's tile rows; nullptr = natural order), costliest first.  cost[ti]:
+  // the rows the tile's last march computed at full cost (0 for identity / skipped tiles),
+  // written by the step kernel and read by the next step's order_tiles.
+  const int* order;
+  unsigned short* cost;
 };
 
 constexpr int FUSED_TX = 120;  // output columns per CTA of the fused kernel (NT - 8)
@@ -44,6 +50,11 @@ constexpr int FUSED_TX = 120;  // output columns per CTA of the fused kernel (NT
 void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long long* gM,
                        int row0, int row1, int tile_rows, const Hgs& hgs, cudaStream_t st,
                        long long* nlaunch);
+
+// Order the tiles of tile rows [tr0, tr1) by descending cost into order[0, ntx (tr1 - tr0))
+// (one CTA, a counting sort; ties in any order: the step's results do not depend on it).
+void launch_order_tiles(const unsigned short* cost, int ntx, int tr0, int tr1, int* order,
+                        cudaStream_t st, long long* nlaunch);
 
 // Service kernels (csph_api.cu).
 void launch_mirror(const StripView& S, const Ctrl* C, int next_parity_from_ctrl,

@@ -189,6 +189,31 @@ def test_hgs_tile_skipping_is_exact(cs, name, n, ny, steps):
         assert np.array_equal(a, b)
 
 
+def test_tile_launch_order_is_exact(cs):
+    """The launch order: tiles run costliest first, by the previous step's
+    costs, through the one-CTA counting sort -- here with more tiles than one sort chunk
+    (137 x 183 tiles of 16 rows > 24576), a single grid and 3 strips: bitwise the same
+    state and dt log as HGS off (natural order, every tile marched)."""
+    c = synth.config("C5", 16384, 2920)
+    f = synth.fill(c)
+    steps = 6
+    res = []
+    for hgs, ns in ((0, 1), (1, 1), (1, 3)):
+        p = cs.params_from(c.params, hgs=hgs, tile_rows=16)
+        if ns == 1:
+            g = cs.csph_create(c.nx, c.ny, c.dx, p)
+        else:
+            g = cs.csph_create_multi(c.nx, c.ny, c.dx, p, [0] * ns)
+        g.set_state(*f)
+        g.step(steps)
+        res.append((g.get_dt_log(steps)[0], g.get_state()))
+        g.destroy()
+    for r in res[1:]:
+        assert np.array_equal(res[0][0], r[0])
+        for a, b in zip(res[0][1], r[1]):
+            assert np.array_equal(a, b)
+
+
 def test_hgs_with_bed_source_term(cs):
     """q+ - q- != 0 changes b in dry cells too: HGS must keep copying (never skip)."""
     c = synth.config("C5", 400, 380)
@@ -233,10 +258,10 @@ def test_hgs_band_rule_narrow_tiles(cs, strips):
         assert res[0][2][2] > 0  # tiles were actually skipped
 
 
-def test_cuda_graph_replay_is_exact(cs, monkeypatch):
+def test_cuda_graph_replay_is_exact(cs):
     """csph_step replays step pairs from CUDA graphs (one per starting buffer parity).
     Odd and even step counts, a re-upload of the state between calls (graph rebuild) and
-    both paths: bitwise equal to plain launches (CSPH_NO_GRAPHS=1) and to the oracle."""
+    both paths: bitwise equal to plain launches (params.graphs = 0) and to the oracle."""
     c = synth.config("C5", 300, 260)
     f = synth.fill(c)
     f2 = synth.fill(synth.config("C3", 300, 260))
@@ -244,11 +269,8 @@ def test_cuda_graph_replay_is_exact(cs, monkeypatch):
     for path in (0, 1):
         res = []
         for nog, default_stream in ((False, False), (True, False), (False, True)):
-            if nog:
-                monkeypatch.setenv("CSPH_NO_GRAPHS", "1")
-            else:
-                monkeypatch.delenv("CSPH_NO_GRAPHS", raising=False)
-            g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, path=path))
+            g = cs.csph_create(c.nx, c.ny, c.dx,
+                               cs.params_from(c.params, path=path, graphs=0 if nog else 1))
             if default_stream:  # what bench.py does: torch's (legacy default) stream
                 g.set_stream(0)
             g.set_state(*f)

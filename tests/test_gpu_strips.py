@@ -120,14 +120,15 @@ def test_dist_split_launches(cs, tile_rows):
     assert np.array_equal(g.get_dt_log(40)[0], dt0)
     for a, r in zip(g.get_state(), ref):
         assert np.array_equal(a, r)
-    # per step: ctrl + the edge tile rows, the interior (when there is one); the last
-    # launch must hold >= 3 rows (a short last tile is merged with the one before it)
+    # per step: ctrl + the edge tile rows, the interior and its tile-order sort (when there
+    # is one); the last launch must hold >= 3 rows (a short last tile is merged with the
+    # one before it)
     nty = -(-c.ny // tile_rows)
     hi = (nty - 1) * tile_rows
     if c.ny - hi < 3:
         hi -= tile_rows
     split = nty >= 3 and hi > tile_rows
-    assert g.last_launch_count() == 40 * (1 + (3 if split else 1))
+    assert g.last_launch_count() == 40 * (1 + (4 if split else 1))
     g.destroy()
 
 

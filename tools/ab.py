@@ -27,7 +27,12 @@ wet = (1.0 + 0.2 * np.sin(X) * np.cos(Y), 0.8 * np.ones((m, m)), 0.3 * np.ones((
        0.05 * np.cos(X + Y), np.full((m, m), 0.4))
 c = synth.config("C5", n)
 out = []
-for name, nn, f, p in [("C5", n, synth.fill(c), c.params), ("wet", m, wet, phys)]:
+cases = [("C5", n, lambda: synth.fill(c), c.params), ("wet", m, lambda: wet, phys)]
+if os.environ.get("C34"):
+    c3, c4 = synth.config("C3"), synth.config("C4")
+    cases += [("C3", 4096, lambda: synth.fill(c3), c3.params), ("C4", 8192, lambda: synth.fill(c4), c4.params)]
+for name, nn, ff, p in cases:
+    f = ff()
     g = csph.csph_create(nn, nn, 1.0, csph.params_from(p))
     g.set_state(*f)
     del f
