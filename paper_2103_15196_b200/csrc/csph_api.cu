@@ -120,8 +120,15 @@ struct Strip {
   int nsm = 148;
   unsigned char* tstate = nullptr;   // HGS identity-copy counters [ntiles]
   unsigned long long* hstats = nullptr;  // HGS tile counters: marched, copied, skipped
-  unsigned short* tcost = nullptr;   // per tile: full-cost rows of its last march [ntiles]
-  int* torder = nullptr;             // launch order of the tiles [ntiles]
+  // launch order, by the state parity a step reads: tcost[p] per tile, the
+  // full-cost rows of the step that read buffer p; torder[p] the order of the step reading
+  // p, sorted on the order stream `ost` from tcost[p] of two steps before while the step
+  // in between runs (ev_ofork / ev_ojoin; osort_pending: a sort not yet joined by st)
+  unsigned short* tcost = nullptr;   // [2][tflag_cap]
+  int* torder = nullptr;             // [2][tflag_cap]
+  cudaStream_t ost = nullptr;
+  cudaEvent_t ev_ofork = nullptr, ev_ojoin = nullptr;
+  bool osort_pending = false;
   int ntx = 0, nty = 0;
   double* Wbuf = nullptr;            // device psi -> W field (when psi varies)
   float* Wbuf32 = nullptr;           // fp32 mode W field
@@ -612,9 +619,8 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
     }
     if ((st = dalloc(s, (void**)&s.hstats, 4 * sizeof(unsigned long long)))) return st;
     CK(cudaMemset(s.hstats, 0, 4 * sizeof(unsigned long long)));
-    if ((st = dalloc(s, (void**)&s.tcost, nt * sizeof(unsigned short)))) return st;
-    CK(cudaMemset(s.tcost, 0, nt * sizeof(unsigned short)));
-    if ((st = dalloc(s, (void**)&s.torder, nt * sizeof(int)))) return st;
+    if ((st = dalloc(s, (void**)&s.tcost, 2 * nt * sizeof(unsigned short)))) return st;
+    if ((st = dalloc(s, (void**)&s.torder, 2 * nt * sizeof(int)))) return st;
   }
   CK(cudaMemset(s.gM, 0, 4 * sizeof(unsigned long long)));
   CK(cudaMemset(s.Mlast, 0, 4 * sizeof(double)));
@@ -638,6 +644,9 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
   CK(cudaEventCreateWithFlags(&s.ev_edge, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&s.ev_int, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&s.ev_comm, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&s.ost, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&s.ev_ofork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&s.ev_ojoin, cudaEventDisableTiming));
   init_ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s.st));
@@ -646,6 +655,7 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
 
 static void strip_free(Strip& s) {
   cudaSetDevice(s.dev);
+  if (s.ost) cudaStreamSynchronize(s.ost);
   if (s.st) cudaStreamSynchronize(s.st);
   for (void* p : s.allocs) cudaFree(p);
   s.allocs.clear();
@@ -655,8 +665,10 @@ static void strip_free(Strip& s) {
     cudaStreamSynchronize(s.cst);
     cudaStreamDestroy(s.cst);
   }
-  for (cudaEvent_t e : {s.ev_edge, s.ev_int, s.ev_comm})
+  if (s.ost) cudaStreamDestroy(s.ost);
+  for (cudaEvent_t e : {s.ev_edge, s.ev_int, s.ev_comm, s.ev_ofork, s.ev_ojoin})
     if (e) cudaEventDestroy(e);
+  s.ost = nullptr;
   s.cst = nullptr;
   s.st = nullptr;
   s.ev = nullptr;
@@ -1346,6 +1358,8 @@ static int upload_rows(csph* H, Strip& s, int j_begin, int j_end, const double* 
 // wet tiles make 2.5 waves of 3 resident CTAs per SM -- while keeping the launch of the
 // skipped ones cheap (at most 40 K tiles in all).  Measured on one B200: C3 4096^2 -> 32 rows
 // (+22 % over 128), C4 8192^2 -> 64 (+9 %), C5 16384^2 -> 128.
+static int order_reset(csph* H, Strip& s);
+
 static int choose_tile_rows(csph* H, Strip& s, int buf = 0) {
   const int nby = (s.v.ny + kTyMin - 1) / kTyMin;
   dim3 grd((unsigned)s.ntx, (unsigned)nby);
@@ -1389,13 +1403,13 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
     CK(cudaSetDevice(s.dev));
     if ((st = upload_rows(H, s, j_begin, j_end, h, hu, hv, b, psi))) return st;
     if (s.auto_ty && H->p.path == CSPH_PATH_FUSED && (st = choose_tile_rows(H, s))) return st;
+    if ((st = order_reset(H, s))) return st;
     init_ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl);
     CK(cudaMemsetAsync(s.gM, 0, 4 * sizeof(unsigned long long), s.st));
     CK(cudaMemsetAsync(s.tflag, HGS_ALL, 2 * s.tflag_cap, s.st));  // all tiles active
     CK(cudaMemsetAsync(s.tstate, 0, s.tflag_cap, s.st));
     CK(cudaMemsetAsync(s.gflag, HGS_ALL, 4 * (size_t)s.ntx, s.st));
     CK(cudaMemsetAsync(s.hstats, 0, 4 * sizeof(unsigned long long), s.st));
-    CK(cudaMemsetAsync(s.tcost, 0, s.tflag_cap * sizeof(unsigned short), s.st));
     // walls: ghosts of buffer 0 (W is read only on owned cells: no ghosts needed)
     launch_mirror(s.v, s.ctrl, 0, s.st, &H->launches);
     CK(cudaGetLastError());
@@ -1539,8 +1553,50 @@ static Hgs hgs_of(const csph* H, const Strip& s) {
   h.enable = H->p.hgs != 0 && H->p.path == CSPH_PATH_FUSED;
   h.stats = s.hstats;
   h.order = nullptr;
-  h.cost = s.tcost;
+  h.cost = s.tcost + s.tflag_cap * (size_t)H->host_parity;
   return h;
+}
+
+// The launch order of this step's ordered launch, tile rows [tr0, tr1):
+// join the sort made during the previous step, then fork the next step's sort onto the
+// order stream (from the costs of the step before this one), beside this step's kernel.
+static int order_step(csph* H, Strip& s, int tr0, int tr1, Hgs& hg) {
+  if (!hg.enable || tr1 <= tr0) return CSPH_OK;
+  const int p = H->host_parity;
+  const size_t cap = s.tflag_cap;
+  if (s.osort_pending) {
+    CK(cudaStreamWaitEvent(s.st, s.ev_ojoin, 0));
+    s.osort_pending = false;
+  }
+  hg.order = s.torder + cap * (size_t)p;
+  CK(cudaEventRecord(s.ev_ofork, s.st));
+  CK(cudaStreamWaitEvent(s.ost, s.ev_ofork, 0));
+  launch_order_tiles(s.tcost + cap * (size_t)(p ^ 1), s.ntx, tr0, tr1,
+                     s.torder + cap * (size_t)(p ^ 1), s.ost, &H->launches);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(s.ev_ojoin, s.ost));
+  s.osort_pending = true;
+  return CSPH_OK;
+}
+
+// The main stream waits for a pending sort (before a capture ends or starts, at the end of
+// csph_step, before the order buffers are reset).
+static int order_join(Strip& s) {
+  if (s.osort_pending) {
+    CK(cudaStreamWaitEvent(s.st, s.ev_ojoin, 0));
+    s.osort_pending = false;
+  }
+  return CSPH_OK;
+}
+
+// Natural order and zero costs for both parities (a new state or tiling).
+static int order_reset(csph* H, Strip& s) {
+  int st;
+  if ((st = order_join(s))) return st;
+  CK(cudaMemsetAsync(s.tcost, 0, 2 * s.tflag_cap * sizeof(unsigned short), s.st));
+  launch_order_identity(s.torder, (int)(2 * s.tflag_cap), s.st, &H->launches);
+  CK(cudaGetLastError());
+  return CSPH_OK;
 }
 
 // One step of a single-grid handle: the 3 launches (clear flags, step kernel(s), ctrl)
@@ -1551,10 +1607,8 @@ static int single_step(csph* H, Strip& s) {
     launch_mirror(s.v, s.ctrl, 1, s.st, &H->launches);
   } else {
     Hgs hg = hgs_of(H, s);
-    if (hg.enable) {  // costliest tiles first (last step's costs)
-      launch_order_tiles(s.tcost, s.ntx, 0, s.nty, s.torder, s.st, &H->launches);
-      hg.order = s.torder;
-    }
+    int st;
+    if ((st = order_step(H, s, 0, s.nty, hg))) return st;  // costliest tiles first
     launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, s.ty, hg, s.st, &H->launches);
   }
   CK(cudaGetLastError());
@@ -1589,11 +1643,14 @@ static int graph_pair(csph* H, Strip& s, long long* per_launch) {
     // graph is then launched on the handle's stream
     if (!H->cap) CK(cudaStreamCreateWithFlags(&H->cap, cudaStreamNonBlocking));
     const cudaStream_t user = s.st;
+    int st;
+    if ((st = order_join(s))) return st;  // no dependency on work outside the capture
     s.st = H->cap;
     cudaError_t e = cudaStreamBeginCapture(s.st, cudaStreamCaptureModeRelaxed);
-    int st = e == cudaSuccess ? CSPH_OK : fail(CSPH_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    st = e == cudaSuccess ? CSPH_OK : fail(CSPH_ECUDA, "graph capture: %s", cudaGetErrorString(e));
     if (!st) st = capture_step(H, s);
     if (!st) st = capture_step(H, s);
+    if (!st) st = order_join(s);  // every forked sort rejoins the capture
     e = cudaStreamEndCapture(s.st, &gr);
     s.st = user;
     H->host_parity = p0;
@@ -1671,11 +1728,8 @@ static int split_step(csph* H, int n, int q) {
     CK(cudaSetDevice(s.dev));
     if (sp[r]) {
       Hgs hg = hgs_of(H, s);
-      if (hg.enable) {  // the interior tile rows, costliest first
-        launch_order_tiles(s.tcost, s.ntx, lo[r] / s.ty, hi[r] / s.ty, s.torder, s.st,
-                           &H->launches);
-        hg.order = s.torder;
-      }
+      // the interior tile rows, costliest first
+      if ((st = order_step(H, s, lo[r] / s.ty, hi[r] / s.ty, hg))) return st;
       launch_fused_step(s.v, s.ctrl, H->P, s.gM, lo[r], hi[r], s.ty, hg, s.st, &H->launches);
     }
     if (H->profiling && r == 0) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
@@ -1763,9 +1817,9 @@ int csph_step(csph_t* H, int nsteps) {
       Strip& s = H->s[si];
       CK(cudaSetDevice(s.dev));
       Hgs hg = hgs_of(H, s);
-      if (H->p.path != CSPH_PATH_STAGED && hg.enable) {  // costliest tiles first
-        launch_order_tiles(s.tcost, s.ntx, 0, s.nty, s.torder, s.st, &H->launches);
-        hg.order = s.torder;
+      if (H->p.path != CSPH_PATH_STAGED) {  // costliest tiles first
+        int st;
+        if ((st = order_step(H, s, 0, s.nty, hg))) return st;
       }
       if (H->profiling && si == 0) CK(cudaEventRecord(H->evs[2 * n], s.st));
       if (H->p.path == CSPH_PATH_STAGED)
@@ -1788,6 +1842,10 @@ int csph_step(csph_t* H, int nsteps) {
     H->host_parity = q;
   }
   int status = 0;
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    if ((status = order_join(s))) return status;
+  }
   for (auto& s : H->s) {
     CK(cudaSetDevice(s.dev));
     Ctrl c;
@@ -2113,6 +2171,7 @@ int csph_rebalance_rows(csph_t* H, const int* bounds) {
     }
     CK(cudaGetLastError());
     if (s.auto_ty && H->p.path == CSPH_PATH_FUSED && (st = choose_tile_rows(H, s, p))) return st;
+    if ((st = order_reset(H, s))) return st;
     CK(cudaStreamSynchronize(s.st));
   }
   // a caller stream (csph_set_stream, single-strip handles) carries over

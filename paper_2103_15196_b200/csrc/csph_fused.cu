@@ -803,7 +803,18 @@ __global__ void __launch_bounds__(kOrdThreads, 1) order_tiles_kernel(
   }
 }
 
+__global__ void order_identity_kernel(int* order, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) order[i] = i;
+}
+
 }  // namespace
+
+void launch_order_identity(int* order, int n, cudaStream_t st, long long* nlaunch) {
+  if (n <= 0) return;
+  order_identity_kernel<<<(n + 255) / 256, 256, 0, st>>>(order, n);
+  *nlaunch += 1;
+}
 
 void launch_order_tiles(const unsigned short* cost, int ntx, int tr0, int tr1, int* order,
                         cudaStream_t st, long long* nlaunch) {

@@ -37,8 +37,8 @@ struct Hgs {
   unsigned long long* stats;  // [0] tiles marched, [1] copied (identity), [2] skipped
   // Launch order: CTA i of the launch takes tile order[i] (linear index
   // within the launch's tile rows; nullptr = natural order), costliest first.  cost[ti]:
-  // the rows the tile's last march computed at full cost (0 for identity / skipped tiles),
-  // written by the step kernel and read by the next step's order_tiles.
+  // the rows the tile's march computed at full cost (0 for identity / skipped tiles),
+  // written by the step kernel; the order of the step after next is sorted from it.
   const int* order;
   unsigned short* cost;
 };
@@ -55,6 +55,9 @@ void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long
 // (one CTA, a counting sort; ties in any order: the step's results do not depend on it).
 void launch_order_tiles(const unsigned short* cost, int ntx, int tr0, int tr1, int* order,
                         cudaStream_t st, long long* nlaunch);
+
+// order[i] = i for i < n (the natural order).
+void launch_order_identity(int* order, int n, cudaStream_t st, long long* nlaunch);
 
 // Service kernels (csph_api.cu).
 void launch_mirror(const StripView& S, const Ctrl* C, int next_parity_from_ctrl,
