@@ -22,6 +22,7 @@ from paper_2103_15196_b200 import csph
 c = synth.config("C5")
 n = c.nx
 steps = int(os.environ.get("STEPS", "10"))
+REPS = int(os.environ.get("REPS", "3"))
 TY = int(os.environ.get("TY", "0"))  # tile rows (0 = the library's auto rule)
 NS = [int(x) for x in os.environ.get("NS", "2,4,8").split(",")]
 KINDS = os.environ.get("KINDS", "even,balanced").split(",")
@@ -35,12 +36,17 @@ def strip_ms(j0, j1):
     f = synth.fill(c, j0, j1)
     g = csph.csph_create(n, j1 - j0, c.dx, csph.params_from(c.params, tile_rows=TY))
     g.set_state(*f)
-    g.step(3)
+    g.step(4)  # even: the timed steps start at parity 0, whose pair graph is captured here
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(); g.step(steps); e1.record(); torch.cuda.synchronize()
+    ts = []
+    for rep in range(REPS):  # the steady state: the fastest of REPS timed regions (a rare
+        e0.record(); g.step(steps); e1.record(); torch.cuda.synchronize()  # slow one is noted)
+        ts.append(e0.elapsed_time(e1) / steps)
     g.destroy()
-    return e0.elapsed_time(e1) / steps
+    if max(ts) > 1.2 * min(ts):
+        print(f"  note: rows [{j0}, {j1}) timed {[round(t, 3) for t in ts]} ms/step", flush=True)
+    return min(ts)
 
 
 HALO_GBS = float(os.environ.get("HALO_GBS", "300"))
