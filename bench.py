@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--partition", choices=["balanced", "even"], default="balanced",
                     help="N > 1 row strips: balanced by the initial wet cells per row "
                          "(csph_balance_rows, DESIGN.md 9) or the paper's even Ny_dev split")
+    ap.add_argument("--halo", choices=["push", "nccl"], default="push",
+                    help="N > 1: ghost rows written by the step kernel into the neighbours' "
+                         "buffers over NVLink (CUDA IPC; DESIGN.md 9) or NCCL send/recv")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                     help="strong: the whole 16384^2 C5 grid split over N GPUs (default); "
                          "weak: rows [0, 2048 N) of the same C5 field, 2048 rows per GPU")
@@ -272,7 +275,7 @@ def run_ours(a, rank, world, local):
                          dict(c.params))
     path = csph.CSPH_PATH_FUSED if a.path == "fused" else csph.CSPH_PATH_STAGED
     p = csph.params_from(c.params, path=path, device=local, tile_rows=a.tile_rows,
-                         precision=a.precision)
+                         precision=a.precision, halo_push=1 if a.halo == "push" else 0)
     bounds = strip_bounds(gen, c.ny, c.nx, world, rank,
                           "dist1" if (a.dist and world == 1 and a.partition == "balanced")
                           else a.partition, "cuda")
@@ -287,6 +290,15 @@ def run_ours(a, rank, world, local):
         dist.broadcast(idt, 0)
         g = csph.csph_create_dist_rows(c.nx, c.ny, c.dx, p, rank, world, bounds, local,
                                        bytes(idt.cpu().numpy().tobytes()))
+        # halo push: every rank maps its neighbours' buffers through CUDA IPC,
+        # so the step kernels write the ghost rows over NVLink (no send/recv, no edge split)
+        if a.halo == "push" and world > 1:
+            blob = torch.frombuffer(bytearray(g.ipc_export()), dtype=torch.uint8).cuda()
+            blobs = [torch.empty_like(blob) for _ in range(world)]
+            dist.all_gather(blobs, blob)
+            nb = [bytes(x.cpu().numpy().tobytes()) for x in blobs]
+            g.ipc_link(nb[rank - 1] if rank > 0 else None,
+                       nb[rank + 1] if rank < world - 1 else None)
     else:
         g = csph.csph_create(c.nx, c.ny, c.dx, p)
     stream = torch.cuda.current_stream()
@@ -427,7 +439,9 @@ def run_ours(a, rank, world, local):
                                f"2048 rows per GPU)" if a.scaling == "weak" else ""),
                 "grid": [c.nx, c.ny], "cells": cells, "dx_m": c.dx, "wet_fraction": wet,
                 "psi": "field" if psi_field else "uniform", "physics": c.params,
-                "path": a.path, "parallelism": f"row strips x{world} (NCCL halos + allreduce)"
+                "path": a.path, "parallelism": f"row strips x{world} ("
+                + ("kernel-pushed halos over NVLink" if a.halo == "push" else "NCCL halos")
+                + " + NCCL max-allreduce)"
                 if distributed else "single GPU",
                 "partition": {"kind": a.partition, "bounds": bounds} if distributed else None,
                 "l2": "state (>= 19 GB) larger than the 126 MB L2; no flush needed",

@@ -88,6 +88,12 @@ typedef struct {
   double m_real;     /* Grass exponent as a real number (Eq.3, "A_J, m are the
                         constant coefficients"); < 0 (default -1): use the integer m_grass;
                         >= 0: |v|^m by the pinned pow of DESIGN.md 3.12 (fp64 only) */
+  int    halo_push;  /* fused path, several strips: 1 (default) the step kernel
+                        writes each strip's first / last 3 rows and facing tile flags
+                        straight into the neighbouring strip's ghost rows (peer memory: a
+                        strip of the same process, or another rank's GPU mapped through CUDA
+                        IPC, csph_ipc_*); 0, or no peer access: peer copies (MULTI) / NCCL
+                        send-recv (DIST) after the edge tile rows.  Bitwise identical. */
 } csph_params;
 
 /* Fill *p with the defaults above. */
@@ -198,9 +204,14 @@ const char* csph_last_error(void);
 
 /* ---- multi-GPU: one process per GPU, row strips, NCCL over NVLink ------- */
 /* Rank 0 makes the NCCL unique id; the harness broadcasts it (e.g. through
- * torch.distributed) and every rank calls csph_create_dist with it.  Halo
- * rows (3 per side x 4 fields) go by ncclSend/ncclRecv to ranks r-1, r+1
- * (no wrap-around, reading #18) and the Eq.7 maxima by ncclAllReduce(max). */
+ * torch.distributed) and every rank calls csph_create_dist with it.  The Eq.7 maxima (and
+ * the negative-depth flag) are combined by ncclAllReduce(max), once per step.  Halo rows
+ * (3 per side x 4 fields, no wrap-around, reading #18) and the facing HGS tile flags:
+ *  - pushed by the step kernel itself into the neighbours' ghost rows over NVLink (peer
+ *    stores from the K8 epilogue of the first / last tile row) once
+ *    csph_ipc_link has mapped the neighbours' buffers (params.halo_push = 1, fused path);
+ *  - otherwise ncclSend/ncclRecv to ranks r-1, r+1 after the edge tile rows, overlapped
+ *    with the interior. */
 int         csph_nccl_id_bytes(void);
 int         csph_make_nccl_id(void* out);
 csph_t*     csph_create_dist(int nx, int ny, double dx, const csph_params* p,
@@ -213,11 +224,27 @@ csph_t*     csph_create_dist_rows(int nx, int ny, double dx, const csph_params* 
                                   int rank, int nranks, const int* bounds, int local_device,
                                   const void* nccl_id);
 
+/* DIST halo push.  csph_ipc_export writes csph_ipc_blob_bytes() bytes
+ * describing this rank's state buffers and ghost tile-flag rows (CUDA IPC handles, strip
+ * geometry) into out (host memory).  The harness all-gathers the blobs and every rank calls
+ * csph_ipc_link with the blob of rank-1 (NULL on rank 0) and of rank+1 (NULL on the last
+ * rank): the buffers are mapped (cudaIpcOpenMemHandle, peer access enabled lazily) and the
+ * following steps push halos from inside the kernel instead of send/recv.  Collective in
+ * effect (every rank must link before the next step).  CSPH_EINVAL for a non-DIST handle,
+ * missing / extra blobs or a blob that is not the neighbour's strip (geometry checked),
+ * CSPH_ECUDA if a handle cannot be opened (e.g. no peer access: call it again with
+ * params.halo_push = 0 semantics by not linking -- the handle keeps send/recv).  A 1-rank
+ * handle needs no link.  csph_rebalance_rows drops the links (new buffers): link again. */
+int         csph_ipc_blob_bytes(void);
+int         csph_ipc_export(csph_t*, void* out);
+int         csph_ipc_link(csph_t*, const void* lo_blob, const void* hi_blob);
+
 /* Single-process row-strip decomposition: nstrips strips on the devices
- * listed in `devices` (strips may share a device), halos copied with
- * cudaMemcpyPeerAsync and the maxima combined on the first device.  The same
- * strip kernels and halo layout as csph_create_dist (PAPER.md:198-218's
- * one-host-thread-drives-all-GPUs arrangement). */
+ * listed in `devices` (strips may share a device), halos pushed by the step kernel into the
+ * neighbouring strips' ghost rows (params.halo_push = 1 and peer access between the devices;
+ * otherwise copied with cudaMemcpyPeerAsync after the edge tile rows) and the maxima combined
+ * on the first device.  The same strip kernels and halo layout as csph_create_dist
+ * (PAPER.md:198-218's one-host-thread-drives-all-GPUs arrangement). */
 csph_t*     csph_create_multi(int nx, int ny, double dx, const csph_params* p,
                               int nstrips, const int* devices);
 /* The same with caller-chosen strip rows bounds[0..nstrips] (as csph_create_dist_rows). */

@@ -29,6 +29,7 @@ EXPORTS = [
     "csph_last_launch_count", "csph_profile", "csph_get_profile",
     "csph_selftest_math", "csph_get_tile_stats", "csph_reset_tile_stats",
     "csph_set_fields", "csph_set_fields_rows", "csph_row_weights", "csph_rebalance_rows",
+    "csph_ipc_blob_bytes", "csph_ipc_export", "csph_ipc_link",
 ]
 
 
@@ -42,7 +43,7 @@ class csph_params(ctypes.Structure):
         ("device", ctypes.c_int), ("path", ctypes.c_int), ("tile_rows", ctypes.c_int),
         ("hgs", ctypes.c_int), ("aj_mode", ctypes.c_int), ("s_rel", ctypes.c_double),
         ("open_bc", ctypes.c_int), ("graphs", ctypes.c_int), ("h_bed_min", ctypes.c_double),
-        ("m_real", ctypes.c_double),
+        ("m_real", ctypes.c_double), ("halo_push", ctypes.c_int),
     ]
 
 
@@ -113,6 +114,9 @@ def lib():
         L.csph_last_launch_count.restype = ctypes.c_longlong
         L.csph_row_weights.argtypes = [_vp, _D]
         L.csph_rebalance_rows.argtypes = [_vp, _I]
+        L.csph_ipc_blob_bytes.restype = ctypes.c_int
+        L.csph_ipc_export.argtypes = [_vp, ctypes.c_void_p]
+        L.csph_ipc_link.argtypes = [_vp, ctypes.c_char_p, ctypes.c_char_p]
         _lib = L
     return _lib
 
@@ -287,6 +291,16 @@ class Csph:
         assert w.shape == (self.ny,)
         _check(lib().csph_row_weights(self.h, _p(w)), "csph_row_weights")
         return w
+
+    def ipc_export(self) -> bytes:
+        """This DIST rank's CUDA IPC blob (csph_ipc_export) for the neighbours' csph_ipc_link."""
+        buf = ctypes.create_string_buffer(lib().csph_ipc_blob_bytes())
+        _check(lib().csph_ipc_export(self.h, buf), "csph_ipc_export")
+        return buf.raw
+
+    def ipc_link(self, lo: bytes | None, hi: bytes | None):
+        """Map the neighbours' buffers for the halo push (csph_ipc_link; None on a global edge)."""
+        return _check(lib().csph_ipc_link(self.h, lo, hi), "csph_ipc_link")
 
     def rebalance_rows(self, bounds):
         """Move to new strip bounds (collective for DIST; csph_rebalance_rows)."""

@@ -161,6 +161,10 @@ struct csph {
   int host_parity = 0;  // buffer the next step reads (as launched)
   long long launches = 0;
   unsigned long long* gather = nullptr;  // MULTI: [nstrips*4] on strip 0's device
+  // halo push: every interior strip edge is linked (StripView nH.. ngflag), so
+  // the split step launches each strip whole and moves no halo rows itself
+  bool push = false;
+  std::vector<void*> ipc_open;  // DIST: neighbour buffers opened through CUDA IPC
   bool profiling = false;
   std::vector<cudaEvent_t> evs;  // pairs around the main kernel of each step (strip 0)
   double prof_ms = 0.0;
@@ -740,6 +744,7 @@ void csph_default_params(csph_params* p) {
   p->open_bc = 0;
   p->graphs = 1;
   p->h_bed_min = -1.0;
+  p->halo_push = 1;
   p->m_real = -1.0;
 }
 
@@ -876,6 +881,66 @@ int csph_balance_rows(int ny, int nranks, const double* w, int* bounds) {
   return check_bounds(ny, nranks, bounds);
 }
 
+// ---- halo push: the neighbours' buffers a strip's step kernel writes into
+
+static void push_clear(StripView& v) {
+  for (int side = 0; side < 2; ++side) {
+    for (int k = 0; k < 2; ++k) v.nH[side][k] = v.nQx[side][k] = v.nQy[side][k] = v.nb[side][k] = nullptr;
+    v.ndel[side] = 0;
+    v.ngflag[side] = nullptr;
+  }
+}
+
+// Side `side` of v pushes into the buffers Hs..bs[2] and ghost flags gflag of the neighbour;
+// del: element offset from v's (col, j) to the neighbour's copy of that cell.
+static void push_side(StripView& v, int side, double* const Hs[2], double* const Qxs[2],
+                      double* const Qys[2], double* const bs[2], unsigned char* gflag,
+                      long long del) {
+  for (int k = 0; k < 2; ++k) {
+    v.nH[side][k] = Hs[k];
+    v.nQx[side][k] = Qxs[k];
+    v.nQy[side][k] = Qys[k];
+    v.nb[side][k] = bs[k];
+  }
+  v.ndel[side] = del;
+  v.ngflag[side] = gflag;
+}
+
+// MULTI: strip r pushes its rows 0..2 into the upper ghost rows of strip r-1 and its rows
+// ny-3..ny-1 into the lower ghost rows of strip r+1 (same device, or peer access between
+// the devices); otherwise (or halo_push = 0, or the staged path) the peer copies stay.
+static void push_link_multi(csph* H) {
+  H->push = false;
+  for (auto& s : H->s) push_clear(s.v);
+  const int n = (int)H->s.size();
+  if (!H->p.halo_push || H->p.path != CSPH_PATH_FUSED) return;
+  if (n < 2) {  // no interior edge: nothing to push, the strip is launched whole
+    H->push = true;
+    return;
+  }
+  for (int r = 0; r + 1 < n; ++r) {
+    const int a = H->s[r].dev, b = H->s[r + 1].dev;
+    int ab = 1, ba = 1;
+    if (a != b) {
+      cudaDeviceCanAccessPeer(&ab, a, b);
+      cudaDeviceCanAccessPeer(&ba, b, a);
+    }
+    if (!ab || !ba) return;
+  }
+  for (int r = 0; r < n; ++r) {
+    StripView& v = H->s[r].v;
+    if (r > 0) {
+      Strip& o = H->s[r - 1];
+      push_side(v, 0, o.v.H, o.v.Qx, o.v.Qy, o.v.b, o.gflag, (long long)o.v.ny * v.pitch);
+    }
+    if (r < n - 1) {
+      Strip& o = H->s[r + 1];
+      push_side(v, 1, o.v.H, o.v.Qx, o.v.Qy, o.v.b, o.gflag, -(long long)v.ny * v.pitch);
+    }
+  }
+  H->push = true;
+}
+
 csph_t* csph_create_multi(int nx, int ny, double dx, const csph_params* p, int nstrips,
                           const int* devices) {
   std::vector<int> b;
@@ -922,6 +987,7 @@ csph_t* csph_create_multi_rows(int nx, int ny, double dx, const csph_params* p, 
     csph_destroy(H);
     return nullptr;
   }
+  push_link_multi(H);
   return H;
 }
 
@@ -981,7 +1047,103 @@ csph_t* csph_create_dist_rows(int nx, int ny, double dx, const csph_params* p, i
     g_err = keep;
     return nullptr;
   }
+  // one rank has no interior edge (launched whole); more push once csph_ipc_link has
+  // mapped the neighbours' buffers, and send/recv halos until then
+  H->push = nranks == 1 && p->halo_push && p->path == CSPH_PATH_FUSED;
   return H;
+}
+
+// ---- DIST halo push through CUDA IPC
+
+namespace {
+struct IpcBlob {
+  int magic, rank, ny, pitch, ntx, prec;
+  cudaIpcMemHandle_t f[4][2];  // H, Qx, Qy, b x parity
+  cudaIpcMemHandle_t gflag;
+};
+constexpr int kIpcMagic = 0x43535048;  // "CSPH"
+}  // namespace
+
+static void ipc_unlink(csph* H) {
+  for (void* p : H->ipc_open) cudaIpcCloseMemHandle(p);
+  H->ipc_open.clear();
+  for (auto& s : H->s) push_clear(s.v);
+  H->push = H->mode == DIST && H->nranks == 1 && H->p.halo_push && H->p.path == CSPH_PATH_FUSED;
+}
+
+int csph_ipc_blob_bytes(void) { return (int)sizeof(IpcBlob); }
+
+int csph_ipc_export(csph_t* H, void* out) {
+  if (!H || !out) return fail(CSPH_EINVAL, "NULL argument");
+  if (H->mode != DIST) return fail(CSPH_EINVAL, "csph_ipc_export needs a DIST handle");
+  Strip& s = H->s[0];
+  CK(cudaSetDevice(s.dev));
+  IpcBlob b;
+  memset(&b, 0, sizeof b);
+  b.magic = kIpcMagic;
+  b.rank = H->rank;
+  b.ny = s.v.ny;
+  b.pitch = s.v.pitch;
+  b.ntx = s.ntx;
+  b.prec = s.v.prec;
+  double* const* F[4] = {s.v.H, s.v.Qx, s.v.Qy, s.v.b};
+  for (int k = 0; k < 4; ++k)
+    for (int q = 0; q < 2; ++q) CK(cudaIpcGetMemHandle(&b.f[k][q], F[k][q]));
+  CK(cudaIpcGetMemHandle(&b.gflag, s.gflag));
+  memcpy(out, &b, sizeof b);
+  return CSPH_OK;
+}
+
+int csph_ipc_link(csph_t* H, const void* lo, const void* hi) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  if (H->mode != DIST) return fail(CSPH_EINVAL, "csph_ipc_link needs a DIST handle");
+  if ((H->rank > 0) != (lo != nullptr) || (H->rank < H->nranks - 1) != (hi != nullptr))
+    return fail(CSPH_EINVAL, "csph_ipc_link: give exactly the neighbours' blobs (rank %d of %d)",
+                H->rank, H->nranks);
+  ipc_unlink(H);
+  if (!H->p.halo_push || H->p.path != CSPH_PATH_FUSED) return CSPH_OK;  // send/recv halos
+  Strip& s = H->s[0];
+  CK(cudaSetDevice(s.dev));
+  graphs_reset(H);  // captured steps bake in the halo transport
+  const void* blobs[2] = {lo, hi};
+  for (int side = 0; side < 2; ++side) {
+    if (!blobs[side]) continue;
+    IpcBlob b;
+    memcpy(&b, blobs[side], sizeof b);
+    const int want = H->rank + (side == 0 ? -1 : 1);
+    if (b.magic != kIpcMagic || b.rank != want || b.pitch != s.v.pitch || b.ntx != s.ntx ||
+        b.prec != s.v.prec || b.ny != H->bounds[want + 1] - H->bounds[want]) {
+      ipc_unlink(H);
+      return fail(CSPH_EINVAL, "csph_ipc_link: blob of side %d is not rank %d's strip", side, want);
+    }
+    double* Fs[4][2];
+    unsigned char* gf = nullptr;
+    for (int k = 0; k < 4; ++k)
+      for (int q = 0; q < 2; ++q) {
+        void* p = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, b.f[k][q], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          ipc_unlink(H);
+          return fail(CSPH_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+        }
+        H->ipc_open.push_back(p);
+        Fs[k][q] = (double*)p;
+      }
+    {
+      void* p = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&p, b.gflag, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        ipc_unlink(H);
+        return fail(CSPH_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+      }
+      H->ipc_open.push_back(p);
+      gf = (unsigned char*)p;
+    }
+    const long long del = side == 0 ? (long long)b.ny * s.v.pitch : -(long long)s.v.ny * s.v.pitch;
+    push_side(s.v, side, Fs[0], Fs[1], Fs[2], Fs[3], gf, del);
+  }
+  H->push = true;
+  return CSPH_OK;
 }
 
 void csph_destroy(csph_t* H) {
@@ -989,6 +1151,7 @@ void csph_destroy(csph_t* H) {
   if (!H->s.empty()) cudaSetDevice(H->s[0].dev);
   graphs_free(H);
   for (auto e : H->evs) cudaEventDestroy(e);
+  for (void* p : H->ipc_open) cudaIpcCloseMemHandle(p);
   for (auto& s : H->s) strip_free(s);
   if (H->gather) {
     cudaSetDevice(H->s.empty() ? 0 : H->s[0].dev);
@@ -1690,7 +1853,10 @@ static bool edge_split(const Strip& s, int* lo, int* hi) {
 // exchange of buffer q on the comm streams (NCCL send/recv or peer copies) overlapped
 // with the interior, then the combine of the Eq.7 maxima and the negative-depth flag, and
 // the ctrl kernel once the halo has landed.
+static int push_step(csph* H, int n);
+
 static int split_step(csph* H, int n, int q) {
+  if (H->push) return push_step(H, n);
   const int ns = (int)H->s.size();
   std::vector<int> lo(ns, 0), hi(ns, 0);
   std::vector<char> sp(ns, 0);
@@ -1752,6 +1918,43 @@ static int split_step(csph* H, int n, int q) {
       for (int o = r - 1; o <= r + 1; ++o)
         if (o >= 0 && o < ns) CK(cudaStreamWaitEvent(s.st, H->s[o].ev_comm, 0));
     }
+  }
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 1);
+    H->launches += 1;
+    CK(cudaGetLastError());
+  }
+  return CSPH_OK;
+}
+
+// One step of a DIST or MULTI handle whose strips push their halos: every strip
+// launched whole (its edge tile rows write the neighbours' ghost rows and flags from inside
+// the kernel), then the combine of the Eq.7 maxima and the negative-depth flag -- which is
+// also the step's barrier: no strip's next step starts before every strip's kernel (and so
+// every push into its ghost rows) is done -- and the ctrl kernels.
+static int push_step(csph* H, int n) {
+  const int ns = (int)H->s.size();
+  int st;
+  for (int r = 0; r < ns; ++r) {
+    Strip& s = H->s[r];
+    CK(cudaSetDevice(s.dev));
+    Hgs hg = hgs_of(H, s);
+    if ((st = order_step(H, s, 0, s.nty, hg))) return st;  // costliest tiles first
+    if (H->profiling && r == 0) CK(cudaEventRecord(H->evs[2 * n], s.st));
+    launch_fused_step(s.v, s.ctrl, H->P, s.gM, 0, s.v.ny, s.ty, hg, s.st, &H->launches);
+    if (H->profiling && r == 0) CK(cudaEventRecord(H->evs[2 * n + 1], s.st));
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s.ev_int, s.st));
+  }
+  if (H->mode == DIST) {
+    Strip& s = H->s[0];
+    CK(cudaStreamWaitEvent(s.cst, s.ev_int, 0));
+    if ((st = allreduce_nccl(H, s.cst))) return st;
+    CK(cudaEventRecord(s.ev_comm, s.cst));
+    CK(cudaStreamWaitEvent(s.st, s.ev_comm, 0));
+  } else if ((st = gather_multi(H, &Strip::ev_int))) {
+    return st;
   }
   for (auto& s : H->s) {
     CK(cudaSetDevice(s.dev));
@@ -2183,6 +2386,8 @@ int csph_rebalance_rows(csph_t* H, const int* bounds) {
   }
   for (auto& s : H->s) strip_free(s);
   H->s = std::move(news);
+  if (H->mode == MULTI) push_link_multi(H);
+  if (H->mode == DIST) ipc_unlink(H);  // new buffers: the caller links them again
   if (H->mode == DIST) H->bounds = nb;
   return CSPH_OK;
 }

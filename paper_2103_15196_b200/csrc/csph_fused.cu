@@ -227,6 +227,13 @@ __global__ void __launch_bounds__(NT, MINB)
   };
   const int tr = y0 / TY;
   const int ti = tr * hg.ntx + bx;
+  // HGS flags of a tile row facing a neighbouring strip go into its ghost flag rows too
+  // (halo push): my first tile row to the strip below, my last to the one above
+  auto push_flags = [&](unsigned m) {
+    const size_t g = 2 * (size_t)hg.ntx * (size_t)(par ^ 1) + (size_t)bx;
+    if (tr == 0 && S.ngflag[0]) S.ngflag[0][g + hg.ntx] = (unsigned char)m;
+    if (tr == hg.nty - 1 && S.ngflag[1]) S.ngflag[1][g] = (unsigned char)m;
+  };
   // across an interior strip edge the facing tile row is the neighbouring strip's, whose
   // flags arrive with the halo rows (hg.glo / hg.ghi); without them such a tile marches
   if (hg.enable && (S.wall_lo || y0 > 0 || hg.glo) && (S.wall_hi || y1 < S.ny || hg.ghi)) {
@@ -262,6 +269,8 @@ __global__ void __launch_bounds__(NT, MINB)
               write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
             else
               write_wall_ghosts_t(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
+            if (j < GY || j >= S.ny - GY)
+              push_halo_cell(S, par ^ 1, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
           }
         }
         const bool any = __syncthreads_or(cwet);
@@ -269,8 +278,10 @@ __global__ void __launch_bounds__(NT, MINB)
           if (hg.cost) hg.cost[ti] = 0;
           hg.tstate[ti] = any ? 0 : (unsigned char)(stt + 1);
           hg.fnext[ti] = any ? HGS_ALL : 0;  // conservative: every band
+          push_flags(any ? HGS_ALL : 0);
           atomicAdd(&hg.stats[1], 1ull);
         }
+        if (tr == 0 || tr == hg.nty - 1) __threadfence_system();  // pushed rows and flags
         // a cell made wet by a source has Q' = +0: its Eq.7 terms are those of a
         // still wet cell
         if (cwet) {
@@ -291,6 +302,8 @@ __global__ void __launch_bounds__(NT, MINB)
       if (t == 0) {
         atomicAdd(&hg.stats[2], 1ull);
         hg.fnext[ti] = 0;
+        push_flags(0);
+        if (tr == 0 || tr == hg.nty - 1) __threadfence_system();
         if (hg.cost) hg.cost[ti] = 0;
       }
       return;  // both buffers already hold the identity (tstate >= 2, no source)
@@ -372,6 +385,7 @@ __global__ void __launch_bounds__(NT, MINB)
       write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
     else
       write_wall_ghosts_t(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
+    if (j < GY || j >= S.ny - GY) push_halo_cell(S, par ^ 1, col, j, Hn, Qxn, Qyn, bn, colg);
     if (wet) {
       T t1, t2, t3;
       dt_terms_t<GEN>(Q, Hn, Qxn, Qyn, W3, aj_at(off(pitch, col, j), Hn),
@@ -669,7 +683,9 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int w = 0; w < NT / 32; ++w) m |= sm.wm[w];
     hg.fnext[ti] = (unsigned char)m;
     hg.tstate[ti] = 0;
+    push_flags(m);
   }
+  if (tr == 0 || tr == hg.nty - 1) __threadfence_system();  // pushed rows: visible to peers
   if (t == 0 && hg.cost) hg.cost[ti] = (unsigned short)min(nfull, 65535);
   if (t == 0 && hg.stats) atomicAdd(&hg.stats[0], 1ull);
   if (t < 3) {

@@ -26,13 +26,17 @@ def single(cs, c, f, steps, path):
     return g.get_dt_log(steps)[0], g.get_state()
 
 
+@pytest.mark.parametrize("push", [1, 0])
 @pytest.mark.parametrize("path", [0, 1])
 @pytest.mark.parametrize("nstrips", [2, 3, 5])
-def test_multi_strips_bitwise(cs, nstrips, path):
+def test_multi_strips_bitwise(cs, nstrips, path, push):
+    """2-5 strips on one device: halos pushed from inside the step kernel (halo_push = 1,
+    fused path) or peer copies (halo_push = 0, and the staged path) -- bitwise the single grid."""
     c = synth.config("C4", 160, 203)
     f = synth.fill(c)
     dt0, ref = single(cs, c, f, 60, path)
-    g = cs.csph_create_multi(c.nx, c.ny, c.dx, cs.params_from(c.params, path=path), [0] * nstrips)
+    g = cs.csph_create_multi(c.nx, c.ny, c.dx, cs.params_from(c.params, path=path, halo_push=push),
+                             [0] * nstrips)
     g.set_state(*f)
     g.step(60)
     dt, _ = g.get_dt_log(60)
@@ -69,8 +73,9 @@ def test_dist_single_rank_nccl(cs):
     g.destroy()
 
 
+@pytest.mark.parametrize("push", [1, 0])
 @pytest.mark.parametrize("path", [0, 1])
-def test_uneven_strips_bitwise(cs, path):
+def test_uneven_strips_bitwise(cs, path, push):
     """Caller-chosen (load-balanced) strip rows, csph_create_multi_rows: strips of 3, 17,
     150 and 33 rows are bitwise the single grid; bounds from csph_balance_rows too."""
     c = synth.config("C4", 160, 203)
@@ -78,7 +83,8 @@ def test_uneven_strips_bitwise(cs, path):
     dt0, ref = single(cs, c, f, 50, path)
     w = (f[0] > 1e-6).sum(axis=1) + 0.03 * c.nx
     for bounds in ([0, 3, 20, 170, 203], cs.csph_balance_rows(c.ny, 3, w)):
-        g = cs.csph_create_multi_rows(c.nx, c.ny, c.dx, cs.params_from(c.params, path=path),
+        g = cs.csph_create_multi_rows(c.nx, c.ny, c.dx,
+                                      cs.params_from(c.params, path=path, halo_push=push),
                                       [0] * (len(bounds) - 1), bounds)
         g.set_state(*f)
         g.step(50)
@@ -88,6 +94,35 @@ def test_uneven_strips_bitwise(cs, path):
         g.destroy()
     with pytest.raises(cs.CsphError):
         cs.csph_create_multi_rows(c.nx, c.ny, c.dx, cs.params_from(c.params), [0, 0], [0, 2, 203])
+
+
+def test_dist_ipc_link_single_rank(cs):
+    """The DIST halo push's link step (csph_ipc_export / csph_ipc_link) on one
+    rank: the blob exports; a rank with no neighbours links nothing and steps whole (sort,
+    fused kernel, ctrl per step: no edge split, no halo traffic), bitwise the single grid; a
+    blob where no neighbour exists, or one for the wrong rank, is rejected."""
+    c = synth.config("C5", 200, 96)
+    f = synth.fill(c)
+    dt0, ref = single(cs, c, f, 40, 0)
+    g = cs.csph_create_dist_rows(c.nx, c.ny, c.dx, cs.params_from(c.params, tile_rows=16),
+                                 0, 1, [0, c.ny], 0, cs.csph_make_nccl_id())
+    blob = g.ipc_export()
+    assert len(blob) == cs.lib().csph_ipc_blob_bytes() and blob[:4] == b"HPSC"
+    g.ipc_link(None, None)
+    with pytest.raises(cs.CsphError):
+        g.ipc_link(blob, None)  # rank 0 has no neighbour below
+    g.ipc_link(None, None)
+    g.set_state(*f)
+    g.step(40)
+    assert np.array_equal(g.get_dt_log(40)[0], dt0)
+    for a, r in zip(g.get_state(), ref):
+        assert np.array_equal(a, r)
+    assert g.last_launch_count() == 40 * 3
+    g.destroy()
+    m = cs.csph_create_multi(c.nx, c.ny, c.dx, cs.params_from(c.params), [0, 0])
+    with pytest.raises(cs.CsphError):
+        m.ipc_export()  # DIST only
+    m.destroy()
 
 
 def test_dist_rows_single_rank(cs):
@@ -107,13 +142,14 @@ def test_dist_rows_single_rank(cs):
 
 @pytest.mark.parametrize("tile_rows", [16, 40, 48, 64])
 def test_dist_split_launches(cs, tile_rows):
-    """The multi-GPU step's launch sequence (edge tile rows, NCCL halo on the comm stream,
-    interior, allreduce) on one rank: 2..6 tile rows, ragged last tile row,
-    HGS on -- bitwise the single grid."""
+    """The send/recv multi-GPU step (halo_push = 0: edge tile rows, NCCL halo on the comm
+    stream, interior, allreduce) on one rank: 2..6 tile rows, ragged last tile
+    row, HGS on -- bitwise the single grid."""
     c = synth.config("C5", 200, 96)
     f = synth.fill(c)
     dt0, ref = single(cs, c, f, 40, 0)
-    g = cs.csph_create_dist_rows(c.nx, c.ny, c.dx, cs.params_from(c.params, tile_rows=tile_rows),
+    g = cs.csph_create_dist_rows(c.nx, c.ny, c.dx,
+                                 cs.params_from(c.params, tile_rows=tile_rows, halo_push=0),
                                  0, 1, [0, c.ny], 0, cs.csph_make_nccl_id())
     g.set_state(*f)
     g.step(40)
@@ -132,8 +168,9 @@ def test_dist_split_launches(cs, tile_rows):
     g.destroy()
 
 
+@pytest.mark.parametrize("push", [1, 0])
 @pytest.mark.parametrize("nstrips", [2, 4])
-def test_front_crosses_strip_edges_hgs(cs, nstrips):
+def test_front_crosses_strip_edges_hgs(cs, nstrips, push):
     """HGS across strip edges (ghost tile flags): a dam-break front starts
     in the first strip and runs into dry strips whose edge tiles were being skipped; with
     16-row tiles and uneven strips the result is bitwise the single grid without HGS."""
@@ -151,7 +188,7 @@ def test_front_crosses_strip_edges_hgs(cs, nstrips):
     dt0, ref = g.get_dt_log(steps)[0], g.get_state()
     g.destroy()
     bounds = [0, 37, 70, 131, 180] if nstrips == 4 else [0, 41, 180]
-    g = cs.csph_create_multi_rows(nx, ny, 1.0, cs.params_from(phys, tile_rows=16),
+    g = cs.csph_create_multi_rows(nx, ny, 1.0, cs.params_from(phys, tile_rows=16, halo_push=push),
                                   [0] * nstrips, bounds)
     g.set_state(*f)
     g.step(steps)
@@ -162,8 +199,9 @@ def test_front_crosses_strip_edges_hgs(cs, nstrips):
     g.destroy()
 
 
+@pytest.mark.parametrize("push", [1, 0])
 @pytest.mark.parametrize("tile_rows", [16, 32])
-def test_split_strips_short_last_tile_vs_oracle(cs, tile_rows):
+def test_split_strips_short_last_tile_vs_oracle(cs, tile_rows, push):
     """Overlapped multi-strip steps (edge tile rows -> halo on the comm stream || interior,
     DESIGN.md 9) with strips whose last tile row has 1 or 2 rows (ny % ty in {1, 2}): the
     halo rows sent at the edge event must all be final.  Four strips of
@@ -181,7 +219,8 @@ def test_split_strips_short_last_tile_vs_oracle(cs, tile_rows):
     assert ref.set_state(*f) == 0
     st, dt0, lim0 = ref.step(steps)
     assert st == 0
-    g = cs.csph_create_multi_rows(c.nx, c.ny, c.dx, cs.params_from(c.params, tile_rows=tile_rows),
+    g = cs.csph_create_multi_rows(c.nx, c.ny, c.dx,
+                                  cs.params_from(c.params, tile_rows=tile_rows, halo_push=push),
                                   [0] * 4, bounds)
     g.set_state(*f)
     g.step(steps)
