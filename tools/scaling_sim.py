@@ -2,14 +2,17 @@
 of rows [j0, j1) is run alone as a walled domain and its step time measured; the N-GPU step
 time is the slowest strip plus the communication the step cannot hide, modelled as:
 
-  * halo: 3 rows x 4 fields x the padded row (2 sides) over NVLink 5 at HALO_GBS (default
-    300 GB/s effective for ~1.6 MB NCCL send/recv) + HALO_US latency (default 15 us); it runs
-    on the comm stream while the interior tile rows compute, so only the part exceeding the
-    interior launch is exposed;
+  * HALO=push (default; csph_ipc_link, the bench's --halo push): the ghost rows are written by
+    the edge tiles' K8 epilogue over NVLink (3 rows x 4 fields x the padded row per side,
+    ~1.6 MB, ~2 us at NVLink 5 rates) inside the step kernel -- nothing exposed, and the strip
+    is launched whole exactly as timed here;
+    HALO=nccl: 3 rows x 4 fields x the padded row (2 sides) over NVLink 5 at HALO_GBS
+    (default 300 GB/s effective for ~1.6 MB NCCL send/recv) + HALO_US latency (default 15 us)
+    on the comm stream while the interior tile rows compute (only the excess over the
+    interior launch is exposed); the strips are timed through a 1-rank DIST handle with
+    halo_push = 0, i.e. with the edge / interior split launches;
   * the Eq.7 max-allreduce of 32 B: ALLRED_US (default 20 us, NCCL on 8 GPUs of one NVSwitch
-    node) -- fully exposed: the ctrl kernel needs tau before the next step;
-  * the split into 3 launches (edge, edge, interior) + ctrl instead of 2: LAUNCH_US per extra
-    launch gap (default 3 us).
+    node) -- fully exposed: the ctrl kernel needs tau before the next step.
 
 Compares the paper's even Ny_dev split with the wet-count-balanced one."""
 import os, sys
@@ -34,7 +37,12 @@ w = wet_rows + 0.03 * n
 
 def strip_ms(j0, j1):
     f = synth.fill(c, j0, j1)
-    g = csph.csph_create(n, j1 - j0, c.dx, csph.params_from(c.params, tile_rows=TY))
+    if HALO == "push":  # a pushing rank launches its strip whole, as a single grid does
+        g = csph.csph_create(n, j1 - j0, c.dx, csph.params_from(c.params, tile_rows=TY))
+    else:  # the send/recv rank's split launches (edge tile rows, interior), NCCL at 1 rank
+        g = csph.csph_create_dist_rows(n, j1 - j0, c.dx,
+                                       csph.params_from(c.params, tile_rows=TY, halo_push=0),
+                                       0, 1, [0, j1 - j0], 0, csph.csph_make_nccl_id())
     g.set_state(*f)
     g.step(4)  # even: the timed steps start at parity 0, whose pair graph is captured here
     torch.cuda.synchronize()
@@ -52,15 +60,19 @@ def strip_ms(j0, j1):
 HALO_GBS = float(os.environ.get("HALO_GBS", "300"))
 HALO_US = float(os.environ.get("HALO_US", "15"))
 ALLRED_US = float(os.environ.get("ALLRED_US", "20"))
-LAUNCH_US = float(os.environ.get("LAUNCH_US", "3"))
 pitch = ((n + 4 + 3 + 4) + 31) // 32 * 32
+
+
+HALO = os.environ.get("HALO", "push")
 
 
 def comm_ms(rows, t_strip):
     """Exposed communication per step of a strip of `rows` rows (see the module doc)."""
+    if HALO == "push":
+        return ALLRED_US * 1e-3
     halo = 2 * 3 * 4 * pitch * 8 / (HALO_GBS * 1e9) * 1e3 + HALO_US * 1e-3
     interior = t_strip * max(0.0, 1.0 - 2 * 128 / rows)  # the interior launch's share
-    return max(0.0, halo - interior) + ALLRED_US * 1e-3 + 2 * LAUNCH_US * 1e-3
+    return max(0.0, halo - interior) + ALLRED_US * 1e-3  # (the split launches are timed)
 
 
 t1 = strip_ms(0, c.ny)
