@@ -297,8 +297,17 @@ def run_ours(a, rank, world, local):
             blobs = [torch.empty_like(blob) for _ in range(world)]
             dist.all_gather(blobs, blob)
             nb = [bytes(x.cpu().numpy().tobytes()) for x in blobs]
-            g.ipc_link(nb[rank - 1] if rank > 0 else None,
-                       nb[rank + 1] if rank < world - 1 else None)
+            ok = torch.ones(1, device="cuda")
+            try:
+                g.ipc_link(nb[rank - 1] if rank > 0 else None,
+                           nb[rank + 1] if rank < world - 1 else None)
+            except csph.CsphError as e:
+                print(f"rank {rank}: halo push unavailable ({e}); NCCL halos", file=sys.stderr)
+                ok.zero_()
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() < 1:  # one transport for all ranks
+                g.ipc_link(None, None)
+                a.halo = "nccl"
     else:
         g = csph.csph_create(c.nx, c.ny, c.dx, p)
     stream = torch.cuda.current_stream()

@@ -232,9 +232,11 @@ csph_t*     csph_create_dist_rows(int nx, int ny, double dx, const csph_params* 
  * following steps push halos from inside the kernel instead of send/recv.  Collective in
  * effect (every rank must link before the next step).  CSPH_EINVAL for a non-DIST handle,
  * missing / extra blobs or a blob that is not the neighbour's strip (geometry checked),
- * CSPH_ECUDA if a handle cannot be opened (e.g. no peer access: call it again with
- * params.halo_push = 0 semantics by not linking -- the handle keeps send/recv).  A 1-rank
- * handle needs no link.  csph_rebalance_rows drops the links (new buffers): link again. */
+ * CSPH_ECUDA if a handle cannot be opened (e.g. no peer access; the handle then keeps
+ * send/recv).  csph_ipc_link(h, NULL, NULL) on a multi-rank handle drops the links (back to
+ * send/recv): every rank must use the same transport, so a harness whose link failed on some
+ * rank unlinks on all.  A 1-rank handle needs no link.  csph_rebalance_rows drops the links
+ * (new buffers): link again. */
 int         csph_ipc_blob_bytes(void);
 int         csph_ipc_export(csph_t*, void* out);
 int         csph_ipc_link(csph_t*, const void* lo_blob, const void* hi_blob);

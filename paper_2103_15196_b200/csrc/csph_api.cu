@@ -1097,6 +1097,12 @@ int csph_ipc_export(csph_t* H, void* out) {
 int csph_ipc_link(csph_t* H, const void* lo, const void* hi) {
   if (!H) return fail(CSPH_EINVAL, "handle is NULL");
   if (H->mode != DIST) return fail(CSPH_EINVAL, "csph_ipc_link needs a DIST handle");
+  if (!lo && !hi && H->nranks > 1) {  // unlink: back to send/recv halos
+    CK(cudaSetDevice(H->s[0].dev));
+    graphs_reset(H);
+    ipc_unlink(H);
+    return CSPH_OK;
+  }
   if ((H->rank > 0) != (lo != nullptr) || (H->rank < H->nranks - 1) != (hi != nullptr))
     return fail(CSPH_EINVAL, "csph_ipc_link: give exactly the neighbours' blobs (rank %d of %d)",
                 H->rank, H->nranks);

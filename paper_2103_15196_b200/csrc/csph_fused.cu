@@ -32,6 +32,9 @@ constexpr int kUnroll = CSPH_UNROLL;  // y-march unroll of the fp64 hot speciali
 #endif
 constexpr int kMinB32 = CSPH_MINB32;  // resident CTAs per SM of the fp32 instance
 
+#ifndef CSPH_PUSH
+#define CSPH_PUSH 1  // development knob: halo push code compiled out (A/B)
+#endif
 #ifndef CSPH_YFAST
 #define CSPH_YFAST true
 #endif
@@ -234,6 +237,38 @@ __global__ void __launch_bounds__(NT, MINB)
     if (tr == 0 && S.ngflag[0]) S.ngflag[0][g + hg.ntx] = (unsigned char)m;
     if (tr == hg.nty - 1 && S.ngflag[1]) S.ngflag[1][g] = (unsigned char)m;
   };
+  // ... and its rows 0..2 / ny-3..ny-1 into the neighbour's ghost rows: once the tile is done
+  // (callers sit behind a barrier), the tile copies them -- with the x-ghost columns the first
+  // and last tile columns wrote -- from its output buffer, outside the march's hot loop
+  auto push_rows = [&]() {
+    if constexpr (CSPH_PUSH) {
+      const int q = par ^ 1;
+      const int c0 = bx == 0 ? -GX : bx * TX;
+      const int c1 = bx * TX + TX >= S.nx ? S.nx + GY : bx * TX + TX;
+      const T* src[4] = {tp(q ? S.H[1] : S.H[0]), tp(q ? S.Qx[1] : S.Qx[0]),
+                         tp(q ? S.Qy[1] : S.Qy[0]), tp(q ? S.b[1] : S.b[0])};
+      bool pushed = false;
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        if (!S.nH[side][q]) continue;
+        const int ja = side == 0 ? y0 : max(y0, S.ny - GY);
+        const int jb = side == 0 ? min(y1, GY) : y1;
+        if (ja >= jb) continue;
+        T* dst[4] = {tp(S.nH[side][q]), tp(S.nQx[side][q]), tp(S.nQy[side][q]),
+                     tp(S.nb[side][q])};
+        for (int j = ja; j < jb; ++j)
+          for (int c = c0 + (int)threadIdx.x; c < c1; c += NT) {
+            const size_t o = off(S.pitch, c, j);
+            const long long r = (long long)o + S.ndel[side];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) dst[f][r] = src[f][o];
+          }
+        pushed = true;
+      }
+      if (pushed || ((tr == 0 || tr == hg.nty - 1) && (S.ngflag[0] || S.ngflag[1])))
+        __threadfence_system();  // visible to the peer before this grid completes
+    }
+  };
   // across an interior strip edge the facing tile row is the neighbouring strip's, whose
   // flags arrive with the halo rows (hg.glo / hg.ghi); without them such a tile marches
   if (hg.enable && (S.wall_lo || y0 > 0 || hg.glo) && (S.wall_hi || y1 < S.ny || hg.ghi)) {
@@ -269,8 +304,6 @@ __global__ void __launch_bounds__(NT, MINB)
               write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
             else
               write_wall_ghosts_t(S, oH, oQx, oQy, ob, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
-            if (j < GY || j >= S.ny - GY)
-              push_halo_cell(S, par ^ 1, col, j, Hn, Qn, Qn, bn, feeds_xghost(S, col));
           }
         }
         const bool any = __syncthreads_or(cwet);
@@ -281,7 +314,7 @@ __global__ void __launch_bounds__(NT, MINB)
           push_flags(any ? HGS_ALL : 0);
           atomicAdd(&hg.stats[1], 1ull);
         }
-        if (tr == 0 || tr == hg.nty - 1) __threadfence_system();  // pushed rows and flags
+        push_rows();  // after __syncthreads_or: every thread's rows are written
         // a cell made wet by a source has Q' = +0: its Eq.7 terms are those of a
         // still wet cell
         if (cwet) {
@@ -385,7 +418,6 @@ __global__ void __launch_bounds__(NT, MINB)
       write_with_ghosts(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
     else
       write_wall_ghosts_t(S, oH, oQx, oQy, ob, col, j, Hn, Qxn, Qyn, bn, colg);
-    if (j < GY || j >= S.ny - GY) push_halo_cell(S, par ^ 1, col, j, Hn, Qxn, Qyn, bn, colg);
     if (wet) {
       T t1, t2, t3;
       dt_terms_t<GEN>(Q, Hn, Qxn, Qyn, W3, aj_at(off(pitch, col, j), Hn),
@@ -685,7 +717,7 @@ __global__ void __launch_bounds__(NT, MINB)
     hg.tstate[ti] = 0;
     push_flags(m);
   }
-  if (tr == 0 || tr == hg.nty - 1) __threadfence_system();  // pushed rows: visible to peers
+  push_rows();  // after the barrier above: every thread's rows are written
   if (t == 0 && hg.cost) hg.cost[ti] = (unsigned short)min(nfull, 65535);
   if (t == 0 && hg.stats) atomicAdd(&hg.stats[0], 1ull);
   if (t < 3) {

@@ -140,35 +140,6 @@ __device__ __forceinline__ void dt_terms_t(const PT<T>& P, T H, T Qx, T Qy, T W,
   t3 = gate ? ((A * pow_m_t<GEN>(P.m_grass, P.m_real, s2, a)) * a) * W : T(0);
 }
 
-// Halo push of an updated cell of rows 0..2 / ny-3..ny-1: the same values into
-// the neighbour's ghost row (buffer q), with the x-ghosts the cell feeds (walls mirror with
-// the normal momentum negated, open edges copy: the neighbour's ghost rows carry x-ghosts).
-template <typename T>
-__device__ __forceinline__ void push_halo_cell(const StripView& S, int q, int col, int j, T Hn,
-                                               T Qxn, T Qyn, T bn, bool gx) {
-#pragma unroll
-  for (int side = 0; side < 2; ++side) {
-    if (side == 0 ? j >= GY : j < S.ny - GY) continue;
-    if (!S.nH[side][q]) continue;
-    T* H = reinterpret_cast<T*>(S.nH[side][q]);
-    T* Qx = reinterpret_cast<T*>(S.nQx[side][q]);
-    T* Qy = reinterpret_cast<T*>(S.nQy[side][q]);
-    T* b = reinterpret_cast<T*>(S.nb[side][q]);
-    const long long d = S.ndel[side];
-    const long long o = (long long)off(S.pitch, col, j) + d;
-    H[o] = Hn; Qx[o] = Qxn; Qy[o] = Qyn; b[o] = bn;
-    if (gx) {
-      int tg[7];
-      bool ng[7];
-      const int c = ghost_targets(col, S.nx, S.bc_xlo, S.bc_xhi, tg, ng);
-      for (int a = 1; a < c; ++a) {
-        const long long g = (long long)off(S.pitch, tg[a], j) + d;
-        H[g] = Hn; Qx[g] = ng[a] ? -Qxn : Qxn; Qy[g] = Qyn; b[g] = bn;
-      }
-    }
-  }
-}
-
 // Wall-only ghost writer (the hot-path specialisation), generic in T.
 template <typename T>
 __device__ __forceinline__ void write_wall_ghosts_t(const StripView& S, T* oH, T* oQx, T* oQy,
