@@ -1543,7 +1543,8 @@ static int choose_tile_rows(csph* H, Strip& s, int buf = 0) {
   CK(cudaStreamSynchronize(s.st));
   const long long want = 5LL * 3 * s.nsm / 2;
   int pick = 0;
-  for (int ty = 128; ty >= kTyMin; ty /= 2) {
+  static const int kTys[] = {192, 128, 64, 32, 16};  // with the costliest-first order (7.5)
+  for (int ty : kTys) {
     const int f = ty / kTyMin, nty = (s.v.ny + ty - 1) / ty;
     if ((long long)nty * s.ntx > 40000) break;  // finer tilings only add skipped-CTA overhead
     long long wet = 0;
