@@ -33,7 +33,7 @@ if os.environ.get("C34"):
     cases += [("C3", 4096, lambda: synth.fill(c3), c3.params), ("C4", 8192, lambda: synth.fill(c4), c4.params)]
 for name, nn, ff, p in cases:
     f = ff()
-    g = csph.csph_create(nn, nn, 1.0, csph.params_from(p))
+    g = csph.csph_create(nn, nn, 1.0, csph.params_from(p, precision=int(os.environ.get("PREC", "64"))))
     g.set_state(*f)
     del f
     g.step(3); torch.cuda.synchronize()
