@@ -104,14 +104,12 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def ncu_traffic(kernel_substr: str):
+def ncu_traffic(key: str):
     """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         d = json.load(open(p))
-        for k, v in d.get("kernels", {}).items():
-            if kernel_substr in k:
-                return v
+        return d.get("kernels", {}).get(key)
     except Exception:
         pass
     return None
@@ -376,7 +374,9 @@ def run_ours(a, rank, world, local):
     bpc_copy = ((3 if psi_field else 2) + 4) * es
     bytes_per_step = own_cells * (bpc * f_march + bpc_copy * f_copy)
     achieved = bytes_per_step / (kern_ms_per / 1e3) / 1e9
-    tr = ncu_traffic("fused_step_kernel" if path == csph.CSPH_PATH_FUSED else "k7_fluxes")
+    # the committed capture of the same kernel and precision (fp32: its own entry, else none)
+    tr = ncu_traffic(("fused_step_kernel" + ("" if a.precision == 64 else "_fp32"))
+                     if path == csph.CSPH_PATH_FUSED else "k7_fluxes")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": (tr or {}).get("dram_bytes_per_launch"),
             "kernel": "fused_step_kernel" if path == csph.CSPH_PATH_FUSED else "staged K1..K8",
