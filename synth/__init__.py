@@ -71,6 +71,7 @@ def config(name: str, n: int | None = None, ny: int | None = None) -> Config:
         "C2N": Config("C2N", 2, 1024, 1024, variant=1, params=dict(_PHYS_ON)),
         "C3": Config("C3", 3, 4096, 4096, params=dict(_PHYS_ON, n_manning=0.025)),
         "C4": Config("C4", 4, 8192, 8192, params=dict(_PHYS_ON)),
+        "C4D": Config("C4D", 4, 8192, 8192, variant=1, params=dict(_PHYS_ON)),
         "C5": Config("C5", 5, 16384, 16384, params=dict(_PHYS_ON)),
     }[name]
     if n is not None:

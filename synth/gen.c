@@ -101,7 +101,7 @@ static int64_t scl(int64_t v, int64_t n, int64_t ref) { return (v * n + ref / 2)
  *   cfg 1: C1 dam break 1D-like (flat bed, H=1 | 0), variant 1 = Stoker (1 | 0.1)
  *   cfg 2: C2 lake at rest over rough terrain (variant 0 dyadic, 1 non-dyadic)
  *   cfg 3: C3 dam break over an erodible bed, dam with a breach
- *   cfg 4: C4 valley with dam across rows and a channel
+ *   cfg 4: C4 valley with dam across rows and a channel; variant 1 = C4D, the dam breached
  *   cfg 5: C5 river-floodplain flood, heterogeneous psi
  * Features are laid out on the reference sizes (C2 1024, C3 4096, C4 8192,
  * C5 16384) and scaled proportionally to the requested nx, ny.
@@ -161,7 +161,10 @@ int syn_fill(int cfg, int variant, int64_t nx, int64_t ny, int64_t j0, int64_t j
             0.2 * F[i];
         int64_t d0 = scl(1016, ny, 8192), d1 = scl(1024, ny, 8192);
         if (d1 <= d0) d1 = d0 + 1;
-        if (j >= d0 && j < d1 && !inch) B = 12.0;
+        /* variant 1 (C4D): the dam has failed over a 1536 m breach around the channel at
+         * t = 0 -- the reservoir floods the valley floor downstream (moving fronts) */
+        const int breach = variant == 1 && fabs((double)i - xc) < 768.0 * s;
+        if (j >= d0 && j < d1 && !inch && !breach) B = 12.0;
         if (j < d0) { H = 6.5 - B; if (H < 0.0) H = 0.0; }
         else if (inch) H = 1.0;
       } else {

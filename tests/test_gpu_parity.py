@@ -189,6 +189,33 @@ def test_hgs_tile_skipping_is_exact(cs, name, n, ny, steps):
         assert np.array_equal(a, b)
 
 
+def test_dam_breach_moving_fronts_vs_oracle(cs):
+    """C4D (the C4 valley with its dam breached over 1536 m at t = 0): the reservoir floods
+    the valley floor, so wet/dry fronts sweep through HGS tiles, the launch order's costs go
+    stale every step and fronts cross strip edges -- single grid and 3 pushing strips, 300
+    steps, bitwise the CPU oracle (state and dt log); the wet area grows by > 3 % of the grid."""
+    import oracle
+    c = synth.config("C4D", 192, 192)
+    f = synth.fill(c)
+    steps = 300
+    ref = oracle.Oracle(c.nx, c.ny, c.dx, oracle.Params(**c.params))
+    assert ref.set_state(*f) == 0
+    st, dt0, lim0 = ref.step(steps)
+    assert st == 0
+    rs = ref.get_state()
+    assert (rs[0] > 1e-6).mean() > (f[0] > 1e-6).mean() + 0.03
+    for g in (cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, tile_rows=16)),
+              cs.csph_create_multi_rows(c.nx, c.ny, c.dx, cs.params_from(c.params, tile_rows=16),
+                                        [0] * 3, [0, 50, 120, 192])):
+        g.set_state(*f)
+        g.step(steps)
+        dt, lim = g.get_dt_log(steps)
+        assert np.array_equal(dt, dt0) and np.array_equal(lim, lim0)
+        for a, r in zip(g.get_state(), rs):
+            assert np.array_equal(a, r)
+        g.destroy()
+
+
 def test_tile_launch_order_is_exact(cs):
     """The launch order: tiles run costliest first, by the previous step's
     costs, through the one-CTA counting sort -- here with more tiles than one sort chunk
