@@ -35,12 +35,6 @@ constexpr int kMinB32 = CSPH_MINB32;  // resident CTAs per SM of the fp32 instan
 #ifndef CSPH_PUSH
 #define CSPH_PUSH 1  // development knob: halo push code compiled out (A/B)
 #endif
-#ifndef CSPH_YFAST
-#define CSPH_YFAST true
-#endif
-#ifndef CSPH_XFAST
-#define CSPH_XFAST true
-#endif
 #ifndef CSPH_GUARD
 #define CSPH_GUARD 0
 #endif
@@ -119,7 +113,7 @@ enum { F_H = 0, F_QX = 1, F_QY = 2, F_B = 3, F_W = 4 };
 #ifndef CSPH_HLL_FAST
 #define CSPH_HLL_FAST 1
 #endif
-template <bool FASTP = true, typename T>
+template <typename T>
 __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T eta_p, T H_p,
                                        T un_p, T ut_p, bool off, T& F0, T& F1, T& F2) {
   const T bs = smax_t(eta_m - H_m, eta_p - H_p);
@@ -135,7 +129,7 @@ __device__ __forceinline__ void hll_bf(T g, T eta_m, T H_m, T un_m, T ut_m, T et
   const bool both = (wm & wp) != 0u;
   const T fl1 = mm * un_m, fl2 = mm * ut_m, fr1 = mp * un_p, fr2 = mp * ut_p;
   const T d0 = Hp - Hm, d1 = mp - mm, d2 = Hp * ut_p - Hm * ut_m;
-  if (CSPH_HLL_FAST && FASTP && __all_sync(0xffffffffu, both & !off)) {
+  if (CSPH_HLL_FAST && __all_sync(0xffffffffu, both & !off)) {
     // warp-uniform common case (both reconstructed sides wet, a face of a wet cell): R's
     // both-wet speeds without the dry-side selects; then, unless some lane is supercritical,
     // the HLL average without the upwind selects.  Same operations, same values.
@@ -592,7 +586,7 @@ __global__ void __launch_bounds__(NT, MINB)
       sy2[3] = minmod_t(ut2 - ut3, ut1 - ut2);
       if (ANYW(w3 || w2)) {
         const bool any = w3 || w2;
-        hll_bf<CSPH_YFAST>(Q.g, fma(T(0.5), sy3[0], eta3), fma(T(0.5), sy3[1], H3), fma(T(0.5), sy3[2], vt3),
+        hll_bf(Q.g, fma(T(0.5), sy3[0], eta3), fma(T(0.5), sy3[1], H3), fma(T(0.5), sy3[2], vt3),
                  fma(T(0.5), sy3[3], ut3), fma(T(-0.5), sy2[0], eta2), fma(T(-0.5), sy2[1], H2),
                  fma(T(-0.5), sy2[2], vt2), fma(T(-0.5), sy2[3], ut2), !any,
                  Gn[0], Gn[2], Gn[1]);  // normal momentum of a y-face -> Qy, tangential -> Qx
@@ -641,7 +635,7 @@ __global__ void __launch_bounds__(NT, MINB)
           const T eR = HR + bR;
           const T uR = X2(1, 1), vR = X2(2, 1);
           // own slopes sigma_x of row L-1: the exchange row written in phase C
-          hll_bf<CSPH_XFAST>(Q.g, fma(T(0.5), XG(sm.X3[1], 0), eta1), fma(T(0.5), XG(sm.X3[2], 0), H1),
+          hll_bf(Q.g, fma(T(0.5), XG(sm.X3[1], 0), eta1), fma(T(0.5), XG(sm.X3[2], 0), H1),
                    fma(T(0.5), XG(sm.X3[3], 0), ut1), fma(T(0.5), XG(sm.X3[4], 0), vt1),
                    fma(T(-0.5), XG(sm.X3[1], 1), eR), fma(T(-0.5), XG(sm.X3[2], 1), HR),
                    fma(T(-0.5), XG(sm.X3[3], 1), uR), fma(T(-0.5), XG(sm.X3[4], 1), vR), !any,
