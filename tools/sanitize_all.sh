@@ -1,6 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 for tool in memcheck racecheck synccheck initcheck; do
-  for case in fused general staged strips fp32 tiles; do
+  for case in fused general staged strips fp32 tiles; do  # every kernel family
     extra=""
     [ $tool = memcheck ] && extra="--leak-check no"
     [ $tool = racecheck ] && extra="--racecheck-report hazard"

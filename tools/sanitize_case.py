@@ -6,8 +6,8 @@
 Cases (each a few steps on a small grid, so that racecheck's ~100x slowdown stays in
 seconds): fused (hot-path specialisation, HGS on, CUDA-graph replay and a profiled plain
 launch), general (the NEXT-3/4 instance: open edges, n_M/beta/src fields, Eq.4 A_J, m = 3),
-staged (the K1..K8 kernels + mirrors), strips (3 uneven strips, overlapped edge / halo /
-interior launches with 16-row tiles), fp32 (the NEXT-2 instance), tiles (every tile height
+staged (the K1..K8 kernels + mirrors), strips (3 uneven strips with 16-row tiles: halos pushed
+by the step kernel, then overlapped edge / peer-copy halo / interior launches), fp32 (the NEXT-2 instance), tiles (every tile height
 with a ragged last tile column and row).  Every case also checks its result against a
 reference (the single grid or the fused path) so a sanitizer run is also a parity run.
 No torch import: only the ctypes binding and numpy.
@@ -81,10 +81,12 @@ def main():
         g = csph.csph_create(c.nx, c.ny, c.dx, csph.params_from(P))
         r1 = run(g, f, 5)
         g.destroy()
-        m = csph.csph_create_multi_rows(c.nx, c.ny, c.dx, csph.params_from(P, tile_rows=16),
-                                        [0, 0, 0], [0, 49, 98, c.ny])
-        same(r1, run(m, f, 5))
-        m.destroy()
+        for push in (1, 0):  # halos pushed by the kernel / peer copies after the edge rows
+            m = csph.csph_create_multi_rows(c.nx, c.ny, c.dx,
+                                            csph.params_from(P, tile_rows=16, halo_push=push),
+                                            [0, 0, 0], [0, 49, 98, c.ny])
+            same(r1, run(m, f, 5))
+            m.destroy()
     elif a.case == "fp32":
         g = csph.csph_create(c.nx, c.ny, c.dx, csph.params_from(P, precision=32, tile_rows=32))
         d, st = run(g, f, 5)
