@@ -54,11 +54,13 @@ def test_gpu_arm_json_line():
 
 
 @pytest.mark.gpu
-def test_gpu_arm_dist_path_under_torchrun():
+@pytest.mark.parametrize("halo", ["push", "nccl"])
+def test_gpu_arm_dist_path_under_torchrun(halo):
     """The multi-GPU code path of bench.py end to end with one rank under torchrun
     (DESIGN.md 9): torch.distributed NCCL group, the all-gathered balanced bounds, the
-    NCCL-id broadcast, csph_create_dist_rows, the split launches + halo exchange + max
-    allreduce of every step, and the e2e leg through csph_set_state_rows/get_state_rows."""
+    NCCL-id broadcast, csph_create_dist_rows, the steps of either halo transport (push: the
+    strip launched whole; nccl: the split launches + send/recv on the comm stream) with the
+    max allreduce, and the e2e leg through csph_set_state_rows/get_state_rows."""
     import socket
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
@@ -67,14 +69,15 @@ def test_gpu_arm_dist_path_under_torchrun():
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "bench.py"), "--dist", "--config", "C5", "--grid-n", "1024",
            "--steps", "4", "--warmup", "3", "--repeats", "1", "--no-cpu-baseline",
-           "--e2e-steps", "4", "--tile-rows", "64"]
+           "--e2e-steps", "4", "--tile-rows", "64", "--halo", halo]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     d = json.loads([l for l in r.stdout.splitlines() if l.strip().startswith("{")][-1])
     assert d["value"] > 0 and d["n_gpus"] == 1
     assert d["config"]["partition"]["bounds"] == [0, 1024]
     assert d["config"]["parallelism"].startswith("row strips")
-    # per step (one rank: no neighbour, the strip is launched whole): the tile-order sort,
-    # the step kernel, ctrl
-    assert d["gpu_launches"] == 4 * 3
+    # per step: the tile-order sort, ctrl and the step kernel -- one rank has no neighbour,
+    # so a pushing rank launches its strip whole; the send/recv path launches the edge tile
+    # rows and the interior (16 tile rows of 64)
+    assert d["gpu_launches"] == 4 * (3 if halo == "push" else 5)
     assert d["e2e"]["value"] > 0
