@@ -288,8 +288,9 @@ def run_ours(a, rank, world, local):
         dist.broadcast(idt, 0)
         g = csph.csph_create_dist_rows(c.nx, c.ny, c.dx, p, rank, world, bounds, local,
                                        bytes(idt.cpu().numpy().tobytes()))
-        # halo push: every rank maps its neighbours' buffers through CUDA IPC,
-        # so the step kernels write the ghost rows over NVLink (no send/recv, no edge split)
+        # peer memory: every rank maps the others' buffers through CUDA IPC, so
+        # the step kernels write the ghost rows and the ctrl kernels combine the Eq.7 maxima
+        # over NVLink (no send/recv, no edge split, no allreduce)
         if a.halo == "push" and world > 1:
             blob = torch.frombuffer(bytearray(g.ipc_export()), dtype=torch.uint8).cuda()
             blobs = [torch.empty_like(blob) for _ in range(world)]
@@ -297,14 +298,13 @@ def run_ours(a, rank, world, local):
             nb = [bytes(x.cpu().numpy().tobytes()) for x in blobs]
             ok = torch.ones(1, device="cuda")
             try:
-                g.ipc_link(nb[rank - 1] if rank > 0 else None,
-                           nb[rank + 1] if rank < world - 1 else None)
+                g.ipc_link(nb)
             except csph.CsphError as e:
                 print(f"rank {rank}: halo push unavailable ({e}); NCCL halos", file=sys.stderr)
                 ok.zero_()
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if ok.item() < 1:  # one transport for all ranks
-                g.ipc_link(None, None)
+                g.ipc_link(None)
                 a.halo = "nccl"
     else:
         g = csph.csph_create(c.nx, c.ny, c.dx, p)

@@ -204,14 +204,14 @@ const char* csph_last_error(void);
 
 /* ---- multi-GPU: one process per GPU, row strips, NCCL over NVLink ------- */
 /* Rank 0 makes the NCCL unique id; the harness broadcasts it (e.g. through
- * torch.distributed) and every rank calls csph_create_dist with it.  The Eq.7 maxima (and
- * the negative-depth flag) are combined by ncclAllReduce(max), once per step.  Halo rows
- * (3 per side x 4 fields, no wrap-around, reading #18) and the facing HGS tile flags:
- *  - pushed by the step kernel itself into the neighbours' ghost rows over NVLink (peer
- *    stores from the K8 epilogue of the first / last tile row) once
- *    csph_ipc_link has mapped the neighbours' buffers (params.halo_push = 1, fused path);
- *  - otherwise ncclSend/ncclRecv to ranks r-1, r+1 after the edge tile rows, overlapped
- *    with the interior. */
+ * torch.distributed) and every rank calls csph_create_dist with it.  Once csph_ipc_link has
+ * mapped the other ranks' buffers (params.halo_push = 1, fused path) a step
+ * moves no data through NCCL: the step kernel's first / last tile rows write their 3 rows
+ * (4 fields) and HGS band flags straight into the neighbours' ghost rows over NVLink, and
+ * each rank's ctrl kernel publishes its Eq.7 maxima (and the negative-depth flag) into every
+ * rank's inbox and combines them (max).  Without the link: ncclSend/ncclRecv of the halo
+ * rows to ranks r-1, r+1 (no wrap-around, reading #18) after the edge tile rows, overlapped
+ * with the interior, and ncclAllReduce(max) of the maxima. */
 int         csph_nccl_id_bytes(void);
 int         csph_make_nccl_id(void* out);
 csph_t*     csph_create_dist(int nx, int ny, double dx, const csph_params* p,
@@ -224,22 +224,22 @@ csph_t*     csph_create_dist_rows(int nx, int ny, double dx, const csph_params* 
                                   int rank, int nranks, const int* bounds, int local_device,
                                   const void* nccl_id);
 
-/* DIST halo push.  csph_ipc_export writes csph_ipc_blob_bytes() bytes
- * describing this rank's state buffers and ghost tile-flag rows (CUDA IPC handles, strip
- * geometry) into out (host memory).  The harness all-gathers the blobs and every rank calls
- * csph_ipc_link with the blob of rank-1 (NULL on rank 0) and of rank+1 (NULL on the last
- * rank): the buffers are mapped (cudaIpcOpenMemHandle, peer access enabled lazily) and the
- * following steps push halos from inside the kernel instead of send/recv.  Collective in
- * effect (every rank must link before the next step).  CSPH_EINVAL for a non-DIST handle,
- * missing / extra blobs or a blob that is not the neighbour's strip (geometry checked),
- * CSPH_ECUDA if a handle cannot be opened (e.g. no peer access; the handle then keeps
- * send/recv).  csph_ipc_link(h, NULL, NULL) on a multi-rank handle drops the links (back to
- * send/recv): every rank must use the same transport, so a harness whose link failed on some
- * rank unlinks on all.  A 1-rank handle needs no link.  csph_rebalance_rows drops the links
- * (new buffers): link again. */
+/* DIST peer memory.  csph_ipc_export writes csph_ipc_blob_bytes() bytes
+ * describing this rank's state buffers, ghost tile-flag rows and combine inbox (CUDA IPC
+ * handles, strip geometry) into out (host memory).  The harness all-gathers the blobs and
+ * every rank calls csph_ipc_link with all of them (nblobs = nranks, rank order, one after the
+ * other in `blobs`): the neighbours' buffers and every rank's inbox are mapped
+ * (cudaIpcOpenMemHandle, peer access enabled lazily) and the following steps push halos from
+ * inside the kernel and combine the maxima in the ctrl kernels (see above).  Collective in
+ * effect: every rank must link before the next step.  CSPH_EINVAL for a non-DIST handle, a
+ * wrong count or a blob that is not rank r's strip (geometry checked), CSPH_ECUDA if a handle
+ * cannot be opened (e.g. no peer access; the handle then keeps NCCL).  csph_ipc_link(h, NULL,
+ * 0) drops the links (back to NCCL): every rank must use the same transport, so a harness
+ * whose link failed on some rank unlinks on all.  A 1-rank handle needs no link.
+ * csph_rebalance_rows drops the links (new buffers): link again. */
 int         csph_ipc_blob_bytes(void);
 int         csph_ipc_export(csph_t*, void* out);
-int         csph_ipc_link(csph_t*, const void* lo_blob, const void* hi_blob);
+int         csph_ipc_link(csph_t*, const void* blobs, int nblobs);
 
 /* Single-process row-strip decomposition: nstrips strips on the devices
  * listed in `devices` (strips may share a device), halos pushed by the step kernel into the

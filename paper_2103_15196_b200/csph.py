@@ -116,7 +116,7 @@ def lib():
         L.csph_rebalance_rows.argtypes = [_vp, _I]
         L.csph_ipc_blob_bytes.restype = ctypes.c_int
         L.csph_ipc_export.argtypes = [_vp, ctypes.c_void_p]
-        L.csph_ipc_link.argtypes = [_vp, ctypes.c_char_p, ctypes.c_char_p]
+        L.csph_ipc_link.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -298,9 +298,12 @@ class Csph:
         _check(lib().csph_ipc_export(self.h, buf), "csph_ipc_export")
         return buf.raw
 
-    def ipc_link(self, lo: bytes | None, hi: bytes | None):
-        """Map the neighbours' buffers for the halo push (csph_ipc_link; None on a global edge)."""
-        return _check(lib().csph_ipc_link(self.h, lo, hi), "csph_ipc_link")
+    def ipc_link(self, blobs: list[bytes] | None):
+        """Map every rank's buffers (csph_ipc_link: halo push and peer combine); all ranks'
+        blobs in rank order, or None to drop the links."""
+        if blobs is None:
+            return _check(lib().csph_ipc_link(self.h, None, 0), "csph_ipc_link")
+        return _check(lib().csph_ipc_link(self.h, b"".join(blobs), len(blobs)), "csph_ipc_link")
 
     def rebalance_rows(self, bounds):
         """Move to new strip bounds (collective for DIST; csph_rebalance_rows)."""

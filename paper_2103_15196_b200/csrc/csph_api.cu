@@ -129,6 +129,10 @@ struct Strip {
   cudaStream_t ost = nullptr;
   cudaEvent_t ev_ofork = nullptr, ev_ojoin = nullptr;
   bool osort_pending = false;
+  // peer combine: this strip's inbox [2][nranks][kInboxW] and the device array
+  // of every rank's inbox pointer (own device memory; nullptr until linked)
+  unsigned long long* inbox = nullptr;
+  unsigned long long** dpeers = nullptr;
   int ntx = 0, nty = 0;
   double* Wbuf = nullptr;            // device psi -> W field (when psi varies)
   float* Wbuf32 = nullptr;           // fp32 mode W field
@@ -164,6 +168,8 @@ struct csph {
   // halo push: every interior strip edge is linked (StripView nH.. ngflag), so
   // the split step launches each strip whole and moves no halo rows itself
   bool push = false;
+  // the Eq.7 maxima combined by the ctrl kernels over peer memory (no gather / allreduce)
+  bool p2p_combine = false;
   std::vector<void*> ipc_open;  // DIST: neighbour buffers opened through CUDA IPC
   bool profiling = false;
   std::vector<cudaEvent_t> evs;  // pairs around the main kernel of each step (strip 0)
@@ -198,9 +204,63 @@ namespace {
 
 constexpr int kTyMin = 16;  // finest automatic tiling (rows)
 
+// The combine of the Eq.7 maxima and the negative-depth flag over peer memory:
+// every strip / rank owns an inbox [2 slots][nranks][kInboxW] u64 that every other one can
+// store to (same process, peer access, or CUDA IPC); peers[r] = rank r's inbox.
+constexpr int kInboxW = 8;  // m0, m1, m2, neg, sequence number, pad
+struct PeerCombine {
+  unsigned long long* const* peers;  // [nranks] device array of inbox pointers, or nullptr
+  unsigned long long* inbox;         // this rank's inbox
+  int nranks, rank;
+};
+
+// Publish this rank's 4 partial maxima of the step just done into slot (step & 1) of every
+// rank's inbox -- the values, a system-scope fence, then the sequence number step + 1 -- and
+// wait until every rank's entry of that slot carries it; gM becomes the max over the ranks.
+// Two slots suffice: a rank can publish step n+2 only after every rank has published n+1,
+// which each does after its own read of step n.  Exact (u64 max of the bit patterns) and
+// independent of arrival order.  A peer silent for 10 s sets CSPH_ENCCL.
+__device__ int peer_combine(const PeerCombine& pc, unsigned long long* gM, long long step) {
+  const int slot = (int)(step & 1);
+  const unsigned long long seq = (unsigned long long)step + 1ull;
+  for (int r = 0; r < pc.nranks; ++r) {
+    unsigned long long* d = pc.peers[r] + ((size_t)slot * pc.nranks + pc.rank) * kInboxW;
+    for (int k = 0; k < 4; ++k) d[k] = gM[k];
+  }
+  __threadfence_system();
+  for (int r = 0; r < pc.nranks; ++r) {
+    volatile unsigned long long* d =
+        pc.peers[r] + ((size_t)slot * pc.nranks + pc.rank) * kInboxW;
+    d[4] = seq;
+  }
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned long long m[4] = {0, 0, 0, 0};
+  for (int r = 0; r < pc.nranks; ++r) {
+    volatile unsigned long long* e = pc.inbox + ((size_t)slot * pc.nranks + r) * kInboxW;
+    while (e[4] != seq) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) return CSPH_ENCCL;
+      __nanosleep(100);
+    }
+    __threadfence_system();
+    for (int k = 0; k < 4; ++k) m[k] = e[k] > m[k] ? e[k] : m[k];
+  }
+  for (int k = 0; k < 4; ++k) gM[k] = m[k];
+  return 0;
+}
+
 __global__ void ctrl_kernel(Ctrl* C, unsigned long long* gM, double* Mlast, double* dtlog,
-                            int* limlog, Phys P, int advance) {
+                            int* limlog, Phys P, int advance, PeerCombine pc = PeerCombine{}) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (advance && pc.peers && C->status == 0) {
+    const int e = peer_combine(pc, gM, C->step);
+    if (e) {
+      C->status = e;
+      return;
+    }
+  }
   if (advance) {
     if (C->status == 0) {
       C->parity ^= 1;
@@ -906,11 +966,44 @@ static void push_side(StripView& v, int side, double* const Hs[2], double* const
   v.ngflag[side] = gflag;
 }
 
+// The peer combine's inbox of a strip for nranks ranks (zeroed) and its device array of the
+// ranks' inbox pointers (peers[r], host array of nranks).
+static int combine_alloc(Strip& s, int nranks) {
+  CK(cudaSetDevice(s.dev));
+  const size_t nb = 2 * (size_t)nranks * kInboxW * sizeof(unsigned long long);
+  int st;
+  if (!s.inbox) {
+    if ((st = dalloc(s, (void**)&s.inbox, nb))) return st;
+    if ((st = dalloc(s, (void**)&s.dpeers, (size_t)nranks * sizeof(void*)))) return st;
+  }
+  CK(cudaMemset(s.inbox, 0, nb));
+  return CSPH_OK;
+}
+
+static int combine_set_peers(Strip& s, const std::vector<unsigned long long*>& peers) {
+  CK(cudaSetDevice(s.dev));
+  CK(cudaMemcpy(s.dpeers, peers.data(), peers.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  return CSPH_OK;
+}
+
+// The ctrl kernel's combine arguments for strip r (none unless the peers are linked).
+static PeerCombine combine_of(const csph* H, const Strip& s, int r) {
+  PeerCombine pc{};
+  if (H->p2p_combine) {
+    pc.peers = s.dpeers;
+    pc.inbox = s.inbox;
+    pc.nranks = H->nranks;
+    pc.rank = r;
+  }
+  return pc;
+}
+
 // MULTI: strip r pushes its rows 0..2 into the upper ghost rows of strip r-1 and its rows
 // ny-3..ny-1 into the lower ghost rows of strip r+1 (same device, or peer access between
 // the devices); otherwise (or halo_push = 0, or the staged path) the peer copies stay.
 static void push_link_multi(csph* H) {
   H->push = false;
+  H->p2p_combine = false;
   for (auto& s : H->s) push_clear(s.v);
   const int n = (int)H->s.size();
   if (!H->p.halo_push || H->p.path != CSPH_PATH_FUSED) return;
@@ -939,6 +1032,15 @@ static void push_link_multi(csph* H) {
     }
   }
   H->push = true;
+  // and the maxima combined by the ctrl kernels through every strip's inbox
+  std::vector<unsigned long long*> peers;
+  for (auto& s : H->s) {
+    if (combine_alloc(s, n)) return;
+    peers.push_back(s.inbox);
+  }
+  for (auto& s : H->s)
+    if (combine_set_peers(s, peers)) return;
+  H->p2p_combine = true;
 }
 
 csph_t* csph_create_multi(int nx, int ny, double dx, const csph_params* p, int nstrips,
@@ -1057,9 +1159,10 @@ csph_t* csph_create_dist_rows(int nx, int ny, double dx, const csph_params* p, i
 
 namespace {
 struct IpcBlob {
-  int magic, rank, ny, pitch, ntx, prec;
+  int magic, rank, nranks, ny, pitch, ntx, prec;
   cudaIpcMemHandle_t f[4][2];  // H, Qx, Qy, b x parity
   cudaIpcMemHandle_t gflag;
+  cudaIpcMemHandle_t inbox;    // the peer combine's inbox
 };
 constexpr int kIpcMagic = 0x43535048;  // "CSPH"
 }  // namespace
@@ -1067,6 +1170,7 @@ constexpr int kIpcMagic = 0x43535048;  // "CSPH"
 static void ipc_unlink(csph* H) {
   for (void* p : H->ipc_open) cudaIpcCloseMemHandle(p);
   H->ipc_open.clear();
+  H->p2p_combine = false;
   for (auto& s : H->s) push_clear(s.v);
   H->push = H->mode == DIST && H->nranks == 1 && H->p.halo_push && H->p.path == CSPH_PATH_FUSED;
 }
@@ -1082,6 +1186,7 @@ int csph_ipc_export(csph_t* H, void* out) {
   memset(&b, 0, sizeof b);
   b.magic = kIpcMagic;
   b.rank = H->rank;
+  b.nranks = H->nranks;
   b.ny = s.v.ny;
   b.pitch = s.v.pitch;
   b.ntx = s.ntx;
@@ -1090,65 +1195,69 @@ int csph_ipc_export(csph_t* H, void* out) {
   for (int k = 0; k < 4; ++k)
     for (int q = 0; q < 2; ++q) CK(cudaIpcGetMemHandle(&b.f[k][q], F[k][q]));
   CK(cudaIpcGetMemHandle(&b.gflag, s.gflag));
+  int st;
+  if ((st = combine_alloc(s, H->nranks))) return st;
+  CK(cudaIpcGetMemHandle(&b.inbox, s.inbox));
   memcpy(out, &b, sizeof b);
   return CSPH_OK;
 }
 
-int csph_ipc_link(csph_t* H, const void* lo, const void* hi) {
+static int ipc_open(csph* H, const cudaIpcMemHandle_t& h, void** p) {
+  const cudaError_t e = cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(CSPH_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  H->ipc_open.push_back(*p);
+  return CSPH_OK;
+}
+
+int csph_ipc_link(csph_t* H, const void* blobs, int nblobs) {
   if (!H) return fail(CSPH_EINVAL, "handle is NULL");
   if (H->mode != DIST) return fail(CSPH_EINVAL, "csph_ipc_link needs a DIST handle");
-  if (!lo && !hi && H->nranks > 1) {  // unlink: back to send/recv halos
-    CK(cudaSetDevice(H->s[0].dev));
-    graphs_reset(H);
-    ipc_unlink(H);
-    return CSPH_OK;
-  }
-  if ((H->rank > 0) != (lo != nullptr) || (H->rank < H->nranks - 1) != (hi != nullptr))
-    return fail(CSPH_EINVAL, "csph_ipc_link: give exactly the neighbours' blobs (rank %d of %d)",
-                H->rank, H->nranks);
-  ipc_unlink(H);
-  if (!H->p.halo_push || H->p.path != CSPH_PATH_FUSED) return CSPH_OK;  // send/recv halos
   Strip& s = H->s[0];
   CK(cudaSetDevice(s.dev));
-  graphs_reset(H);  // captured steps bake in the halo transport
-  const void* blobs[2] = {lo, hi};
+  graphs_reset(H);  // captured steps bake in the transports
+  ipc_unlink(H);
+  if (!blobs && nblobs == 0) return CSPH_OK;  // unlink: send/recv halos, NCCL allreduce
+  if (!blobs || nblobs != H->nranks)
+    return fail(CSPH_EINVAL, "csph_ipc_link: give every rank's blob (%d), rank order", H->nranks);
+  if (!H->p.halo_push || H->p.path != CSPH_PATH_FUSED) return CSPH_OK;
+  std::vector<IpcBlob> B(nblobs);
+  for (int r = 0; r < nblobs; ++r) {
+    memcpy(&B[r], (const char*)blobs + (size_t)r * sizeof(IpcBlob), sizeof(IpcBlob));
+    const IpcBlob& b = B[r];
+    if (b.magic != kIpcMagic || b.rank != r || b.nranks != H->nranks || b.pitch != s.v.pitch ||
+        b.ntx != s.ntx || b.prec != s.v.prec || b.ny != H->bounds[r + 1] - H->bounds[r])
+      return fail(CSPH_EINVAL, "csph_ipc_link: blob %d is not rank %d's strip", r, r);
+  }
+  if (H->nranks == 1) return CSPH_OK;  // no neighbour, nothing to combine across
+  int st;
+  // halo push: the neighbours' state buffers and ghost-flag rows
   for (int side = 0; side < 2; ++side) {
-    if (!blobs[side]) continue;
-    IpcBlob b;
-    memcpy(&b, blobs[side], sizeof b);
-    const int want = H->rank + (side == 0 ? -1 : 1);
-    if (b.magic != kIpcMagic || b.rank != want || b.pitch != s.v.pitch || b.ntx != s.ntx ||
-        b.prec != s.v.prec || b.ny != H->bounds[want + 1] - H->bounds[want]) {
-      ipc_unlink(H);
-      return fail(CSPH_EINVAL, "csph_ipc_link: blob of side %d is not rank %d's strip", side, want);
-    }
+    const int o = H->rank + (side == 0 ? -1 : 1);
+    if (o < 0 || o >= H->nranks) continue;
     double* Fs[4][2];
-    unsigned char* gf = nullptr;
     for (int k = 0; k < 4; ++k)
       for (int q = 0; q < 2; ++q) {
         void* p = nullptr;
-        const cudaError_t e = cudaIpcOpenMemHandle(&p, b.f[k][q], cudaIpcMemLazyEnablePeerAccess);
-        if (e != cudaSuccess) {
-          ipc_unlink(H);
-          return fail(CSPH_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
-        }
-        H->ipc_open.push_back(p);
+        if ((st = ipc_open(H, B[o].f[k][q], &p))) { ipc_unlink(H); return st; }
         Fs[k][q] = (double*)p;
       }
-    {
-      void* p = nullptr;
-      const cudaError_t e = cudaIpcOpenMemHandle(&p, b.gflag, cudaIpcMemLazyEnablePeerAccess);
-      if (e != cudaSuccess) {
-        ipc_unlink(H);
-        return fail(CSPH_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
-      }
-      H->ipc_open.push_back(p);
-      gf = (unsigned char*)p;
-    }
-    const long long del = side == 0 ? (long long)b.ny * s.v.pitch : -(long long)s.v.ny * s.v.pitch;
-    push_side(s.v, side, Fs[0], Fs[1], Fs[2], Fs[3], gf, del);
+    void* gf = nullptr;
+    if ((st = ipc_open(H, B[o].gflag, &gf))) { ipc_unlink(H); return st; }
+    const long long del = side == 0 ? (long long)B[o].ny * s.v.pitch : -(long long)s.v.ny * s.v.pitch;
+    push_side(s.v, side, Fs[0], Fs[1], Fs[2], Fs[3], (unsigned char*)gf, del);
   }
+  // peer combine: every rank's inbox (mine is local memory)
+  if ((st = combine_alloc(s, H->nranks))) { ipc_unlink(H); return st; }
+  std::vector<unsigned long long*> peers(H->nranks, nullptr);
+  for (int r = 0; r < H->nranks; ++r) {
+    if (r == H->rank) { peers[r] = s.inbox; continue; }
+    void* p = nullptr;
+    if ((st = ipc_open(H, B[r].inbox, &p))) { ipc_unlink(H); return st; }
+    peers[r] = (unsigned long long*)p;
+  }
+  if ((st = combine_set_peers(s, peers))) { ipc_unlink(H); return st; }
   H->push = true;
+  H->p2p_combine = true;
   return CSPH_OK;
 }
 
@@ -1584,6 +1693,14 @@ int csph_set_state_rows(csph_t* H, int j_begin, int j_end, const double* h, cons
     launch_mirror(s.v, s.ctrl, 0, s.st, &H->launches);
     CK(cudaGetLastError());
   }
+  // a new run restarts the combine's sequence numbers: clear the inboxes (before the
+  // initial combine below, which no rank passes before every rank got here)
+  for (auto& s : H->s)
+    if (s.inbox) {
+      CK(cudaSetDevice(s.dev));
+      CK(cudaMemsetAsync(s.inbox, 0, 2 * (size_t)H->nranks * kInboxW * sizeof(unsigned long long),
+                         s.st));
+    }
   // maxima of the initial state, combined across strips / ranks
   for (auto& s : H->s) {
     CK(cudaSetDevice(s.dev));
@@ -1954,7 +2071,9 @@ static int push_step(csph* H, int n) {
     CK(cudaGetLastError());
     CK(cudaEventRecord(s.ev_int, s.st));
   }
-  if (H->mode == DIST) {
+  if (H->p2p_combine) {
+    // each ctrl kernel publishes its maxima to every rank's inbox and waits for all
+  } else if (H->mode == DIST) {
     Strip& s = H->s[0];
     CK(cudaStreamWaitEvent(s.cst, s.ev_int, 0));
     if ((st = allreduce_nccl(H, s.cst))) return st;
@@ -1963,9 +2082,11 @@ static int push_step(csph* H, int n) {
   } else if ((st = gather_multi(H, &Strip::ev_int))) {
     return st;
   }
-  for (auto& s : H->s) {
+  for (int r = 0; r < ns; ++r) {
+    Strip& s = H->s[r];
     CK(cudaSetDevice(s.dev));
-    ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 1);
+    ctrl_kernel<<<1, 1, 0, s.st>>>(s.ctrl, s.gM, s.Mlast, s.dtlog, s.limlog, H->P, 1,
+                                   combine_of(H, s, H->mode == DIST ? H->rank : r));
     H->launches += 1;
     CK(cudaGetLastError());
   }

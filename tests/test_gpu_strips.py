@@ -108,10 +108,13 @@ def test_dist_ipc_link_single_rank(cs):
                                  0, 1, [0, c.ny], 0, cs.csph_make_nccl_id())
     blob = g.ipc_export()
     assert len(blob) == cs.lib().csph_ipc_blob_bytes() and blob[:4] == b"HPSC"
-    g.ipc_link(None, None)
+    g.ipc_link([blob])
     with pytest.raises(cs.CsphError):
-        g.ipc_link(blob, None)  # rank 0 has no neighbour below
-    g.ipc_link(None, None)
+        g.ipc_link([blob, blob])  # one rank: one blob
+    with pytest.raises(cs.CsphError):
+        g.ipc_link([b"\0" * len(blob)])  # not a blob of this handle's geometry
+    g.ipc_link(None)
+    g.ipc_link([blob])
     g.set_state(*f)
     g.step(40)
     assert np.array_equal(g.get_dt_log(40)[0], dt0)
