@@ -11,8 +11,10 @@ time is the slowest strip plus the communication the step cannot hide, modelled 
     on the comm stream while the interior tile rows compute (only the excess over the
     interior launch is exposed); the strips are timed through a 1-rank DIST handle with
     halo_push = 0, i.e. with the edge / interior split launches;
-  * the Eq.7 max-allreduce of 32 B: ALLRED_US (default 20 us, NCCL on 8 GPUs of one NVSwitch
-    node) -- fully exposed: the ctrl kernel needs tau before the next step.
+  * the combine of the Eq.7 maxima, fully exposed (the ctrl kernel needs tau before the next
+    step): with HALO=push the ctrl kernels' peer combine -- 8 x 40 B of NVLink stores and a
+    flag poll, COMBINE_US (default 5 us); with HALO=nccl the 32 B max-allreduce, ALLRED_US
+    (default 20 us, NCCL on 8 GPUs of one NVSwitch node).
 
 Compares the paper's even Ny_dev split with the wet-count-balanced one."""
 import os, sys
@@ -60,6 +62,7 @@ def strip_ms(j0, j1):
 HALO_GBS = float(os.environ.get("HALO_GBS", "300"))
 HALO_US = float(os.environ.get("HALO_US", "15"))
 ALLRED_US = float(os.environ.get("ALLRED_US", "20"))
+COMBINE_US = float(os.environ.get("COMBINE_US", "5"))
 pitch = ((n + 4 + 3 + 4) + 31) // 32 * 32
 
 
@@ -69,7 +72,7 @@ HALO = os.environ.get("HALO", "push")
 def comm_ms(rows, t_strip):
     """Exposed communication per step of a strip of `rows` rows (see the module doc)."""
     if HALO == "push":
-        return ALLRED_US * 1e-3
+        return COMBINE_US * 1e-3
     halo = 2 * 3 * 4 * pitch * 8 / (HALO_GBS * 1e9) * 1e3 + HALO_US * 1e-3
     interior = t_strip * max(0.0, 1.0 - 2 * 128 / rows)  # the interior launch's share
     return max(0.0, halo - interior) + ALLRED_US * 1e-3  # (the split launches are timed)
