@@ -28,6 +28,7 @@ c = synth.config("C5")
 n = c.nx
 steps = int(os.environ.get("STEPS", "10"))
 REPS = int(os.environ.get("REPS", "3"))
+REBAL = int(os.environ.get("REBAL", "2"))  # measured-time re-balancing rounds
 TY = int(os.environ.get("TY", "0"))  # tile rows (0 = the library's auto rule)
 NS = [int(x) for x in os.environ.get("NS", "2,4,8").split(",")]
 KINDS = os.environ.get("KINDS", "even,balanced").split(",")
@@ -78,6 +79,16 @@ def comm_ms(rows, t_strip):
     return max(0.0, halo - interior) + ALLRED_US * 1e-3  # (the split launches are timed)
 
 
+def report(N, kind, b, ts):
+    tc = [t + comm_ms(b[r + 1] - b[r], t) for r, t in enumerate(ts)]
+    tN, tNc = max(ts), max(tc)
+    print(f"N={N} {kind:8s}: strips {[b[r + 1] - b[r] for r in range(N)]} ms "
+          f"{[round(x, 3) for x in ts]} -> {c.cells / tN / 1e6:.1f} Gcell/s, "
+          f"efficiency {t1 / (N * tN):.2f} (compute only); with modelled comm "
+          f"{tNc:.3f} ms -> {c.cells / tNc / 1e6:.1f} Gcell/s, efficiency "
+          f"{t1 / (N * tNc):.2f}", flush=True)
+
+
 t1 = strip_ms(0, c.ny)
 print(f"N=1: {t1:.3f} ms/step, {c.cells / t1 / 1e6:.1f} Gcell/s", flush=True)
 for N in NS:
@@ -85,10 +96,16 @@ for N in NS:
         b = ([csph.csph_strip_rows(c.ny, N, r)[0] for r in range(N)] + [c.ny]) if kind == "even" \
             else csph.csph_balance_rows(c.ny, N, w)
         ts = [strip_ms(b[r], b[r + 1]) for r in range(N)]
-        tc = [t + comm_ms(b[r + 1] - b[r], t) for r, t in enumerate(ts)]
-        tN, tNc = max(ts), max(tc)
-        print(f"N={N} {kind:8s}: strips {[b[r + 1] - b[r] for r in range(N)]} ms "
-              f"{[round(x, 3) for x in ts]} -> {c.cells / tN / 1e6:.1f} Gcell/s, "
-              f"efficiency {t1 / (N * tN):.2f} (compute only); with modelled comm "
-              f"{tNc:.3f} ms -> {c.cells / tNc / 1e6:.1f} Gcell/s, efficiency "
-              f"{t1 / (N * tNc):.2f}", flush=True)
+        report(N, kind, b, ts)
+        if kind != "balanced":
+            continue
+        # measured-time re-balancing: scale each strip's row weights by its
+        # measured step time over the mean, balance again, measure again
+        wm = w.copy()
+        for it in range(REBAL):
+            mean = sum(ts) / N
+            for r in range(N):
+                wm[b[r]:b[r + 1]] *= ts[r] / mean
+            b = csph.csph_balance_rows(c.ny, N, wm)
+            ts = [strip_ms(b[r], b[r + 1]) for r in range(N)]
+            report(N, f"measured{it + 1}", b, ts)
