@@ -149,6 +149,24 @@ int         csph_get_state(csph_t*, double* h, double* hu, double* hv, double* b
 int         csph_get_state_rows(csph_t*, int j_begin, int j_end, double* h, double* hu,
                                 double* hv, double* b);
 
+/* Asynchronous Save (the "Save" block: states are recorded every
+ * 100-1000 iterations, and CUDA streams separate the CPU<->GPU copies from the
+ * computation).  Snapshots the state as of the last completed step into a
+ * device buffer (dense fp64 [4][owned rows][nx], allocated on first use:
+ * 32 B per owned cell), then copies it to the caller's global-layout arrays
+ * [ny][nx] (owned rows only; any may be NULL) on a separate stream, and returns
+ * without waiting.  csph_step calls made afterwards run concurrently with that
+ * copy and do not change what it delivers.  The host arrays are the caller's
+ * and must stay valid and untouched until csph_save_wait; pinned (page-locked)
+ * arrays are needed for the copy to overlap the steps.  A second csph_save_begin
+ * before csph_save_wait is ordered after the first on the device.  Errors:
+ * CSPH_EINVAL (NULL handle), CSPH_ENOSTATE, CSPH_ENOMEM, CSPH_ECUDA. */
+int         csph_save_begin(csph_t*, double* h, double* hu, double* hv, double* b);
+
+/* Block until every csph_save_begin issued on this handle has landed in host
+ * memory.  CSPH_OK when none is pending. */
+int         csph_save_wait(csph_t*);
+
 /* Simulated time t = sum of tau, steps done, last tau. */
 int         csph_get_time(csph_t*, double* t, long long* steps_done, double* last_dt);
 

@@ -29,7 +29,8 @@ EXPORTS = [
     "csph_last_launch_count", "csph_profile", "csph_get_profile",
     "csph_selftest_math", "csph_get_tile_stats", "csph_reset_tile_stats",
     "csph_set_fields", "csph_set_fields_rows", "csph_row_weights", "csph_rebalance_rows",
-    "csph_ipc_blob_bytes", "csph_ipc_export", "csph_ipc_link",
+    "csph_ipc_blob_bytes", "csph_ipc_export", "csph_ipc_link", "csph_save_begin",
+    "csph_save_wait",
 ]
 
 
@@ -92,6 +93,8 @@ def lib():
         L.csph_set_fields_rows.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _D, _D, _D]
         L.csph_get_state.argtypes = [_vp, _D, _D, _D, _D]
         L.csph_get_state_rows.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D]
+        L.csph_save_begin.argtypes = [_vp, _D, _D, _D, _D]
+        L.csph_save_wait.argtypes = [_vp]
         L.csph_get_time.argtypes = [_vp, _D, ctypes.POINTER(ctypes.c_longlong), _D]
         L.csph_get_dt_log.argtypes = [_vp, _D, _I, ctypes.c_int, _I]
         L.csph_get_maxima.argtypes = [_vp, _D]
@@ -139,6 +142,14 @@ def _arr(a, shape):
     a = np.ascontiguousarray(a, dtype=np.float64)
     if a.shape != shape:
         raise ValueError(f"expected shape {shape}, got {a.shape}")
+    return a
+
+
+def _out(a, shape):
+    """An output array the library writes in place: no conversion copy is allowed."""
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+            and a.flags.writeable and a.shape == shape):
+        raise ValueError(f"expected a writable C-contiguous float64 array of shape {shape}")
     return a
 
 
@@ -241,6 +252,15 @@ class Csph:
         _check(lib().csph_get_state_rows(self.h, j_begin, j_end, *[_p(x) for x in out]),
                "csph_get_state_rows")
         return tuple(out)
+
+    def save_begin(self, h, hu, hv, b):
+        """Asynchronous Save into the caller's [ny][nx] float64 arrays (C-contiguous; pinned
+        for overlap, e.g. torch pin_memory().numpy()); they must stay alive until save_wait."""
+        outs = [x if x is None else _out(x, (self.ny, self.nx)) for x in (h, hu, hv, b)]
+        _check(lib().csph_save_begin(self.h, *[_p(x) for x in outs]), "csph_save_begin")
+
+    def save_wait(self):
+        _check(lib().csph_save_wait(self.h), "csph_save_wait")
 
     def get_time(self):
         t, n, d = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_double()

@@ -137,6 +137,12 @@ struct Strip {
   double* Wbuf = nullptr;            // device psi -> W field (when psi varies)
   float* Wbuf32 = nullptr;           // fp32 mode W field
   double* tmpd = nullptr;            // fp32 mode: fp64 staging for get_state
+  // asynchronous Save (csph_save_begin): dense fp64 snapshot [4][ny][nx] of the owned rows,
+  // copied to the host on its own stream `sst` while later steps run on `st`
+  double* snap = nullptr;
+  cudaStream_t sst = nullptr;
+  cudaEvent_t ev_snap = nullptr, ev_saved = nullptr;
+  bool save_issued = false;  // ev_saved recorded at least once
   double *cgbuf = nullptr, *betabuf = nullptr, *srcbuf = nullptr;  // NEXT-3 fields
   double* ajbuf = nullptr;  // NEXT-4: 0.05 n_M^3 field for Eq.4
   cudaStream_t st = nullptr;
@@ -719,6 +725,7 @@ static int strip_init(csph* H, Strip& s, int dev, int gj0, int rows, bool staged
 
 static void strip_free(Strip& s) {
   cudaSetDevice(s.dev);
+  if (s.sst) cudaStreamSynchronize(s.sst);  // a pending asynchronous Save reads s.snap
   if (s.ost) cudaStreamSynchronize(s.ost);
   if (s.st) cudaStreamSynchronize(s.st);
   for (void* p : s.allocs) cudaFree(p);
@@ -730,8 +737,14 @@ static void strip_free(Strip& s) {
     cudaStreamDestroy(s.cst);
   }
   if (s.ost) cudaStreamDestroy(s.ost);
-  for (cudaEvent_t e : {s.ev_edge, s.ev_int, s.ev_comm, s.ev_ofork, s.ev_ojoin})
+  if (s.sst) cudaStreamDestroy(s.sst);
+  for (cudaEvent_t e : {s.ev_edge, s.ev_int, s.ev_comm, s.ev_ofork, s.ev_ojoin, s.ev_snap,
+                        s.ev_saved})
     if (e) cudaEventDestroy(e);
+  s.sst = nullptr;
+  s.ev_snap = s.ev_saved = nullptr;
+  s.snap = nullptr;
+  s.save_issued = false;
   s.ost = nullptr;
   s.cst = nullptr;
   s.st = nullptr;
@@ -2248,6 +2261,78 @@ int csph_get_state_rows(csph_t* H, int j_begin, int j_end, double* h, double* hu
 int csph_get_state(csph_t* H, double* h, double* hu, double* hv, double* b) {
   if (!H) return fail(CSPH_EINVAL, "handle is NULL");
   return csph_get_state_rows(H, 0, H->ny, h, hu, hv, b);
+}
+
+// Asynchronous Save (the Save block records states every 100-1000 iterations,
+// CUDA streams separating the CPU<->GPU copies from the computation).  On the step stream:
+// wait until the previous Save has left the snapshot, then copy the owned rows of the state
+// (widened to fp64 in fp32 mode) into the dense snapshot; on the save stream: wait for that
+// copy, then move the snapshot to the caller's arrays.  Later csph_step calls run on the step
+// stream while the device->host copy drains, and never touch the snapshot.
+int csph_save_begin(csph_t* H, double* h, double* hu, double* hv, double* b) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  if (!H->have_state) return fail(CSPH_ENOSTATE, "no state");
+  double* dst[4] = {h, hu, hv, b};
+  for (auto& s : H->s) {
+    CK(cudaSetDevice(s.dev));
+    const StripView& v = s.v;
+    const size_t plane = (size_t)v.ny * H->nx;
+    if (!s.sst) {
+      CK(cudaStreamCreateWithFlags(&s.sst, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&s.ev_snap, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&s.ev_saved, cudaEventDisableTiming));
+    }
+    if (!s.snap) {
+      int st = dalloc(s, (void**)&s.snap, 4 * plane * 8);
+      if (st) return st;
+    }
+    const size_t ntot = (size_t)(v.ny + 2 * GY) * v.pitch;
+    if (v.prec == 4 && !s.tmpd) {
+      int st = dalloc(s, (void**)&s.tmpd, ntot * 8);
+      if (st) return st;
+    }
+    // the buffer holding the state: the ctrl block's parity once the launched steps are done
+    // (a frozen step, CSPH_ENEGDEPTH, does not flip it); the steps are complete on return
+    // from csph_step, so this read does not wait for device work
+    Ctrl c;
+    CK(cudaMemcpyAsync(&c, s.ctrl, sizeof c, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    const int p = c.parity;
+    const double* src[4] = {v.H[p], v.Qx[p], v.Qy[p], v.b[p]};
+    if (s.save_issued) CK(cudaStreamWaitEvent(s.st, s.ev_saved, 0));
+    for (int k = 0; k < 4; ++k) {
+      if (!dst[k]) continue;
+      const double* sk = src[k];
+      if (v.prec == 4) {
+        to_f64_kernel<<<(unsigned)((ntot + 255) / 256), 256, 0, s.st>>>(s.tmpd, (const float*)sk,
+                                                                         ntot);
+        CK(cudaGetLastError());
+        sk = s.tmpd;
+      }
+      CK(cudaMemcpy2DAsync(s.snap + k * plane, (size_t)H->nx * 8, sk + off(v.pitch, 0, 0),
+                           (size_t)v.pitch * 8, (size_t)H->nx * 8, v.ny,
+                           cudaMemcpyDeviceToDevice, s.st));
+    }
+    CK(cudaEventRecord(s.ev_snap, s.st));
+    CK(cudaStreamWaitEvent(s.sst, s.ev_snap, 0));
+    for (int k = 0; k < 4; ++k)
+      if (dst[k])
+        CK(cudaMemcpyAsync(dst[k] + (size_t)s.gj0 * H->nx,
+                           s.snap + k * plane, plane * 8, cudaMemcpyDeviceToHost, s.sst));
+    CK(cudaEventRecord(s.ev_saved, s.sst));
+    s.save_issued = true;
+  }
+  return CSPH_OK;
+}
+
+int csph_save_wait(csph_t* H) {
+  if (!H) return fail(CSPH_EINVAL, "handle is NULL");
+  for (auto& s : H->s) {
+    if (!s.sst) continue;
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.sst));
+  }
+  return CSPH_OK;
 }
 
 int csph_get_time(csph_t* H, double* t, long long* steps_done, double* last_dt) {
