@@ -195,6 +195,14 @@ def cpu_baseline(cfg_name, n, crop, steps):
             "host": host_info()}
 
 
+def workload_name(a, c, gen):
+    """The `config.workload` string both arms print for the same run."""
+    return ((f"{a.config} river-floodplain flood + sediment transport"
+             if a.config == "C5" else a.config)
+            + (f", rows [0, {c.ny}) of the {gen.nx}x{gen.ny} field (weak scaling, "
+               f"2048 rows per GPU)" if a.scaling == "weak" else ""))
+
+
 def run_reference(a, rank, world):
     if rank != 0:
         return
@@ -212,6 +220,10 @@ def run_reference(a, rank, world):
     st, dt, _ = o.step(a.steps)
     el = time.perf_counter() - t
     v = crop * crop * len(dt) / el / 1e9
+    cw = c  # our arm's domain: weak scaling runs rows [0, 2048 N) of the same field
+    if a.scaling == "weak":
+        cw = synth.Config(c.name, c.cfg, c.nx, min(c.ny, 2048 * world), c.dx, c.variant,
+                          dict(c.params))
     sample = (f"each step = one oracle step on the {crop}x{crop} centre crop of {a.config} "
               f"{c.nx}x{c.ny} (own walled domain), single thread")
     line = {
@@ -219,7 +231,11 @@ def run_reference(a, rank, world):
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": el / max(len(dt), 1) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{a.config} crop {crop}x{crop}", "grid": [crop, crop]},
+        # the same workload as our arm's line (each timed step a bounded sample of it: one
+        # oracle step on a centre crop, see cpu_baseline.sample)
+        "config": {"workload": workload_name(a, cw, c), "grid": [cw.nx, cw.ny],
+                   "cells": cw.nx * cw.ny, "dx_m": c.dx, "physics": c.params,
+                   "sample": f"{crop}x{crop} centre crop, own walled domain"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
                          "host": host_info()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -391,7 +407,11 @@ def run_ours(a, rank, world, local):
             # included -- bytes the launch did not have to move (reported beside, not as, the
             # achieved figure above)
             "dense_equivalent": {"achieved": own_cells * bpc / (kern_ms_per / 1e3) / 1e9,
-                                 "frac": own_cells * bpc / (kern_ms_per / 1e3) / 1e9 / peak}}
+                                 "frac": own_cells * bpc / (kern_ms_per / 1e3) / 1e9 / peak},
+            # report the binding roof.  The fp64 step is not HBM-bound: ncu puts
+            # DRAM at ~1.0x the algorithmic bytes and the fp64 pipe / issue slots ahead of it
+            # (DESIGN.md 8), so the binding roof is roofline_fp64 below, when present.
+            "binding_roof": "roofline_fp64" if a.precision == 64 else "issue (ALU)"}
     fp64 = None
     if tr and tr.get("fp64_inst_per_launch"):
         # fp64 pipe roof: 64 fp64 lanes/clk/SM x 148 SMs x the SM clock
@@ -468,10 +488,7 @@ def run_ours(a, rank, world, local):
             "scaling": a.scaling, "vs_baseline": None,
             "dtype": "f64" if a.precision == 64 else "f32", "data": "synthetic",
             "config": {
-                "workload": (f"{a.config} river-floodplain flood + sediment transport"
-                             if a.config == "C5" else a.config)
-                            + (f", rows [0, {c.ny}) of the {gen.nx}x{gen.ny} field (weak scaling, "
-                               f"2048 rows per GPU)" if a.scaling == "weak" else ""),
+                "workload": workload_name(a, c, gen),
                 "grid": [c.nx, c.ny], "cells": cells, "dx_m": c.dx, "wet_fraction": wet,
                 "psi": "field" if psi_field else "uniform", "physics": c.params,
                 "path": a.path, "parallelism": f"row strips x{world} ("

@@ -27,6 +27,9 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     assert d["cpu_baseline"]["host"]["nproc"] >= 1 and "cpu_model" in d["cpu_baseline"]["host"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    # the same workload as our arm's line (the crop is the per-step sample)
+    assert d["config"]["workload"] == "C2" and d["config"]["grid"] == [256, 256]
+    assert "96x96" in d["config"]["sample"]
 
 
 @pytest.mark.gpu
