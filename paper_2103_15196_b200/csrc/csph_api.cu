@@ -1663,7 +1663,7 @@ static int choose_tile_rows(csph* H, Strip& s, int buf = 0) {
   std::vector<unsigned char> w((size_t)s.ntx * nby);
   CK(cudaMemcpyAsync(w.data(), s.wetblk, w.size(), cudaMemcpyDeviceToHost, s.st));
   CK(cudaStreamSynchronize(s.st));
-  const long long want = 5LL * 3 * s.nsm / 2;
+  const long long want = 5LL * FUSED_MINB * s.nsm / 2;
   int pick = 0;
   static const int kTys[] = {192, 128, 64, 32, 16};  // with the costliest-first order (7.5)
   for (int ty : kTys) {

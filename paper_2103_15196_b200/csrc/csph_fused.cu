@@ -873,11 +873,10 @@ void launch_fused_step(const StripView& S, Ctrl* C, const Phys& P, unsigned long
   // 128 threads (120 output columns), an 8-row TMA ring prefetching 3 rows ahead,
   // 3 resident CTAs per SM in fp64 (5 in fp32: <= 102 registers, 89 used, no spills)
 #ifndef CSPH_RING
-#define CSPH_RING 8   // development knobs: ring slots, prefetch distance, CTAs per SM
+#define CSPH_RING 8   // development knobs: ring slots, prefetch distance
 #define CSPH_PF 3
-#define CSPH_MINB 3
 #endif
-  launch_v<128, CSPH_RING, CSPH_PF, CSPH_MINB>(S, C, P, gM, row0, row1, TY, hg, st);
+  launch_v<FUSED_NT, CSPH_RING, CSPH_PF, FUSED_MINB>(S, C, P, gM, row0, row1, TY, hg, st);
   *nlaunch += 1;
 }
 

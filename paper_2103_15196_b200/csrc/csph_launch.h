@@ -43,7 +43,15 @@ struct Hgs {
   unsigned short* cost;
 };
 
-constexpr int FUSED_TX = 120;  // output columns per CTA of the fused kernel (NT - 8)
+#ifndef CSPH_NT
+#define CSPH_NT 128   // threads per CTA of the fused kernel (development knob)
+#endif
+#ifndef CSPH_MINB
+#define CSPH_MINB 3   // resident fp64 CTAs per SM (development knob, with CSPH_NT)
+#endif
+constexpr int FUSED_NT = CSPH_NT;
+constexpr int FUSED_TX = CSPH_NT - 8;  // output columns per CTA of the fused kernel (NT - 8)
+constexpr int FUSED_MINB = CSPH_MINB;
 
 // Fused y-marching step (csph_fused.cu). Rows [row0, row1) of the strip; row0 must be
 // a multiple of tile_rows when HGS is enabled.
