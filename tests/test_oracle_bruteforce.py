@@ -36,7 +36,7 @@ def _params(**kw):
     return p
 
 
-def _random_case(seed, films=False, bc=None, fields=False, closures=False):
+def _random_case(seed, films=False, bc=None, fields=False, closures=False, spacing=False):
     """A tiny grid with moving water.  Cells are wet (H in [0.15, 1.2]), dry (H = 0) or,
     with films, thin films 0 < H < eps; velocities up to 1.2 m/s in any direction; the
     bed has steps of up to 0.5 m; psi in [0.3, 0.45]."""
@@ -59,6 +59,9 @@ def _random_case(seed, films=False, bc=None, fields=False, closures=False):
         prm.update(aj_mode=1, m_grass=int(rs.choice([1, 3, 4])), d50=2e-4)
         if rs.uniform() < 0.5:  # a real exponent through the pinned pow
             prm.update(m_real=float(rs.uniform(1.2, 3.8)))
+    if spacing:  # h != 1 (lambda = tau/h, Eq.7's h and h^2, the Eq.2 slope) and Eq.1's q+/q-
+        prm.update(_dx=float(rs.uniform(0.4, 3.0)), q_plus=float(rs.uniform(0.0, 2e-4)),
+                   q_minus=float(rs.uniform(0.0, 1e-4)))
     if bc is None:
         bc = (1, 1, 1, 1)
     fl = {}
@@ -68,8 +71,14 @@ def _random_case(seed, films=False, bc=None, fields=False, closures=False):
     return nx, ny, prm, (H, Qx, Qy, b, psi), bc, fl
 
 
+def _dx(prm):
+    """Grid spacing of a case (the "spacing" family draws one != 1; "_dx" is not a param)."""
+    return prm.get("_dx", 1.0), {k: v for k, v in prm.items() if k != "_dx"}
+
+
 def _oracle(orc, nx, ny, prm, st, bc, fl):
-    o = orc.Oracle(nx, ny, 1.0, orc.Params(**prm))
+    dx, prm = _dx(prm)
+    o = orc.Oracle(nx, ny, dx, orc.Params(**prm))
     o.set_walls(*bc)
     assert o.set_state(*st) == 0
     if fl:
@@ -80,7 +89,8 @@ def _oracle(orc, nx, ny, prm, st, bc, fl):
 def _brute(nx, ny, prm, st, bc, fl):
     H, Qx, Qy, b, psi = (a.tolist() for a in st)
     kw = {k: v.tolist() for k, v in fl.items()}
-    return BruteR(nx, ny, 1.0, prm, H, Qx, Qy, b, psi, bc=bc, **kw)
+    dx, prm = _dx(prm)
+    return BruteR(nx, ny, dx, prm, H, Qx, Qy, b, psi, bc=bc, **kw)
 
 
 def _err(state_o, state_b):
@@ -126,7 +136,8 @@ def _check(out):
 def _cases(kind, n, **kw):
     """Accepted cases of a family: seeds are drawn until n have every branch of R at
     least MARGIN away from its threshold over both steps."""
-    got, seed = [], 1000 * (1 + ["moving", "films", "open", "fields", "closures"].index(kind))
+    got, seed = [], 1000 * (1 + ["moving", "films", "open", "fields", "closures",
+                                 "spacing"].index(kind))
     while len(got) < n:
         seed += 1
         case = _random_case(seed, **kw)
@@ -146,6 +157,7 @@ def _cases(kind, n, **kw):
     ("open", {"bc": (2, 1, 1, 2)}),
     ("fields", {"fields": True}),
     ("closures", {"closures": True}),
+    ("spacing", {"spacing": True}),
 ])
 def test_oracle_matches_bruteforce_R(orc, kind, kw):
     """Two steps of R on random tiny grids with moving water."""

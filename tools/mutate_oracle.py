@@ -24,7 +24,8 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = "oracle/csph_oracle.c"
 PIN_TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_bruteforce.py",
-             "tests/test_next3_fields.py", "tests/test_next4_closures.py"]
+             "tests/test_next3_fields.py", "tests/test_next4_closures.py",
+             "tests/test_oracle_sweep_pins.py"]
 
 # (name, original text, mutated text)
 MUTATIONS = [
