@@ -129,3 +129,22 @@ def test_fp32_rejects_fp64_only_features(cs):
         cs.csph_create(16, 16, 1.0, cs.csph_default_params(precision=32, path=1))
     with pytest.raises(cs.CsphError):
         cs.csph_create(16, 16, 1.0, cs.csph_default_params(precision=32, open_bc=1))
+
+
+@pytest.mark.parametrize("dx", [0.37, 2.5])
+def test_fp32_bitwise_non_unit_spacing(cs, dx):
+    """The fp32 mode with h != 1 (lambda, c_P, Eq.7's h and h^2, the Eq.2 slope in binary32):
+    bitwise the binary32 oracle after 60 steps."""
+    c = synth.config("C5", 200, 180)
+    f = synth.fill(c)
+    ref = oracle.Oracle(c.nx, c.ny, dx, oracle.Params(**c.params), precision=32)
+    assert ref.set_state(*f) == 0
+    st, dt_ref, _ = ref.step(60)
+    assert st == 0
+    g = cs.csph_create(c.nx, c.ny, dx, cs.params_from(c.params, precision=32))
+    g.set_state(*f)
+    g.step(60)
+    assert np.array_equal(g.get_dt_log(60)[0], dt_ref)
+    for a, r in zip(g.get_state(), ref.get_state()):
+        assert np.array_equal(a, r)
+    g.destroy()

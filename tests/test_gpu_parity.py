@@ -344,8 +344,8 @@ def test_tilings_are_bitwise_identical(cs):
 def test_randomised_configs_bitwise(cs, seed):
     """Randomised parity net: grid size, terrain/flow config, every physics switch (friction,
     transport, Shamov gate, slope term, Grass exponent, Eq.4 A_J, Exner sources), Courant
-    number, dry threshold, open edges, HGS, tile height and path -- status, dt log and
-    state bitwise equal to the oracle after 30 steps."""
+    number, dry threshold, open edges, HGS, tile height, path and grid spacing -- status, dt
+    log and state bitwise equal to the oracle after 30 steps."""
     rng = np.random.default_rng(1000 + seed)
     nx, ny = int(rng.integers(12, 300)), int(rng.integers(12, 260))
     name = ["C2", "C3", "C4", "C5"][int(rng.integers(0, 4))]
@@ -369,13 +369,16 @@ def test_randomised_configs_bitwise(cs, seed):
     open_bc = int(rng.integers(0, 16)) if rng.random() < 0.4 else 0
     walls = [2 if open_bc & m else 1 for m in (1, 2, 4, 8)]
     steps = 30
-    ref = oracle.Oracle(nx, ny, c.dx, oracle.Params(**ph))
+    # grid spacing: 1 m, or a non-unit h (lambda = tau/h, c_P = g/(4h), Eq.7's h and h^2, the
+    # Eq.2 slope) from a generator of its own, so the other draws of a seed are unchanged
+    dx = float(np.random.default_rng(5000 + seed).choice([1.0, 0.37, 2.5, 6.1]))
+    ref = oracle.Oracle(nx, ny, dx, oracle.Params(**ph))
     ref.set_walls(*walls)
     assert ref.set_state(*f) == 0
     st_ref, dt_ref, lim_ref = ref.step(steps)
     kw = dict(path=int(rng.integers(0, 2)), hgs=int(rng.integers(0, 2)),
               tile_rows=int(rng.choice([0, 16, 40])), open_bc=open_bc)
-    g = cs.csph_create(nx, ny, c.dx, cs.params_from(ph, **kw))
+    g = cs.csph_create(nx, ny, dx, cs.params_from(ph, **kw))
     g.set_state(*f)
     st = g.step(steps, check=False)
     dt, lim = g.get_dt_log(steps)
@@ -384,4 +387,4 @@ def test_randomised_configs_bitwise(cs, seed):
     assert st == st_ref, (ph, kw, st, st_ref)
     assert np.array_equal(dt, dt_ref) and np.array_equal(lim, lim_ref), (ph, kw)
     for a, r in zip(out, ref.get_state()):
-        assert np.array_equal(a, r), (ph, kw)
+        assert np.array_equal(a, r), (ph, kw, dx)
