@@ -173,3 +173,28 @@ def test_hll_sl_zero_takes_the_left_flux():
             SR = u + math.sqrt(G * H)
             seen_diff |= ((SR * m) * (1.0 / SR) != m) or ((SR * (m * u)) * (1.0 / SR) != m * u)
     assert seen_diff
+
+
+def test_hll_sr_zero_takes_the_right_flux():
+    """Reading #25: else S_R <= 0 -> F = F(q+) exactly, at S_R = 0 (u = -sqrt(g H) on both
+    sides, so S_L < 0 = S_R)."""
+    seen_diff = False
+    for H in (1.0, 0.37, 2.3, 0.9, 0.1507, 0.2055):
+        u = -math.sqrt(G * H)
+        for ut in (0.0, 0.4, -0.7):
+            F = oracle.hll_face(G, (H, H, u, ut), (H, H, u, ut))
+            m = H * u
+            assert F[0] == m and F[1] == m * u and F[2] == m * ut
+            SL = u - math.sqrt(G * H)
+            # the HLL average at S_R = 0: (-S_L F(q+)) / (0 - S_L)
+            seen_diff |= ((-SL * m) * (1.0 / -SL) != m) or ((-SL * (m * u)) * (1.0 / -SL) != m * u)
+    assert seen_diff
+
+
+def test_pow_pinned_range_edges():
+    """x^q closed forms at the edges of the pinned pow's range: 0^q = 0 for
+    q > 0 (also where q log2 of the scaled zero would stay in range), x^1 = x at the smallest
+    and largest binary exponents it returns (2^-1021, 2^1023)."""
+    assert oracle.pow_pinned(0.0, 0.5) == 0.0 and oracle.pow_pinned(0.0, 0.1) == 0.0
+    for e in (-1021, -1000, 1000, 1023):
+        assert oracle.pow_pinned(2.0 ** e, 1.0) == 2.0 ** e

@@ -148,8 +148,11 @@ def main():
     ap.add_argument("--limit", type=int, default=0)
     ap.add_argument("--kind", default="arithmetic,relational,boundary,index,constant")
     ap.add_argument("--list", action="store_true")
+    ap.add_argument("--grep", default="", help="only mutants whose name contains this")
     a = ap.parse_args()
     ms = mutants(set(a.kind.split(",")))
+    if a.grep:
+        ms = [m for m in ms if a.grep in m[0]]
     if a.limit:
         ms = ms[:a.limit]
     if a.list:
