@@ -4,6 +4,8 @@ csph_create_multi puts several strips on the same device and moves the 3 halo
 rows with cudaMemcpyPeerAsync; csph_create_dist with one rank exercises the NCCL
 communicator and the allreduce-max of the Eq.7 maxima.  Max is exact and
 order-free, so every decomposition must be bitwise equal to the single grid."""
+import os
+
 import numpy as np
 import pytest
 
@@ -353,3 +355,39 @@ def test_rebalance_dist_single_rank(cs):
     with pytest.raises(cs.CsphError):
         d.rebalance_rows([0, 2, c.ny])  # wrong rank count
     d.destroy()
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("CSPH_STRIP_SEEDS", "8"))))
+def test_randomised_strips_vs_oracle(cs, seed):
+    """Randomised strip net: 2-6 strips with random bounds (>= 3 rows each),
+    halo push or peer copies, automatic or fixed tile heights, HGS on/off, random config,
+    grid spacing and physics switches -- dt log and state bitwise the CPU oracle's after
+    40 steps."""
+    import oracle
+    rng = np.random.default_rng(7000 + seed)
+    nx, ny = int(rng.integers(20, 220)), int(rng.integers(30, 240))
+    name = ["C2", "C3", "C4", "C5"][int(rng.integers(0, 4))]
+    c = synth.config(name, nx, ny)
+    f = synth.fill(c)
+    ph = dict(c.params, C_J=float(rng.uniform(0.0, 3.0)), K=float(rng.uniform(0.15, 0.35)),
+              C_Sh=float(rng.choice([0.0, 4.0])), q_plus=float(rng.choice([0.0, 1e-6])))
+    dx = float(rng.choice([1.0, 0.6, 3.0]))
+    ns = int(rng.integers(2, 7))
+    while True:
+        cuts = sorted(rng.choice(np.arange(3, ny - 2), size=ns - 1, replace=False).tolist())
+        bounds = [0] + cuts + [ny]
+        if min(b - a for a, b in zip(bounds, bounds[1:])) >= 3:
+            break
+    kw = dict(halo_push=int(rng.integers(0, 2)), hgs=int(rng.integers(0, 2)),
+              tile_rows=int(rng.choice([0, 0, 16, 24])))
+    ref = oracle.Oracle(nx, ny, dx, oracle.Params(**ph))
+    assert ref.set_state(*f) == 0
+    st, dt0, lim0 = ref.step(40)
+    g = cs.csph_create_multi_rows(nx, ny, dx, cs.params_from(ph, **kw), [0] * ns, bounds)
+    g.set_state(*f)
+    assert g.step(40, check=False) == st
+    dt, lim = g.get_dt_log(40)
+    assert np.array_equal(dt, dt0) and np.array_equal(lim, lim0), (bounds, kw, dx)
+    for a, r in zip(g.get_state(), ref.get_state()):
+        assert np.array_equal(a, r), (bounds, kw, dx)
+    g.destroy()
