@@ -388,3 +388,43 @@ def test_randomised_configs_bitwise(cs, seed):
     assert np.array_equal(dt, dt_ref) and np.array_equal(lim, lim_ref), (ph, kw)
     for a, r in zip(out, ref.get_state()):
         assert np.array_equal(a, r), (ph, kw, dx)
+
+
+def _tie_states():
+    """Two states whose x-faces have u~_L + u~_R = 0 exactly (the sediment donor tie, reading
+    #25; the same constructions as tests/test_oracle_sweep_pins.py): a lake at rest along x
+    carrying a flow in y over an x-sloping bed (u~ = +0 on both sides, |J0| averaged with the
+    Eq.2 slope term), and a state mirror-symmetric about the face (2|3) with different y-flows
+    on the two sides (u~_L = -u~_R, J0x averaged)."""
+    ny = 4
+    b = np.tile(np.array([0.0, 0.1, 0.25, 0.3, 0.45, 0.5]), (ny, 1))
+    h = 1.2 - b
+    hv = h * np.tile(np.array([0.5, 0.7, 0.9, 1.1, 0.8, 0.6]), (ny, 1))
+    yield 2.5, (h, np.zeros_like(h), hv, b, np.full_like(h, 0.4))
+    ny = 3
+    rows = [np.array(r) for r in ([0.8, 1.0, 1.1, 1.1, 1.0, 0.8], [0.3, 0.2, 0.1, 0.1, 0.2, 0.3],
+                                  [0.1, 0.3, 0.4, -0.4, -0.3, -0.1],
+                                  [0.2, 0.3, 0.5, 0.1, 0.0, -0.2])]
+    h, b, hu, hv = (np.tile(r, (ny, 1)) for r in rows)
+    yield 1.0, (h, hu, hv, b, np.full_like(h, 0.4))
+
+
+@pytest.mark.parametrize("path", ["fused", "staged"])
+def test_sediment_donor_tie_bitwise(cs, path):
+    """The donor tie of the sediment face flux on the GPU: 1 and 5 steps bitwise the oracle's
+    (the first step ties exactly; a 0.25 average or a wrong side would change b')."""
+    ph = dict(A_J=0.01, C_J=2.0, C_Sh=0.0, n_manning=0.0)
+    for dx, f in _tie_states():
+        ny, nx = f[0].shape
+        for steps in (1, 5):
+            ref = oracle.Oracle(nx, ny, dx, oracle.Params(**ph))
+            assert ref.set_state(*f) == 0
+            st, dt0, _ = ref.step(steps)
+            assert st == 0
+            g = cs.csph_create(nx, ny, dx, cs.params_from(ph, path=PATHS[path]))
+            g.set_state(*f)
+            g.step(steps)
+            assert np.array_equal(g.get_dt_log(steps)[0], dt0)
+            for a, r in zip(g.get_state(), ref.get_state()):
+                assert np.array_equal(a, r)
+            g.destroy()
