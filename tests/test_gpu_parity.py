@@ -428,3 +428,40 @@ def test_sediment_donor_tie_bitwise(cs, path):
             for a, r in zip(g.get_state(), ref.get_state()):
                 assert np.array_equal(a, r)
             g.destroy()
+
+
+@pytest.mark.parametrize("case", ["t1=t2", "t2=t3", "t3 at h=2"])
+def test_eq7_limiters_on_device(cs, case):
+    """Eq.7 ties on the device (reading #25: the lower limiter index wins), with g = 4 so that
+    sqrt(gH) is exact: t1 = t2 for a uniform H = 1, u = 2 flow (|u| = c = 2: M1 = 4, M2 = 4,
+    h/(2 sqrt M1) = h/M2 = 1/4); t2 = t3 < t1 for still water of depth 4 (c = 4: M2 = 4) beside
+    a 1 m deep flow at u = 1 with A_J = 2, psi = 0 (M1 = 1, M3 = A |u|^3 = 2: t2 = t3 = 1/4,
+    t1 = 1/2); and the bed term binding on a 2 m grid (H = 1, u = 1, A_J = 10: t1 = 1, t2 = 2/3,
+    t3 = h^2/(2 M3) = 4/20).  The device's first tau and limiter equal the oracle's and the
+    closed form."""
+    n, dx, tau_want = 4, 1.0, 0.25 * 0.25
+    if case == "t3 at h=2":
+        h = np.ones((n, n)); hu = np.ones((n, n))
+        ph = dict(g=4.0, K=0.25, A_J=10.0, C_J=0.0, C_Sh=0.0)
+        lim_want, dx, tau_want = 2, 2.0, 0.25 * (4.0 / 20.0)
+    elif case == "t1=t2":
+        h = np.ones((n, n)); hu = 2.0 * h
+        ph = dict(g=4.0, K=0.25, A_J=0.0)
+        lim_want = 0
+    else:
+        h = np.ones((n, n)); h[:, : n // 2] = 4.0
+        hu = np.zeros((n, n)); hu[:, n // 2:] = 1.0
+        ph = dict(g=4.0, K=0.25, A_J=2.0, C_J=0.0, C_Sh=0.0)
+        lim_want = 1
+    f = (h, hu, np.zeros((n, n)), np.zeros((n, n)), np.zeros((n, n)))
+    ref = oracle.Oracle(n, n, dx, oracle.Params(**ph))
+    assert ref.set_state(*f) == 0
+    st, dt0, lim0 = ref.step(1)
+    assert st == 0 and lim0[0] == lim_want and dt0[0] == tau_want
+    for path in (0, 1):
+        g = cs.csph_create(n, n, dx, cs.params_from(ph, path=path))
+        g.set_state(*f)
+        g.step(1)
+        dt, lim = g.get_dt_log(1)
+        assert dt[0] == dt0[0] and lim[0] == lim_want, (path, dt, lim)
+        g.destroy()

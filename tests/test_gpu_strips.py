@@ -173,14 +173,18 @@ def test_dist_split_launches(cs, tile_rows):
     g.destroy()
 
 
+@pytest.mark.parametrize("up", [False, True])
 @pytest.mark.parametrize("push", [1, 0])
 @pytest.mark.parametrize("nstrips", [2, 4])
-def test_front_crosses_strip_edges_hgs(cs, nstrips, push):
+def test_front_crosses_strip_edges_hgs(cs, nstrips, push, up):
     """HGS across strip edges (ghost tile flags): a dam-break front starts
-    in the first strip and runs into dry strips whose edge tiles were being skipped; with
-    16-row tiles and uneven strips the result is bitwise the single grid without HGS."""
+    in the first (up: the last) strip and runs into dry strips whose edge tiles were being
+    skipped -- so both ghost-flag rows of a strip (facing the strip below and above) decide;
+    with 16-row tiles and uneven strips the result is bitwise the single grid without HGS."""
     nx, ny = 150, 180
     jj, ii = np.mgrid[0:ny, 0:nx]
+    if up:
+        jj = ny - 1 - jj
     h = np.where(jj < 30, 1.5, 0.0)
     b = 0.4 - 0.002 * jj + 0.01 * np.sin(0.2 * ii)  # downhill, away from the dam
     z = np.zeros((ny, nx))
@@ -200,7 +204,8 @@ def test_front_crosses_strip_edges_hgs(cs, nstrips, push):
     assert np.array_equal(g.get_dt_log(steps)[0], dt0)
     for a, r in zip(g.get_state(), ref):
         assert np.array_equal(a, r)
-    assert ref[0][76:].max() > 0  # the front crossed the strip edges at rows 37/41 and 70
+    # the front crossed the strip edges at rows 37/41 and 70 (up: 131 and 70)
+    assert (ref[0][:104] if up else ref[0][76:]).max() > 0
     g.destroy()
 
 

@@ -62,6 +62,34 @@ MUTANTS = [
     ("K4: theta -> tau (control)", "csph_fused.cu", "fma(-theta, div, T(1))",
      "fma(-tau, div, T(1))", 0),
     ("fp32 icbrt seed", "csph_real.cuh", "0x54A2FA8C", "0x54A2FA9C", 0),
+    # ---- second batch: the ctrl kernel, open edges, NEXT-3 fields, strips, math recipes
+    ("ctrl Eq.7: t2 tie to t2", "csph_api.cu", "if (t2 < m) { m = t2; lim = 1; }",
+     "if (t2 <= m) { m = t2; lim = 1; }", 0),
+    ("ctrl Eq.7: t3 tie to t3", "csph_api.cu", "if (t3 < m) { m = t3; lim = 2; }",
+     "if (t3 <= m) { m = t3; lim = 2; }", 0),
+    ("ctrl Eq.7: h^2 -> h/h", "csph_api.cu", "double t3 = (h * h) / (2.0 * M[2]);",
+     "double t3 = (h / h) / (2.0 * M[2]);", 0),
+    ("peer combine: min instead of max", "csph_api.cu",
+     "m[k] = e[k] > m[k] ? e[k] : m[k];", "m[k] = e[k] > m[k] ? m[k] : e[k];", 0),
+    ("open lo edge: ghost negated", "csph_internal.cuh",
+     "for (int g = 1; g <= 3; ++g) { t[k] = -g; neg[k++] = false; }",
+     "for (int g = 1; g <= 3; ++g) { t[k] = -g; neg[k++] = true; }", 0),
+    ("open hi edge: 2 ghost layers", "csph_internal.cuh",
+     "for (int g = 0; g < 3; ++g) { t[k] = n + g; neg[k++] = false; }",
+     "for (int g = 0; g < 2; ++g) { t[k] = n + g; neg[k++] = false; }", 0),
+    ("NEXT-3 source sign", "csph_internal.cuh", "Hn = (Hn + tau * S.src[c]) * a;",
+     "Hn = (Hn - tau * S.src[c]) * a;", 0),
+    ("NEXT-3 friction field row", "csph_fused.cu", "S.cg[fidx(col, L)]", "S.cg[fidx(col, L - 1)]", 0),
+    ("HGS ghost flag slot", "csph_fused.cu", "S.ngflag[0][g + hg.ntx] = (unsigned char)m;",
+     "S.ngflag[0][g] = (unsigned char)m;", 0),
+    ("rcp all-ones fix dropped", "csph_internal.cuh", "| (ones == 0xFFFFFFFFu))", "| 0u)", 0),
+    ("icbrt 4 Newton steps", "csph_internal.cuh", "for (int k = 0; k < 5; ++k) {",
+     "for (int k = 0; k < 4; ++k) {", 0),
+    ("sediment slope: * inv_h -> / inv_h", "csph_real.cuh", "(bR - bL) * P.inv_h",
+     "(bR - bL) / P.inv_h", 0),
+    ("K8 bed: lam -> tau", "csph_fused.cu",
+     "const T bn = fma(-(lam * W3), dJ, b3) + (tau * W3) * Q.src;",
+     "const T bn = fma(-(tau * W3), dJ, b3) + (tau * W3) * Q.src;", 1),
 ]
 
 GPU_TESTS = ["tests/test_gpu_parity.py", "tests/test_gpu_strips.py", "tests/test_gpu_fp32.py",
@@ -97,8 +125,10 @@ def cmd_build():
     from paper_2103_15196_b200 import build
     build.build()
     shutil.copy2(SO, os.path.join(VAR, "kmut_base.so"))
+    only = {int(x) for x in sys.argv[2].split(",")} if len(sys.argv) > 2 else None
     with cf.ThreadPoolExecutor(4) as ex:
-        futs = [ex.submit(build_one, i, *m) for i, m in enumerate(MUTANTS)]
+        futs = [ex.submit(build_one, i, *m) for i, m in enumerate(MUTANTS)
+                if only is None or i in only]
         for f in futs:
             print("%-45s %s" % f.result(), flush=True)
 
