@@ -396,3 +396,41 @@ def test_randomised_strips_vs_oracle(cs, seed):
     for a, r in zip(g.get_state(), ref.get_state()):
         assert np.array_equal(a, r), (bounds, kw, dx)
     g.destroy()
+
+
+def test_ghost_flag_rows_are_per_side(cs):
+    """Each strip's two ghost-flag rows carry the facing tile row of the
+    right neighbour: strip 1 (two 16-row tile rows, dry) sits between strip 0, whose dam-break
+    front reaches its last row after a few steps (water then about to enter strip 1 from
+    below), and strip 2, wet inside its first tile row but not at its ends (a slower tile
+    whose flags have no BOT band).  Both transports; bitwise the single grid without HGS.
+    (A mutant that writes strip 2's flags into strip 1's lower ghost row instead of strip
+    0's upper one was not caught by this either: profiles/r02_kernel_mutations.txt.)"""
+    nx, ny = 120, 128
+    jj, ii = np.mgrid[0:ny, 0:nx]
+    h = np.zeros((ny, nx))
+    h[30:41, :] = 0.6  # strip 0's reservoir: its front reaches the strip edge after some steps
+    h[81:95, :] = 0.8
+    b = 0.5 - 0.004 * jj + 0.01 * np.sin(0.3 * ii)
+    b[81:95, :] = 0.5 - 0.004 * 96  # strip 2's pool on a flat shelf between two bed walls,
+    b[80, :] = b[95, :] = 2.0       # so its first tile row stays wet inside, dry at both ends
+    z = np.zeros((ny, nx))
+    f = (h, z.copy(), z.copy(), b, np.full((ny, nx), 0.4))
+    phys = dict(n_manning=0.02, A_J=1e-3, C_J=1.0, C_Sh=0.0)
+    steps = 120
+    g = cs.csph_create(nx, ny, 1.0, cs.params_from(phys, hgs=0))
+    g.set_state(*f)
+    g.step(steps)
+    dt0, ref = g.get_dt_log(steps)[0], g.get_state()
+    g.destroy()
+    assert ref[0][48:56].max() > 1e-3  # water entered strip 1's first tile row
+    for push in (1, 0):
+        g = cs.csph_create_multi_rows(nx, ny, 1.0, cs.params_from(phys, tile_rows=16,
+                                                                  halo_push=push),
+                                      [0] * 3, [0, 48, 80, ny])
+        g.set_state(*f)
+        g.step(steps)
+        assert np.array_equal(g.get_dt_log(steps)[0], dt0), push
+        for a, r in zip(g.get_state(), ref):
+            assert np.array_equal(a, r), push
+        g.destroy()
