@@ -404,8 +404,9 @@ def test_ghost_flag_rows_are_per_side(cs):
     front reaches its last row after a few steps (water then about to enter strip 1 from
     below), and strip 2, wet inside its first tile row but not at its ends (a slower tile
     whose flags have no BOT band).  Both transports; bitwise the single grid without HGS.
-    (A mutant that writes strip 2's flags into strip 1's lower ghost row instead of strip
-    0's upper one was not caught by this either: profiles/r02_kernel_mutations.txt.)"""
+    Stepped one step per call, so that the three strips' kernels start together: a mutant
+    writing strip 2's flags into strip 1's lower ghost row (racing with strip 0's correct
+    write) then shows (profiles/r02_kernel_mutations.txt)."""
     nx, ny = 120, 128
     jj, ii = np.mgrid[0:ny, 0:nx]
     h = np.zeros((ny, nx))
@@ -429,7 +430,8 @@ def test_ghost_flag_rows_are_per_side(cs):
                                                                   halo_push=push),
                                       [0] * 3, [0, 48, 80, ny])
         g.set_state(*f)
-        g.step(steps)
+        for _ in range(steps):  # one step per call: the strips' kernels start together
+            g.step(1)
         assert np.array_equal(g.get_dt_log(steps)[0], dt0), push
         for a, r in zip(g.get_state(), ref):
             assert np.array_equal(a, r), push
