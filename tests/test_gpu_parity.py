@@ -56,7 +56,7 @@ def assert_parity(gpu, ref, tol=1e-9, bitwise=True):
     assert np.array_equal(lim, lim_r)
     errs = parity_err(out, out_r)
     assert max(errs) <= tol, errs
-    assert tg[1] == tr[1]
+    assert tg[1] == tr[1] and tg[0] == tr[0] and tg[2] == tr[2]  # steps, time = sum of tau, last tau
     if bitwise:
         for a, r in zip(out, out_r):
             assert np.array_equal(a, r)
@@ -383,8 +383,10 @@ def test_randomised_configs_bitwise(cs, seed):
     st = g.step(steps, check=False)
     dt, lim = g.get_dt_log(steps)
     out = g.get_state()
+    tg = g.get_time()
     g.destroy()
     assert st == st_ref, (ph, kw, st, st_ref)
+    assert tg == ref.time(), (tg, ref.time())  # steps done, sum of tau, last tau
     assert np.array_equal(dt, dt_ref) and np.array_equal(lim, lim_ref), (ph, kw)
     for a, r in zip(out, ref.get_state()):
         assert np.array_equal(a, r), (ph, kw, dx)

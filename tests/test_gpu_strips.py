@@ -396,6 +396,7 @@ def test_randomised_strips_vs_oracle(cs, seed):
         code = g.step(k, check=False)
         done += k
     assert code == st
+    assert g.get_time() == ref.time()  # steps done, sum of tau, last tau
     dt, lim = g.get_dt_log(40)
     assert np.array_equal(dt, dt0) and np.array_equal(lim, lim0), (bounds, kw, dx)
     for a, r in zip(g.get_state(), ref.get_state()):

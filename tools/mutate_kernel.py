@@ -90,10 +90,29 @@ MUTANTS = [
     ("K8 bed: lam -> tau", "csph_fused.cu",
      "const T bn = fma(-(lam * W3), dJ, b3) + (tau * W3) * Q.src;",
      "const T bn = fma(-(tau * W3), dJ, b3) + (tau * W3) * Q.src;", 1),
+    # ---- third batch: host / service logic of csph_api.cu
+    ("ctrl: simulated time not accumulated", "csph_api.cu", "C->t += C->tau;", "C->t = C->tau;", 0),
+    ("dt log ring: off by one", "csph_api.cu", "long long first = (done - m) % LOGCAP;",
+     "long long first = (done - m + 1) % LOGCAP;", 0),
+    ("peer-copy halo: send_hi row", "csph_api.cu", "m.send_hi = off(v.pitch, -GX, v.ny - GY);",
+     "m.send_hi = off(v.pitch, -GX, v.ny - GY + 1);", 0),
+    ("peer-copy flags: hi into lo slot", "csph_api.cu", "m.frecv_hi = m.frecv_lo + s.ntx;",
+     "m.frecv_hi = m.frecv_lo;", 0),
+    ("get_state_rows: row offset", "csph_api.cu", "sk + off(v.pitch, 0, lo - s.gj0), (size_t)v.pitch * 8,",
+     "sk + off(v.pitch, 0, lo - s.gj0 + 1), (size_t)v.pitch * 8,", 0),
+    ("set_state: upper halo rows", "csph_api.cu", "int hi = s.gj0 + v.ny + (v.wall_hi ? 0 : GY);",
+     "int hi = s.gj0 + v.ny + (v.wall_hi ? 0 : GY - 1);", 0),
+    ("save: owned-row offset", "csph_api.cu", "dst[k] + (size_t)s.gj0 * H->nx,", "dst[k],", 0),
+    ("validate: psi = 1 accepted", "csph_api.cu", "if (!(p >= 0.0 && p < 1.0)) f |= 4;",
+     "if (!(p >= 0.0 && p <= 1.0)) f |= 4;", 0),
+    ("validate: negative depth accepted", "csph_api.cu", "if (H < 0.0) f |= 2;",
+     "if (H < -1.0) f |= 2;", 0),
+    ("W = 1/(1-psi) -> 1/(1+psi)", "csph_api.cu", "W[k] = 1.0 / (1.0 - psi[k]);",
+     "W[k] = 1.0 / (1.0 + psi[k]);", 0),
 ]
 
 GPU_TESTS = ["tests/test_gpu_parity.py", "tests/test_gpu_strips.py", "tests/test_gpu_fp32.py",
-             "tests/test_next3_fields.py", "tests/test_next4_closures.py"]
+             "tests/test_next3_fields.py", "tests/test_next4_closures.py", "tests/test_gpu_save.py"]
 
 
 def build_one(i, name, fname, old, new, occ):
