@@ -1655,9 +1655,9 @@ static int choose_tile_rows(csph* H, Strip& s, int buf = 0) {
   const int nby = (s.v.ny + kTyMin - 1) / kTyMin;
   dim3 grd((unsigned)s.ntx, (unsigned)nby);
   if (s.v.prec == 4)
-    wet_blocks_kernel<float><<<grd, 128, 0, s.st>>>(s.v, H->P.eps, s.wetblk, buf);
+    wet_blocks_kernel<float><<<grd, FUSED_NT, 0, s.st>>>(s.v, H->P.eps, s.wetblk, buf);
   else
-    wet_blocks_kernel<double><<<grd, 128, 0, s.st>>>(s.v, H->P.eps, s.wetblk, buf);
+    wet_blocks_kernel<double><<<grd, FUSED_NT, 0, s.st>>>(s.v, H->P.eps, s.wetblk, buf);
   H->launches += 1;
   CK(cudaGetLastError());
   std::vector<unsigned char> w((size_t)s.ntx * nby);

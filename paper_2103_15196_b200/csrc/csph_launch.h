@@ -52,6 +52,7 @@ struct Hgs {
 constexpr int FUSED_NT = CSPH_NT;
 constexpr int FUSED_TX = CSPH_NT - 8;  // output columns per CTA of the fused kernel (NT - 8)
 constexpr int FUSED_MINB = CSPH_MINB;
+static_assert(FUSED_NT % 32 == 0 && FUSED_NT >= 64 && FUSED_NT <= 1024, "CTA width: whole warps");
 
 // Fused y-marching step (csph_fused.cu). Rows [row0, row1) of the strip; row0 must be
 // a multiple of tile_rows when HGS is enabled.
