@@ -142,6 +142,46 @@ def test_C5_full_size_cones_vs_oracle(cs):
     g.destroy()
 
 
+def test_C5_full_size_fp32_cones_vs_binary32_oracle(cs):
+    """NEXT-2 at the bench's size: the fp32 mode on C5 16384^2 (the `bench.py --precision 32`
+    configuration) against the binary32 oracle (reading #33) on the dependency cones of 48^2
+    patches (wall corners, wet/dry fronts, random) after 20 and 100 steps, replaying the
+    GPU's tau log -- bitwise."""
+    c = synth.config("C5")
+    P = oracle.Params(**c.params)
+    f = synth.fill(c)
+    h, hu, hv, b, psi = f
+    g = cs.csph_create(c.nx, c.ny, c.dx, cs.params_from(c.params, precision=32))
+    g.set_state(*f)
+    size = 48
+    W = 1.0 / (1.0 - psi)  # rounded to binary32 by the oracle as by the library
+    rng = np.random.default_rng(2104)
+    patches = _patches(h > P.eps_dry, 4, rng, size)
+    done = 0
+    for k in (20, 100):
+        g.step(k - done)
+        done = k
+        dt, _ = g.get_dt_log(k)
+        assert len(dt) == k
+        m = 3 * k
+        for (pi, pj) in patches:
+            i0, i1 = max(0, pi - m), min(c.nx, pi + size + m)
+            j0, j1 = max(0, pj - m), min(c.ny, pj + size + m)
+            o = oracle.Oracle(i1 - i0, j1 - j0, c.dx, P, precision=32)
+            o.set_walls(i0 == 0, i1 == c.nx, j0 == 0, j1 == c.ny)
+            assert o.set_state_padded(*[_window(a, i0, i1, j0, j1, 0.0) for a in (h, hu, hv, b)],
+                                      _window(W, i0, i1, j0, j1, 1.0)) == 0
+            for tau in dt:
+                assert o.step_tau(float(tau)) == 0
+            ref = o.get_state()
+            got = g.get_state_rows(pj, pj + size)
+            for a, r in zip(got, ref):
+                assert np.array_equal(a[:, pi:pi + size],
+                                      r[pj - j0:pj - j0 + size, pi - i0:pi - i0 + size]), (k, pi, pj)
+            del o
+    g.destroy()
+
+
 def test_C5_full_size_hgs_and_conservation(cs):
     c = synth.config("C5")
     f = synth.fill(c)
