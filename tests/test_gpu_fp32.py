@@ -3,6 +3,7 @@ at 1e-4 after 100 steps (north_star's bar for the optional fp32 mode).  The fp32
 dt sequence is its own (computed from fp32 state), so the comparison is at equal
 step counts with the simulated times checked to agree closely."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -143,3 +144,42 @@ def test_fp32_bitwise_non_unit_spacing(cs, dx):
     for a, r in zip(g.get_state(), ref.get_state()):
         assert np.array_equal(a, r)
     g.destroy()
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("CSPH_RAND32_SEEDS", "12"))))
+def test_fp32_randomised_bitwise(cs, seed):
+    """Randomised net of the fp32 mode (within its scope: walls, m = 2, constant A_J, no
+    fields): grid size, config, grid spacing, physics switches, Courant number, dry
+    threshold, HGS and tile height -- dt log and state bitwise the binary32 oracle's after
+    30 steps (reading #33)."""
+    rng = np.random.default_rng(9000 + seed)
+    nx, ny = int(rng.integers(12, 300)), int(rng.integers(12, 260))
+    name = ["C2", "C3", "C4", "C5"][int(rng.integers(0, 4))]
+    c = synth.config(name, nx, ny)
+    f = synth.fill(c)
+    ph = dict(
+        n_manning=float(rng.choice([0.0, rng.uniform(0.01, 0.05)])),
+        A_J=float(rng.choice([0.0, rng.uniform(1e-4, 3e-3)])),
+        C_J=float(rng.uniform(0.0, 3.0)),
+        C_Sh=float(rng.choice([0.0, rng.uniform(2.0, 6.0)])),
+        d50=float(rng.uniform(5e-4, 2e-3)),
+        K=float(rng.uniform(0.1, 0.4)),
+        eps_dry=float(rng.choice([1e-6, 1e-4])),
+        q_plus=float(rng.choice([0.0, 0.0, 1e-6])),
+    )
+    dx = float(rng.choice([1.0, 0.37, 2.5]))
+    steps = 30
+    ref = oracle.Oracle(nx, ny, dx, oracle.Params(**ph), precision=32)
+    assert ref.set_state(*f) == 0
+    st_ref, dt_ref, lim_ref = ref.step(steps)
+    kw = dict(precision=32, hgs=int(rng.integers(0, 2)), tile_rows=int(rng.choice([0, 16, 40])))
+    g = cs.csph_create(nx, ny, dx, cs.params_from(ph, **kw))
+    g.set_state(*f)
+    st = g.step(steps, check=False)
+    dt, lim = g.get_dt_log(steps)
+    out = g.get_state()
+    g.destroy()
+    assert st == st_ref, (ph, kw, st, st_ref)
+    assert np.array_equal(dt, dt_ref) and np.array_equal(lim, lim_ref), (ph, kw, dx)
+    for a, r in zip(out, ref.get_state()):
+        assert np.array_equal(a, r), (ph, kw, dx)
