@@ -9,7 +9,7 @@ c = synth.config(os.environ.get("CFG", "C5"))
 f = synth.fill(c)
 W = 1.0 / (1.0 - f[4])
 vol0, sed0 = float(np.sum(f[0])), float(np.sum(f[3] / W))
-g = csph.csph_create(c.nx, c.ny, c.dx, csph.params_from(c.params))
+g = csph.csph_create(c.nx, c.ny, c.dx, csph.params_from(c.params, precision=int(os.environ.get("PREC", "64"))))
 g.set_state(*f)
 del f
 steps, chunk = int(os.environ.get("STEPS", "3000")), 500
